@@ -1,0 +1,164 @@
+/*
+ * exageo.h -- C ABI of the B200-native exact Gaussian log-likelihood library
+ * (hot path of ExaGeoStat, arXiv 1708.02835). libexageo.so implements every
+ * function declared here; the Python binding paper_1708_02835_b200 mirrors the
+ * names one to one.
+ *
+ * Citations: "P:<line>" = PAPER.md line of arXiv 1708.02835 (LaTeX text);
+ * "R<k>" = reading k in DESIGN.md (where the paper is silent or garbled).
+ *
+ * Conventions (all functions):
+ *   - Plain pointers and sizes only. Unless a name ends in _dev, array
+ *     arguments are HOST pointers owned by the caller; the library copies them.
+ *     *_dev functions take DEVICE pointers on the context's device and enqueue
+ *     work on the context's stream (they synchronise only where they return a
+ *     host scalar, as documented).
+ *   - Matrices are column-major with an explicit leading dimension.
+ *   - Every function returns an exageo_status; nothing aborts the process.
+ *     On failure, exageo_last_error(ctx) describes the cause.
+ *   - theta = (theta1, theta2, theta3) = (variance, range, smoothness) of the
+ *     Matern covariance Eq. (2); each must be finite and > 0,
+ *     otherwise EXAGEO_EINVAL.
+ *   - The library never falls back to a CPU implementation: without a usable
+ *     CUDA device, context creation fails with EXAGEO_ECUDA.
+ */
+#ifndef EXAGEO_H
+#define EXAGEO_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Matern parameter vector theta. */
+typedef struct {
+  double sigma2; /* theta1 > 0: variance              */
+  double beta;   /* theta2 > 0: spatial range          */
+  double nu;     /* theta3 > 0: smoothness             */
+} exageo_theta;
+
+typedef enum {
+  EXAGEO_OK = 0,
+  EXAGEO_EINVAL = -1,  /* invalid argument (theta <= 0 / non-finite, n < 1, NULL, bad ld) */
+  EXAGEO_ENOTPD = -2,  /* Sigma(theta) not positive definite; info.npd_pivot = global pivot */
+  EXAGEO_ENOMEM = -3,  /* tile workspace does not fit in device memory                      */
+  EXAGEO_ECUDA = -4,   /* CUDA runtime error (no device, launch failure, ...)                */
+  EXAGEO_ENCCL = -5,   /* reserved: collective failure (multi-GPU)                           */
+  EXAGEO_EFIT = -6     /* reserved: every optimizer evaluation failed (exageo_mle)           */
+} exageo_status;
+
+/* Opaque context: device, stream, tile workspace (panel layout, DESIGN.md
+ * "Data layout"), per-step events. Not thread-safe; one per device/stream. */
+typedef struct exageo_ctx exageo_ctx;
+
+typedef struct {
+  int device;   /* CUDA device ordinal                                               */
+  int nb;       /* tile size (multiple of 128); 0 = automatic (512 for n >= 10000, else 128/256) */
+  void* stream; /* cudaStream_t to run on; NULL = the library creates its own stream */
+} exageo_opts;
+
+/* Per-evaluation details of exageo_loglik*. */
+typedef struct {
+  double loglik;      /* l(theta), Eq. (1)                                   */
+  double logdet;      /* log|Sigma| = 2 sum log L_ii (R5)                    */
+  double quad;        /* z^T Sigma^{-1} z = ||L^{-1} z||^2 (R6, R7)          */
+  int64_t npd_pivot;  /* -1, or the 0-based global index of the first non-positive pivot */
+  int64_t n, nb, ntiles; /* problem size, tile size, T = ceil(n/nb)           */
+  double flops;       /* n^3/3 Cholesky flop count used for TFLOP/s */
+  double ms_total;    /* device time of the whole evaluation (CUDA events)    */
+  double ms_gen;      /* device time of the covariance generation (Alg. 2 l.2) */
+  double ms_chol;     /* device time of factorization + fused forward solve   */
+  double ms_reduce;   /* device time of the log-det / dot reduction            */
+  int64_t kernels;    /* number of kernel launches this evaluation issued     */
+} exageo_loglik_info;
+
+/* Human-readable name of a status. Never NULL. */
+const char* exageo_strerror(exageo_status s);
+
+/* Message of the most recent failure on ctx (or of the last context creation
+ * when ctx is NULL). Valid until the next call on ctx. Never NULL. */
+const char* exageo_last_error(const exageo_ctx* ctx);
+
+/* Create a context on opts->device. opts may be NULL (device 0, automatic nb,
+ * own stream). Fails with EXAGEO_ECUDA if no CUDA device is usable. */
+exageo_status exageo_create(exageo_ctx** ctx, const exageo_opts* opts);
+void exageo_destroy(exageo_ctx* ctx);
+
+/* Bytes of device workspace exageo_loglik needs for n locations with tile
+ * size nb (0 = automatic): 8 * nb * sum_j (N - j*nb + 128), N = T*nb
+ * (lower block-column panels plus the z row block). */
+size_t exageo_workspace_bytes(int64_t n, int nb);
+
+/* Hand the context a caller-owned device buffer (e.g. a torch tensor) to use
+ * as tile workspace; it must stay alive while the context uses it. ptr = NULL
+ * returns to library-managed allocation. */
+exageo_status exageo_set_workspace(exageo_ctx* ctx, void* ptr, size_t bytes);
+
+/* Jittered-grid locations (Sec. 7.1; R1-R3):
+ *   s_q = ((r - 0.5 + X_rl)/g, (l - 0.5 + Y_rl)/g), g = ceil(sqrt n),
+ *   X, Y ~ U(-0.4, 0.4) from counter-based SplitMix64 streams; for non-square
+ *   n the n grid cells with the smallest SplitMix64 keys are kept, in
+ *   row-major cell order. Integer RNG + IEEE arithmetic without contraction:
+ *   bit-exact across platforms. x, y: host arrays of n doubles (caller-owned).
+ * Computed on the host (input preparation, not the timed path). */
+exageo_status exageo_gen_locations(int64_t n, uint64_t seed, double* x, double* y);
+
+/* Dense Matern covariance block, Eq. (2) (Alg. 3 l.3-6):
+ *   C[i + j*ldc] = C(||s1_i - s2_j||; theta), 0 <= i < m, 0 <= j < n,
+ * with C(0) = theta1 (R9). Host arrays x1,y1 (m), x2,y2 (n), C (ldc*n,
+ * ldc >= m). Computed on the GPU by the same device evaluator as the tile
+ * generator. */
+exageo_status exageo_matern_cov(exageo_ctx* ctx, const exageo_theta* theta, int64_t m, const double* x1,
+                                const double* y1, int64_t n, const double* x2, const double* y2, double* C,
+                                int64_t ldc);
+
+/* Exact Gaussian log-likelihood, Eq. (1) by Alg. 2:
+ *   Sigma = genCovMatrix(theta); Sigma = L L^T; y = L^{-1} z;
+ *   l = -0.5 y^T y - 0.5 (2 sum log L_ii) - (n/2) log(2 pi).
+ * x, y, z: host arrays of n doubles. On success *loglik is set; info (may be
+ * NULL) receives the details. Not positive definite -> EXAGEO_ENOTPD with
+ * info->npd_pivot set and *loglik = -inf. Host<->device copies included. */
+exageo_status exageo_loglik(exageo_ctx* ctx, const exageo_theta* theta, int64_t n, const double* x,
+                            const double* y, const double* z, double* loglik, exageo_loglik_info* info);
+
+/* Same as exageo_loglik with DEVICE arrays x_d, y_d, z_d (n doubles each) on
+ * the context's device. Enqueued on the context stream; returns after the
+ * 32-byte result has been copied back (the only synchronisation). */
+exageo_status exageo_loglik_dev(exageo_ctx* ctx, const exageo_theta* theta, int64_t n, const double* x_d,
+                                const double* y_d, const double* z_d, double* loglik,
+                                exageo_loglik_info* info);
+
+/* Synthetic data generator, Alg. 1 (R18): z = L e with
+ * Sigma(theta) = L L^T. The normal variates e (n doubles, host) are an input.
+ * Writes z (n doubles, host). Non-PD -> EXAGEO_ENOTPD. */
+exageo_status exageo_simulate(exageo_ctx* ctx, const exageo_theta* theta, int64_t n, const double* x,
+                              const double* y, const double* e, double* z);
+
+/* --- Stage-level entry points (same kernels as exageo_loglik_dev, exposed
+ *     so that each step of Alg. 2 can be checked on its own). ---------- */
+
+/* Alg. 2 l.2: generate Sigma(theta) into the workspace (lower panels, identity
+ * padding, z in the z row block). Device arrays. Enqueued, no sync. */
+exageo_status exageo_stage_generate_dev(exageo_ctx* ctx, const exageo_theta* theta, int64_t n, const double* x_d,
+                                        const double* y_d, const double* z_d);
+/* Alg. 2 l.3-4: factor the workspace in place (Sigma -> L) with the fused
+ * forward solve of the z row (y = L^{-1} z). Enqueued, no sync. */
+exageo_status exageo_stage_factor(exageo_ctx* ctx);
+/* Alg. 2 l.5-7: reductions; synchronises and writes out[3] =
+ * {loglik, logdet, quad} (host) and *npd_pivot (host, may be NULL). */
+exageo_status exageo_stage_finish(exageo_ctx* ctx, double* out3, int64_t* npd_pivot);
+/* Copy the lower triangle (incl. diagonal) of the current workspace matrix
+ * (Sigma after generate, L after factor) to host dense column-major
+ * dst[i + j*ld], 0 <= j <= i < n; the strict upper triangle of dst is not
+ * written. Synchronises. */
+exageo_status exageo_read_lower(exageo_ctx* ctx, double* dst, int64_t ld);
+/* Copy the current z row (z after generate, y = L^{-1} z after factor) to the
+ * host array dst (n doubles). Synchronises. */
+exageo_status exageo_read_zrow(exageo_ctx* ctx, double* dst);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EXAGEO_H */

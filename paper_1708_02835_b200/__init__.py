@@ -1,0 +1,268 @@
+"""paper_1708_02835_b200 -- B200-native exact Gaussian log-likelihood (ExaGeoStat hot path).
+
+Thin ctypes binding over the C ABI in ``include/exageo.h`` (libexageo.so, built
+in-tree by ``paper_1708_02835_b200.build``). The functions keep the C names
+without the ``exageo_`` prefix and do argument marshalling only: every step of
+the evaluation runs in the library's CUDA kernels. There is no CPU fallback --
+if the shared library is missing or no CUDA device is usable, the calls raise.
+
+Host arrays are numpy float64; the ``*_dev`` variants take torch CUDA float64
+tensors (torch is used only for device memory and streams).
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_lib", "libexageo.so")
+
+OK, EINVAL, ENOTPD, ENOMEM, ECUDA, ENCCL, EFIT = 0, -1, -2, -3, -4, -5, -6
+
+_f64p = ctypes.POINTER(ctypes.c_double)
+_i64p = ctypes.POINTER(ctypes.c_int64)
+
+
+class Theta(ctypes.Structure):
+    _fields_ = [("sigma2", ctypes.c_double), ("beta", ctypes.c_double), ("nu", ctypes.c_double)]
+
+
+class Opts(ctypes.Structure):
+    _fields_ = [("device", ctypes.c_int), ("nb", ctypes.c_int), ("stream", ctypes.c_void_p)]
+
+
+class LoglikInfo(ctypes.Structure):
+    _fields_ = [("loglik", ctypes.c_double), ("logdet", ctypes.c_double), ("quad", ctypes.c_double),
+                ("npd_pivot", ctypes.c_int64), ("n", ctypes.c_int64), ("nb", ctypes.c_int64),
+                ("ntiles", ctypes.c_int64), ("flops", ctypes.c_double), ("ms_total", ctypes.c_double),
+                ("ms_gen", ctypes.c_double), ("ms_chol", ctypes.c_double), ("ms_reduce", ctypes.c_double),
+                ("kernels", ctypes.c_int64)]
+
+    def as_dict(self) -> dict:
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+# (name, restype, argtypes) of every symbol declared in include/exageo.h
+_C = ctypes.c_void_p
+SIGNATURES = [
+    ("exageo_strerror", ctypes.c_char_p, [ctypes.c_int]),
+    ("exageo_last_error", ctypes.c_char_p, [_C]),
+    ("exageo_create", ctypes.c_int, [ctypes.POINTER(_C), ctypes.POINTER(Opts)]),
+    ("exageo_destroy", None, [_C]),
+    ("exageo_workspace_bytes", ctypes.c_size_t, [ctypes.c_int64, ctypes.c_int]),
+    ("exageo_set_workspace", ctypes.c_int, [_C, ctypes.c_void_p, ctypes.c_size_t]),
+    ("exageo_gen_locations", ctypes.c_int, [ctypes.c_int64, ctypes.c_uint64, _f64p, _f64p]),
+    ("exageo_matern_cov", ctypes.c_int, [_C, ctypes.POINTER(Theta), ctypes.c_int64, _f64p, _f64p, ctypes.c_int64,
+                                         _f64p, _f64p, _f64p, ctypes.c_int64]),
+    ("exageo_loglik", ctypes.c_int, [_C, ctypes.POINTER(Theta), ctypes.c_int64, _f64p, _f64p, _f64p, _f64p,
+                                     ctypes.POINTER(LoglikInfo)]),
+    ("exageo_loglik_dev", ctypes.c_int, [_C, ctypes.POINTER(Theta), ctypes.c_int64, ctypes.c_void_p,
+                                         ctypes.c_void_p, ctypes.c_void_p, _f64p, ctypes.POINTER(LoglikInfo)]),
+    ("exageo_simulate", ctypes.c_int, [_C, ctypes.POINTER(Theta), ctypes.c_int64, _f64p, _f64p, _f64p, _f64p]),
+    ("exageo_stage_generate_dev", ctypes.c_int, [_C, ctypes.POINTER(Theta), ctypes.c_int64, ctypes.c_void_p,
+                                                 ctypes.c_void_p, ctypes.c_void_p]),
+    ("exageo_stage_factor", ctypes.c_int, [_C]),
+    ("exageo_stage_finish", ctypes.c_int, [_C, _f64p, _i64p]),
+    ("exageo_read_lower", ctypes.c_int, [_C, _f64p, ctypes.c_int64]),
+    ("exageo_read_zrow", ctypes.c_int, [_C, _f64p]),
+]
+
+_lib = None
+
+
+def load_library():
+    """Load libexageo.so (raises if it has not been built -- no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} is missing: run `python -m paper_1708_02835_b200.build` "
+                               "(this package has no CPU fallback)")
+        L = ctypes.CDLL(LIB_PATH)
+        for name, res, args in SIGNATURES:
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+class ExageoError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{strerror(status)}: {msg}")
+        self.status = status
+
+
+class NotPositiveDefinite(ExageoError):
+    def __init__(self, status: int, msg: str, pivot: int):
+        super().__init__(status, msg)
+        self.pivot = pivot
+
+
+def strerror(status: int) -> str:
+    return load_library().exageo_strerror(status).decode()
+
+
+def _p(a: np.ndarray):
+    return a.ctypes.data_as(_f64p)
+
+
+def _f(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.float64))
+
+
+def _theta(theta) -> Theta:
+    t1, t2, t3 = (float(v) for v in theta)
+    return Theta(t1, t2, t3)
+
+
+def gen_locations(n: int, seed: int):
+    """Jittered-grid locations (DESIGN R1-R3) -> (x, y) numpy float64."""
+    x = np.empty(n, np.float64)
+    y = np.empty(n, np.float64)
+    st = load_library().exageo_gen_locations(int(n), int(seed) & (2**64 - 1), _p(x), _p(y))
+    if st != OK:
+        raise ExageoError(st, load_library().exageo_last_error(None).decode())
+    return x, y
+
+
+def workspace_bytes(n: int, nb: int = 0) -> int:
+    return int(load_library().exageo_workspace_bytes(int(n), int(nb)))
+
+
+@dataclass
+class Result:
+    loglik: float
+    logdet: float
+    quad: float
+    info: dict
+
+
+class Context:
+    """An exageo_ctx on one CUDA device (own stream unless `stream` is given)."""
+
+    def __init__(self, device: int = 0, nb: int = 0, stream=None):
+        self._lib = load_library()
+        self._ctx = ctypes.c_void_p()
+        sp = None
+        if stream is not None:
+            sp = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+        o = Opts(int(device), int(nb), sp)
+        st = self._lib.exageo_create(ctypes.byref(self._ctx), ctypes.byref(o))
+        if st != OK:
+            raise ExageoError(st, self._lib.exageo_last_error(None).decode())
+        self._workspace = None
+
+    # -- plumbing ---------------------------------------------------------
+    def close(self):
+        if self._ctx:
+            self._lib.exageo_destroy(self._ctx)
+            self._ctx = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def _check(self, st: int, pivot: int = -1):
+        if st == OK:
+            return
+        msg = self._lib.exageo_last_error(self._ctx).decode()
+        if st == ENOTPD:
+            raise NotPositiveDefinite(st, msg, pivot)
+        raise ExageoError(st, msg)
+
+    def set_workspace(self, tensor):
+        """Use a caller-owned torch CUDA tensor as tile workspace (None = library-managed)."""
+        if tensor is None:
+            self._check(self._lib.exageo_set_workspace(self._ctx, None, 0))
+        else:
+            nbytes = tensor.numel() * tensor.element_size()
+            self._check(self._lib.exageo_set_workspace(self._ctx, ctypes.c_void_p(tensor.data_ptr()), nbytes))
+        self._workspace = tensor
+
+    # -- API ----------------------------------------------------------------
+    def matern_cov(self, x1, y1, x2, y2, theta) -> np.ndarray:
+        """Dense (m, n) covariance block C_ij = C(||s1_i - s2_j||; theta) computed on the GPU."""
+        x1, y1, x2, y2 = _f(x1), _f(y1), _f(x2), _f(y2)
+        m, n = x1.size, x2.size
+        C = np.empty((n, m), np.float64)  # column-major (m, n)
+        t = _theta(theta)
+        self._check(self._lib.exageo_matern_cov(self._ctx, ctypes.byref(t), m, _p(x1), _p(y1), n, _p(x2), _p(y2),
+                                                _p(C), m))
+        return C.T.copy()
+
+    def loglik(self, x, y, z, theta) -> Result:
+        """Eq. (1) through Alg. 2 with host arrays (H2D copies included)."""
+        x, y, z = _f(x), _f(y), _f(z)
+        t = _theta(theta)
+        out = ctypes.c_double()
+        info = LoglikInfo()
+        st = self._lib.exageo_loglik(self._ctx, ctypes.byref(t), z.size, _p(x), _p(y), _p(z), ctypes.byref(out),
+                                     ctypes.byref(info))
+        self._check(st, info.npd_pivot)
+        return Result(info.loglik, info.logdet, info.quad, info.as_dict())
+
+    def loglik_dev(self, x, y, z, theta) -> Result:
+        """Eq. (1) with torch CUDA float64 tensors already resident on the device."""
+        for a in (x, y, z):
+            if not (a.is_cuda and str(a.dtype) == "torch.float64" and a.is_contiguous()):
+                raise ValueError("loglik_dev needs contiguous CUDA float64 tensors")
+        t = _theta(theta)
+        out = ctypes.c_double()
+        info = LoglikInfo()
+        st = self._lib.exageo_loglik_dev(self._ctx, ctypes.byref(t), z.numel(), ctypes.c_void_p(x.data_ptr()),
+                                         ctypes.c_void_p(y.data_ptr()), ctypes.c_void_p(z.data_ptr()),
+                                         ctypes.byref(out), ctypes.byref(info))
+        self._check(st, info.npd_pivot)
+        return Result(info.loglik, info.logdet, info.quad, info.as_dict())
+
+    def simulate(self, x, y, e, theta) -> np.ndarray:
+        """Alg. 1: z = L(theta) e for given normal variates e."""
+        x, y, e = _f(x), _f(y), _f(e)
+        z = np.empty_like(e)
+        t = _theta(theta)
+        self._check(self._lib.exageo_simulate(self._ctx, ctypes.byref(t), e.size, _p(x), _p(y), _p(e), _p(z)))
+        return z
+
+    # -- stage-level access (tests) -------------------------------------------
+    def stage_generate_dev(self, x, y, z, theta):
+        t = _theta(theta)
+        zp = ctypes.c_void_p(z.data_ptr()) if z is not None else None
+        self._check(self._lib.exageo_stage_generate_dev(self._ctx, ctypes.byref(t), x.numel(),
+                                                        ctypes.c_void_p(x.data_ptr()),
+                                                        ctypes.c_void_p(y.data_ptr()), zp))
+
+    def stage_factor(self):
+        self._check(self._lib.exageo_stage_factor(self._ctx))
+
+    def stage_finish(self):
+        out = np.zeros(3, np.float64)
+        piv = ctypes.c_int64(-1)
+        st = self._lib.exageo_stage_finish(self._ctx, _p(out), ctypes.byref(piv))
+        self._check(st, piv.value)
+        return float(out[0]), float(out[1]), float(out[2])
+
+    def read_lower(self, n: int) -> np.ndarray:
+        """Lower triangle of the workspace matrix as a dense (n, n) array (upper = 0)."""
+        buf = np.zeros((n, n), np.float64)  # column-major n x n == row-major transpose
+        self._check(self._lib.exageo_read_lower(self._ctx, _p(buf), n))
+        return buf.T.copy()
+
+    def read_zrow(self, n: int) -> np.ndarray:
+        buf = np.empty(n, np.float64)
+        self._check(self._lib.exageo_read_zrow(self._ctx, _p(buf)))
+        return buf
+
+
+LOG2PI = math.log(2.0 * math.pi)

@@ -1,0 +1,187 @@
+// matern.cu -- K1: Matern covariance generation (Eq. (2); Alg. 2 l.2).
+//
+// Device evaluator of C(r; theta) = theta1 / (2^(nu-1) Gamma(nu)) x^nu K_nu(x),
+// x = r / theta2, with an in-house modified Bessel function of the second kind:
+//   * nu in {1/2, 3/2, 5/2}: closed forms (P:260-262 for nu = 1/2);
+//   * otherwise Temme's method: write nu = mu + nl, |mu| <= 1/2, evaluate
+//     K_mu and K_mu+1 by Temme's power series (x <= 2) or by Steed's
+//     continued fraction CF2 (x > 2, scaled by e^x), then recur upward
+//     K_{a+1} = K_{a-1} + (2a/x) K_a, which is stable for K.
+// Per-theta constants (prefactor, Temme's gamma_1/gamma_2, 1/Gamma(1 +- mu))
+// are computed once on the host in long double (exageo::matern_consts).
+//
+// The generator writes the lower block-column panels of the workspace
+// (internal.h), one CTA per (panel, column), coalesced double2 stores down the
+// column; identity padding for rows/cols >= n; z into the z row block.
+#include <cmath>
+
+#include "internal.h"
+
+namespace exageo {
+
+namespace {
+
+constexpr double kPi = 3.141592653589793238462643383279502884;
+
+// Temme series for K_mu(x), K_mu+1(x), 0 < x <= 2 (unscaled).
+__device__ __forceinline__ void bessel_k_temme(double x, const MaternConsts& c, double& kmu, double& kmu1) {
+  const double mu = c.mu;
+  const double x2 = 0.5 * x;
+  const double d = -log(x2);          // ln(2/x)
+  const double e = mu * d;            // sigma = mu ln(2/x)
+  const double sinh_e_over_e = (fabs(e) < 1e-4) ? (1.0 + e * e * (1.0 / 6.0 + e * e * (1.0 / 120.0))) : sinh(e) / e;
+  double f = c.pimu_sin * (c.gam1 * cosh(e) + c.gam2 * sinh_e_over_e * d);  // f_0
+  const double ee = exp(e);           // (2/x)^mu
+  double p = 0.5 * ee / c.gampl;      // p_0 = (x/2)^-mu Gamma(1+mu) / 2
+  double q = 0.5 / (ee * c.gammi);    // q_0 = (x/2)^mu  Gamma(1-mu) / 2
+  double ck = 1.0;
+  const double dd = x2 * x2;
+  double sum = f, sum1 = p;
+  const double mu2 = mu * mu;
+  for (int i = 1; i < 200; ++i) {
+    const double di = (double)i;
+    f = (di * f + p + q) / (di * di - mu2);
+    ck *= dd / di;
+    p /= (di - mu);
+    q /= (di + mu);
+    const double del = ck * f;
+    sum += del;
+    sum1 += ck * (p - di * f);
+    if (fabs(del) < 1e-17 * fabs(sum)) break;
+  }
+  kmu = sum;
+  kmu1 = sum1 * (2.0 / x);
+}
+
+// Steed's algorithm (CF2, Temme 1975) for e^x K_mu(x), e^x K_mu+1(x), x > 2.
+__device__ __forceinline__ void bessel_k_cf2_scaled(double x, double mu, double& kmu, double& kmu1) {
+  const double a1 = 0.25 - mu * mu;
+  double b = 2.0 * (1.0 + x);
+  double d = 1.0 / b;
+  double h = d, delh = d;
+  double q1 = 0.0, q2 = 1.0;
+  double q = a1, c = a1, a = -a1;
+  double s = 1.0 + q * delh;
+  for (int i = 1; i < 500; ++i) {
+    const double di = (double)i;
+    a -= 2.0 * di;
+    c = -a * c / (di + 1.0);
+    const double qn = (q1 - b * q2) / a;
+    q1 = q2;
+    q2 = qn;
+    q += c * qn;
+    b += 2.0;
+    d = 1.0 / (b + a * d);
+    delh = (b * d - 1.0) * delh;
+    h += delh;
+    const double dels = q * delh;
+    s += dels;
+    if (fabs(dels) < 1e-17 * fabs(s)) break;
+  }
+  h = a1 * h;
+  kmu = sqrt(kPi / (2.0 * x)) / s;
+  kmu1 = kmu * (mu + x + 0.5 - h) / x;
+}
+
+}  // namespace
+
+// Matern covariance at distance r (Eq. (2)); C(0) = theta1 (R9).
+__device__ __forceinline__ double matern_eval(double r, const MaternConsts& c) {
+  if (r == 0.0) return c.theta1;
+  const double x = r * c.inv_theta2;
+  switch (c.kind) {
+    case 1: return c.theta1 * exp(-x);
+    case 2: return c.theta1 * (1.0 + x) * exp(-x);
+    case 3: return c.theta1 * (1.0 + x + x * x * (1.0 / 3.0)) * exp(-x);
+    default: break;
+  }
+  double k0, k1;
+  const bool small = x <= 2.0;
+  if (small) bessel_k_temme(x, c, k0, k1);
+  else bessel_k_cf2_scaled(x, c.mu, k0, k1);
+  double knu;
+  if (c.nl == 0) {
+    knu = k0;
+  } else {
+    double a = c.mu + 1.0;
+    for (int i = 1; i < c.nl; ++i) {
+      const double kn = k0 + (2.0 * a / x) * k1;
+      k0 = k1;
+      k1 = kn;
+      a += 1.0;
+    }
+    knu = k1;
+  }
+  // x^nu K_nu(x) = exp(nu ln x) K (small x) or exp(nu ln x - x) [e^x K] (large x)
+  const double lx = log(x);
+  const double ex = small ? exp(c.nu * lx) : exp(c.nu * lx - x);
+  return c.pref * ex * knu;
+}
+
+__device__ __forceinline__ double dist2d(double x1, double y1, double x2, double y2) {
+  const double dx = x1 - x2, dy = y1 - y2;
+  return sqrt(dx * dx + dy * dy);
+}
+
+// One CTA per (panel j = blockIdx.y, column cc = blockIdx.x) -> walks the rows
+// of that column with coalesced double2 stores.
+__global__ void __launch_bounds__(256) gen_panels_kernel(Layout L, double* __restrict__ ws, MaternConsts mc,
+                                                         const double* __restrict__ x, const double* __restrict__ y,
+                                                         const double* __restrict__ z) {
+  const int j = blockIdx.y;
+  const int cc = blockIdx.x;
+  const int64_t c = (int64_t)j * L.nb + cc;  // global column
+  const int64_t ld = L.ld(j);
+  const int64_t R = L.N - (int64_t)j * L.nb;  // square rows of this panel
+  double* col = ws + L.off(j) + (int64_t)cc * ld;
+  const bool cin = c < L.n;
+  const double xc = cin ? x[c] : 0.0, yc = cin ? y[c] : 0.0;
+  for (int64_t rr = 2 * (int64_t)threadIdx.x; rr < ld; rr += 2 * blockDim.x) {
+    double v[2];
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int64_t lr = rr + e;
+      double val;
+      if (lr < R) {
+        const int64_t r = (int64_t)j * L.nb + lr;  // global row
+        if (r >= L.n || !cin) val = (r == c) ? 1.0 : 0.0;
+        else if (r == c) val = mc.theta1;
+        else val = matern_eval(dist2d(x[r], y[r], xc, yc), mc);
+      } else {
+        val = (lr == R && cin && z != nullptr) ? z[c] : 0.0;  // z row block
+      }
+      v[e] = val;
+    }
+    *reinterpret_cast<double2*>(col + rr) = make_double2(v[0], v[1]);
+  }
+}
+
+__global__ void __launch_bounds__(256) matern_dense_kernel(MaternConsts mc, int64_t m, const double* __restrict__ x1,
+                                                           const double* __restrict__ y1, int64_t n,
+                                                           const double* __restrict__ x2,
+                                                           const double* __restrict__ y2, double* __restrict__ C,
+                                                           int64_t ldc) {
+  const int64_t j = blockIdx.y;
+  const double xj = x2[j], yj = y2[j];
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+    C[i + j * ldc] = matern_eval(dist2d(x1[i], y1[i], xj, yj), mc);
+}
+
+void launch_gen_panels(const Layout& L, double* ws, const MaternConsts& mc, const double* x, const double* y,
+                       const double* z, cudaStream_t s) {
+  dim3 grid(L.nb, L.T);
+  gen_panels_kernel<<<grid, 256, 0, s>>>(L, ws, mc, x, y, z);
+}
+
+void launch_matern_dense(const MaternConsts& mc, int64_t m, const double* x1, const double* y1, int64_t n,
+                         const double* x2, const double* y2, double* C, int64_t ldc, cudaStream_t s) {
+  for (int64_t j0 = 0; j0 < n; j0 += 65535) {
+    const int64_t nj = (n - j0) < 65535 ? (n - j0) : 65535;
+    int gx = (int)((m + 255) / 256);
+    if (gx > 64) gx = 64;
+    dim3 grid(gx, (unsigned)nj);
+    matern_dense_kernel<<<grid, 256, 0, s>>>(mc, m, x1, y1, nj, x2 + j0, y2 + j0, C + j0 * ldc, ldc);
+  }
+}
+
+}  // namespace exageo

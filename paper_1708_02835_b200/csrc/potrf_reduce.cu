@@ -1,0 +1,220 @@
+// potrf_reduce.cu -- K2 (diagonal-block POTRF + inverse + log-det partial),
+// K6 (deterministic log-det / dot reductions and l(theta)), read-back and TRMV.
+//
+//  * potrf_block: the PB x PB (PB = 64) diagonal block of the current panel is
+//    factored in shared memory by the right-looking unblocked algorithm
+//    (L_jj = sqrt(a_jj); l_ij = a_ij / L_jj; a_ic -= l_ij l_cj), the paper's
+//    dpotrf at tile granularity (Alg. 2 l.3). The same CTA forms
+//    W = L^{-1} so that the panel TRSM becomes a DMMA multiplication, and the
+//    partial log-determinant sum_i log L_ii (R5). The first
+//    non-positive pivot is recorded as a global index (R14); every later
+//    kernel reads the info word and exits.
+//  * finish: logdet = 2 sum(partials), quad = sum y_i^2 over the z row
+//    (y = L^{-1} z, Alg. 2 l.4-6, R6-R7), l = -quad/2 - logdet/2 - n/2 log 2 pi
+//    (Alg. 2 l.7) -- fixed-order trees, bitwise reproducible.
+#include <cmath>
+
+#include "internal.h"
+
+namespace exageo {
+
+namespace {
+
+constexpr int LDS_P = PB + 1;
+
+__global__ void __launch_bounds__(256) potrf_block_kernel(double* __restrict__ a, int64_t lda, double* __restrict__ W,
+                                                          double* __restrict__ slot, int* __restrict__ info,
+                                                          int64_t pivot_base) {
+  if (*(volatile int*)info != 0) return;
+  extern __shared__ double smem_p[];
+  double* s = smem_p;               // column-major, s[c * LDS_P + r]
+  double* w = smem_p + PB * LDS_P;  // W = L^{-1}, same layout
+  __shared__ int bad;
+  const int tid = threadIdx.x;
+  for (int idx = tid; idx < PB * PB; idx += blockDim.x) {
+    const int r = idx % PB, c = idx / PB;
+    s[c * LDS_P + r] = (r >= c) ? a[(int64_t)c * lda + r] : 0.0;
+  }
+  if (tid == 0) bad = -1;
+  __syncthreads();
+  for (int j = 0; j < PB; ++j) {
+    if (tid == 0) {
+      const double d = s[j * LDS_P + j];
+      if (!(d > 0.0)) bad = j;
+      else s[j * LDS_P + j] = sqrt(d);
+    }
+    __syncthreads();
+    if (bad >= 0) break;
+    const double ljj = s[j * LDS_P + j];
+    if (tid > j && tid < PB) s[j * LDS_P + tid] /= ljj;
+    __syncthreads();
+    const int m = PB - 1 - j;
+    for (int idx = tid; idx < m * m; idx += blockDim.x) {
+      const int r = j + 1 + idx % m, c = j + 1 + idx / m;
+      if (r >= c) s[c * LDS_P + r] -= s[j * LDS_P + r] * s[j * LDS_P + c];
+    }
+    __syncthreads();
+  }
+  if (bad >= 0) {
+    if (tid == 0) *info = (int)(pivot_base + bad + 1);
+    return;
+  }
+  // W = L^{-1}: thread t < PB owns column t (forward substitution on e_t).
+  if (tid < PB) {
+    const int t = tid;
+    for (int r = 0; r < t; ++r) w[t * LDS_P + r] = 0.0;
+    w[t * LDS_P + t] = 1.0 / s[t * LDS_P + t];
+    for (int i = t + 1; i < PB; ++i) {
+      double acc = 0.0;
+      for (int p = t; p < i; ++p) acc += s[p * LDS_P + i] * w[t * LDS_P + p];
+      w[t * LDS_P + i] = -acc / s[i * LDS_P + i];
+    }
+  }
+  if (tid == 0) {
+    double ld = 0.0;
+    for (int i = 0; i < PB; ++i) ld += log(s[i * LDS_P + i]);
+    *slot = ld;
+  }
+  __syncthreads();
+  for (int idx = tid; idx < PB * PB; idx += blockDim.x) {
+    const int r = idx % PB, c = idx / PB;
+    a[(int64_t)c * lda + r] = (r >= c) ? s[c * LDS_P + r] : 0.0;
+    W[c * PB + r] = w[c * LDS_P + r];
+  }
+}
+
+// Fixed-shape block sum (blockDim.x a multiple of 32): deterministic tree.
+__device__ double block_sum(double v, double* red) {
+  const int tid = threadIdx.x;
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  if ((tid & 31) == 0) red[tid >> 5] = v;
+  __syncthreads();
+  double r = 0.0;
+  if (tid < 32) {
+    r = (tid < (int)(blockDim.x >> 5)) ? red[tid] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) r += __shfl_down_sync(0xffffffffu, r, o);
+  }
+  __syncthreads();
+  return r;  // valid in thread 0
+}
+
+constexpr int kFinishBlocks = 148;
+
+// Stage 1: kFinishBlocks CTAs, CTA b sums y_c^2 over its contiguous range of c.
+__global__ void __launch_bounds__(512) quad_partial_kernel(Layout L, const double* __restrict__ ws,
+                                                            double* __restrict__ part) {
+  __shared__ double red[32];
+  const int64_t per = (L.n + gridDim.x - 1) / gridDim.x;
+  const int64_t lo = (int64_t)blockIdx.x * per;
+  const int64_t hi = (lo + per) < L.n ? (lo + per) : L.n;
+  double v = 0.0;
+  for (int64_t c = lo + threadIdx.x; c < hi; c += blockDim.x) {
+    const int j = (int)(c / L.nb);
+    const int64_t jb = (int64_t)j * L.nb;
+    const double yv = ws[L.off(j) + (c - jb) * L.ld(j) + (L.N - jb)];
+    v += yv * yv;
+  }
+  const double s = block_sum(v, red);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
+// Stage 2: one CTA combines the partials in fixed order.
+__global__ void __launch_bounds__(1024) finish_kernel(Layout L, const double* __restrict__ slots, int nslots,
+                                                      const double* __restrict__ part, int nparts,
+                                                      double* __restrict__ out) {
+  __shared__ double red[32];
+  double a = 0.0, b = 0.0;
+  for (int i = threadIdx.x; i < nslots; i += blockDim.x) a += slots[i];
+  for (int i = threadIdx.x; i < nparts; i += blockDim.x) b += part[i];
+  const double sa = block_sum(a, red);
+  const double sb = block_sum(b, red);
+  if (threadIdx.x == 0) {
+    const double logdet = 2.0 * sa;
+    const double quad = sb;
+    const double log2pi = 1.8378770664093454835606594728112;
+    out[0] = -0.5 * quad - 0.5 * logdet - 0.5 * (double)L.n * log2pi;
+    out[1] = logdet;
+    out[2] = quad;
+  }
+}
+
+__global__ void read_lower_kernel(Layout L, const double* __restrict__ ws, double* __restrict__ dst, int64_t ld) {
+  const int64_t c = blockIdx.x;
+  const int j = (int)(c / L.nb);
+  const int64_t jb = (int64_t)j * L.nb;
+  const double* col = ws + L.off(j) + (c - jb) * L.ld(j) - jb;  // index by global row
+  for (int64_t r = c + threadIdx.x; r < L.n; r += blockDim.x) dst[c * ld + r] = col[r];
+}
+
+__global__ void read_zrow_kernel(Layout L, const double* __restrict__ ws, double* __restrict__ dst) {
+  for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < L.n; c += (int64_t)gridDim.x * blockDim.x) {
+    const int j = (int)(c / L.nb);
+    const int64_t jb = (int64_t)j * L.nb;
+    dst[c] = ws[L.off(j) + (c - jb) * L.ld(j) + (L.N - jb)];
+  }
+}
+
+// TRMV stage 1: part[j][r] = sum_{c in panel j, c <= r} L[r][c] e[c]  (grid: row blocks x panels).
+__global__ void __launch_bounds__(256) trmv_partial_kernel(Layout L, const double* __restrict__ ws,
+                                                           const double* __restrict__ e, double* __restrict__ part) {
+  const int j = blockIdx.y;
+  const int64_t jb = (int64_t)j * L.nb;
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= L.N) return;
+  double acc = 0.0;
+  if (r >= jb) {
+    const double* P = ws + L.off(j) + (r - jb);
+    const int64_t ld = L.ld(j);
+    const int64_t cend = (r - jb + 1) < L.nb ? (r - jb + 1) : L.nb;
+    for (int64_t cc = 0; cc < cend; ++cc) {
+      const int64_t c = jb + cc;
+      if (c < L.n) acc += P[cc * ld] * e[c];
+    }
+  }
+  part[(int64_t)j * L.N + r] = acc;
+}
+
+__global__ void trmv_sum_kernel(Layout L, const double* __restrict__ part, double* __restrict__ z) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= L.n) return;
+  double acc = 0.0;
+  for (int j = 0; j < L.T; ++j) acc += part[(int64_t)j * L.N + r];
+  z[r] = acc;
+}
+
+}  // namespace
+
+constexpr int kPotrfSmem = 2 * PB * LDS_P * (int)sizeof(double);
+
+cudaError_t potrf_init() {
+  return cudaFuncSetAttribute(potrf_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kPotrfSmem);
+}
+
+void launch_potrf_block(double* a, int64_t lda, double* W, double* slot, int* info, int64_t pivot_base,
+                        cudaStream_t s) {
+  potrf_block_kernel<<<1, 256, kPotrfSmem, s>>>(a, lda, W, slot, info, pivot_base);
+}
+
+void launch_finish(const Layout& L, const double* ws, const double* slots, int nslots, double* out, cudaStream_t s) {
+  // out[3 .. 3 + kFinishBlocks) is scratch for the partial dot products.
+  double* part = out + 4;
+  quad_partial_kernel<<<kFinishBlocks, 512, 0, s>>>(L, ws, part);
+  finish_kernel<<<1, 1024, 0, s>>>(L, slots, nslots, part, kFinishBlocks, out);
+}
+
+void launch_read_lower(const Layout& L, const double* ws, double* dst, int64_t ld, cudaStream_t s) {
+  read_lower_kernel<<<(unsigned)L.n, 256, 0, s>>>(L, ws, dst, ld);
+}
+
+void launch_read_zrow(const Layout& L, const double* ws, double* dst, cudaStream_t s) {
+  read_zrow_kernel<<<128, 256, 0, s>>>(L, ws, dst);
+}
+
+void launch_trmv_lower(const Layout& L, const double* ws, const double* e, double* z, double* part,
+                       cudaStream_t s) {
+  dim3 g1((unsigned)((L.N + 255) / 256), (unsigned)L.T);
+  trmv_partial_kernel<<<g1, 256, 0, s>>>(L, ws, e, part);
+  trmv_sum_kernel<<<(unsigned)((L.n + 255) / 256), 256, 0, s>>>(L, part, z);
+}
+
+}  // namespace exageo

@@ -1,0 +1,244 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Tolerances:
+  * covariance entries: max relative error <= 5e-14 (K_nu evaluator vs the
+    oracle's quadrature; R-budget in DESIGN.md);
+  * factor: ||L_gpu - L_oracle||_max / ||L||_max <= 1e-12;
+  * l(theta): |dl| <= 1e-10 * max(|l|, |logdet|/2, quad/2, (n/2) log 2 pi)
+    (BASELINE.json north_star 1e-10 relative, guarded against cancellation, R13).
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+import synth_inputs as si
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_1708_02835_b200 as ex  # noqa: E402
+
+LOG2PI = math.log(2 * math.pi)
+
+
+def ll_tol(ll, logdet, quad, n):
+    return 1e-10 * max(abs(ll), 0.5 * abs(logdet), 0.5 * abs(quad), 0.5 * n * LOG2PI)
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    c = ex.Context(device=0)
+    yield c
+    c.close()
+
+
+@pytest.fixture(scope="module")
+def ctx128():
+    c = ex.Context(device=0, nb=128)
+    yield c
+    c.close()
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).cuda()
+
+
+THETAS = [(1.0, 0.1, 0.5), (1.0, 0.1, 1.0), (2.0, 0.05, 1.5), (0.7, 0.2, 2.5), (1.3, 0.08, 0.3),
+          (1.0, 0.1, 0.77), (0.9, 0.03, 1.7), (1.0, 0.1, 2.2), (1.0, 0.3, 3.6)]
+
+
+@pytest.mark.parametrize("theta", THETAS)
+def test_matern_cov_entrywise(ctx, theta):
+    x, y = oracle.gen_locations(300, 2)
+    xn, yn = oracle.gen_locations(90, 5)
+    got = ctx.matern_cov(xn, yn, x, y, theta)
+    ref = oracle.cov(xn, yn, x, y, theta)
+    rel = np.abs(got - ref) / np.maximum(np.abs(ref), 1e-300)
+    mask = np.abs(ref) > 1e-290
+    assert rel[mask].max() <= 5e-14, (theta, rel[mask].max())
+
+
+def test_matern_cov_distance_sweep(ctx):
+    # distances r/theta2 from 1e-4 to 700 across the Temme / CF2 switch (x = 2)
+    r = np.concatenate([np.geomspace(1e-5, 70.0, 400), [0.2 - 1e-12, 0.2, 0.2 + 1e-12]])
+    x2, y2 = np.zeros(1), np.zeros(1)
+    for nu in [0.1, 0.35, 0.5, 0.99, 1.0, 1.01, 1.5, 1.49999, 2.0, 2.5, 3.3, 4.9]:
+        theta = (1.0, 0.1, nu)
+        got = ctx.matern_cov(r, np.zeros_like(r), x2, y2, theta)[:, 0]
+        ref = np.array([oracle.matern(v, theta) for v in r])
+        mask = ref > 1e-290
+        rel = np.abs(got[mask] - ref[mask]) / ref[mask]
+        # exp(nu ln x - x) has relative condition number ~x: allow 4e-16 x on top
+        bound = 5e-14 + 4e-16 * r[mask] / 0.1
+        assert np.all(rel <= bound), (nu, rel.max(), r[mask][(rel / bound).argmax()])
+
+
+@pytest.mark.parametrize("n,nb,nu", [(700, 128, 0.5), (1000, 256, 1.3), (131, 128, 2.5)])
+def test_generated_panels_match_oracle(n, nb, nu):
+    c = ex.Context(device=0, nb=nb)
+    x, y = ex.gen_locations(n, 3)
+    z = si.normals(n, 4)
+    theta = (1.2, 0.1, nu)
+    c.stage_generate_dev(dev(x), dev(y), dev(z), theta)
+    S = c.read_lower(n)
+    ref = np.tril(oracle.cov(x, y, x, y, theta))
+    rel = np.abs(S - ref) / np.maximum(np.abs(ref), 1e-300)
+    assert rel.max() <= 5e-14
+    np.testing.assert_array_equal(c.read_zrow(n), z)
+    c.close()
+
+
+@pytest.mark.parametrize("n,nb,theta", [(700, 128, (1.0, 0.1, 0.5)), (1000, 256, (1.0, 0.1, 1.0)),
+                                        (1100, 128, (1.5, 0.05, 1.5)), (257, 128, (1.0, 0.2, 0.9))])
+def test_factor_and_solve_match_oracle(n, nb, theta):
+    c = ex.Context(device=0, nb=nb)
+    x, y = ex.gen_locations(n, 7)
+    z = si.normals(n, 8)
+    c.stage_generate_dev(dev(x), dev(y), dev(z), theta)
+    c.stage_factor()
+    L = c.read_lower(n)
+    yv = c.read_zrow(n)
+    Lo = oracle.cholesky(oracle.cov(x, y, x, y, theta))
+    err = np.abs(L - Lo).max() / np.abs(Lo).max()
+    assert err <= 1e-12, err
+    yo = oracle.forward(Lo, z)
+    assert np.abs(yv - yo).max() / np.abs(yo).max() <= 1e-10
+    ll, logdet, quad = c.stage_finish()
+    llo, ldo, qo = oracle.loglik(x, y, z, theta)
+    assert abs(ll - llo) <= ll_tol(llo, ldo, qo, n)
+    c.close()
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 17, 128, 129, 400, 1000, 1600])
+@pytest.mark.parametrize("theta", [(1.0, 0.1, 0.5), (1.0, 0.1, 1.0), (2.0, 0.07, 0.6)])
+def test_loglik_matches_oracle(ctx, n, theta):
+    x, y = ex.gen_locations(n, 1)
+    e = si.normals(n, 2)
+    z = oracle.simulate(x, y, (1.0, 0.1, 0.5), e)
+    r = ctx.loglik(x, y, z, theta)
+    llo, ldo, qo = oracle.loglik(x, y, z, theta)
+    assert abs(r.loglik - llo) <= ll_tol(llo, ldo, qo, n), (r.loglik, llo)
+    assert r.logdet == pytest.approx(ldo, rel=1e-10, abs=1e-10)
+    assert r.quad == pytest.approx(qo, rel=1e-10)
+
+
+def test_loglik_config1_n400(ctx):
+    # BASELINE.json configs[0]: n = 400 (20 x 20 grid), theta = (1, 0.1, 0.5), z from a fixed seed
+    n, theta = 400, (1.0, 0.1, 0.5)
+    x, y = ex.gen_locations(n, 1)
+    z = oracle.simulate(x, y, theta, si.normals(n, 1))
+    for nb in (128, 256, 512):
+        c = ex.Context(device=0, nb=nb)
+        r = c.loglik(x, y, z, theta)
+        llo, ldo, qo = oracle.loglik(x, y, z, theta)
+        assert abs(r.loglik - llo) <= ll_tol(llo, ldo, qo, n)
+        c.close()
+
+
+def test_loglik_closed_forms(ctx):
+    # n = 1 and n = 2
+    r = ctx.loglik([0.3], [0.4], [0.0], (1.0, 0.1, 0.5))
+    assert r.loglik == pytest.approx(-0.5 * LOG2PI, rel=1e-15)
+    t1, t2, nu = 1.7, 0.1, 0.5
+    rho = math.exp(-1.0)
+    z1, z2 = 1.0, -0.5
+    logdet = 2 * math.log(t1) + math.log(1 - rho * rho)
+    quad = (z1 * z1 - 2 * rho * z1 * z2 + z2 * z2) / (t1 * (1 - rho * rho))
+    r = ctx.loglik([0.1, 0.16], [0.2, 0.28], [z1, z2], (t1, t2, nu))
+    assert r.loglik == pytest.approx(-LOG2PI - 0.5 * logdet - 0.5 * quad, rel=1e-14)
+
+
+def kms(z, t1, rho):
+    n = z.size
+    logdet = n * math.log(t1) + (n - 1) * math.log1p(-rho * rho)
+    w = np.empty(n)
+    w[0] = z[0] / math.sqrt(t1)
+    w[1:] = (z[1:] - rho * z[:-1]) / math.sqrt(t1 * (1 - rho * rho))
+    quad = float(np.dot(w, w))
+    return -0.5 * quad - 0.5 * logdet - 0.5 * n * LOG2PI, logdet, quad
+
+
+@pytest.mark.parametrize("n", [5000, 23456])
+def test_loglik_ar1_closed_form(ctx, n):
+    h, t1, t2 = 2.0**-12, 1.3, 0.05
+    x, y = si.collinear_sites(n, h)
+    z = si.normals(n, 31)
+    r = ctx.loglik(x, y, z, (t1, t2, 0.5))
+    ll, ld, qd = kms(z, t1, math.exp(-h / t2))
+    assert abs(r.loglik - ll) <= ll_tol(ll, ld, qd, n)
+    assert r.logdet == pytest.approx(ld, rel=1e-11)
+
+
+def test_loglik_identity_covariance(ctx):
+    n, t1 = 3000, 2.3
+    x, y = si.spread_sites(n, 100.0)
+    z = si.normals(n, 4)
+    r = ctx.loglik(x, y, z, (t1, 0.1, 1.5))
+    assert r.logdet == pytest.approx(n * math.log(t1), rel=1e-13)
+    assert r.quad == pytest.approx(float(z @ z) / t1, rel=1e-13)
+
+
+def test_not_positive_definite_pivot(ctx):
+    x = np.array([0.1, 0.5, 0.5, 0.9])
+    y = np.array([0.1, 0.5, 0.5, 0.2])
+    with pytest.raises(ex.NotPositiveDefinite) as ei:
+        ctx.loglik(x, y, [1.0, 2.0, 3.0, 4.0], (1.0, 0.1, 0.5))
+    assert ei.value.pivot == 2
+    # the context stays usable afterwards
+    r = ctx.loglik([0.3], [0.4], [0.0], (1.0, 0.1, 0.5))
+    assert r.loglik == pytest.approx(-0.5 * LOG2PI, rel=1e-15)
+
+
+def test_invalid_theta(ctx):
+    for bad in [(0.0, 0.1, 0.5), (1.0, -0.1, 0.5), (1.0, 0.1, float("nan"))]:
+        with pytest.raises(ex.ExageoError) as ei:
+            ctx.loglik([0.1], [0.2], [0.3], bad)
+        assert ei.value.status == ex.EINVAL
+
+
+def test_deterministic(ctx):
+    n = 3000
+    x, y = ex.gen_locations(n, 1)
+    z = si.normals(n, 2)
+    a = ctx.loglik(x, y, z, (1.0, 0.1, 0.8))
+    b = ctx.loglik(x, y, z, (1.0, 0.1, 0.8))
+    assert a.loglik == b.loglik and a.logdet == b.logdet and a.quad == b.quad
+
+
+def test_loglik_dev_matches_host(ctx):
+    n = 2000
+    x, y = ex.gen_locations(n, 4)
+    z = si.normals(n, 5)
+    a = ctx.loglik(x, y, z, (1.0, 0.1, 0.5))
+    b = ctx.loglik_dev(dev(x), dev(y), dev(z), (1.0, 0.1, 0.5))
+    assert a.loglik == b.loglik
+
+
+def test_nb_independence():
+    n = 2100
+    x, y = ex.gen_locations(n, 6)
+    z = si.normals(n, 7)
+    vals = []
+    for nb in (128, 256, 384, 512):
+        c = ex.Context(device=0, nb=nb)
+        vals.append(c.loglik(x, y, z, (1.0, 0.1, 1.0)).loglik)
+        c.close()
+    assert max(vals) - min(vals) <= 1e-12 * abs(vals[0])
+
+
+def test_simulate_matches_oracle_and_roundtrip(ctx):
+    n = 900
+    theta = (1.0, 0.1, 1.0)
+    x, y = ex.gen_locations(n, 9)
+    e = si.normals(n, 10)
+    z = ctx.simulate(x, y, e, theta)
+    zo = oracle.simulate(x, y, theta, e)
+    assert np.abs(z - zo).max() <= 1e-11 * np.abs(zo).max()
+    # Alg. 1 then Alg. 2 at the same theta: y = L^{-1} z = e, so quad = e^T e
+    r = ctx.loglik(x, y, z, theta)
+    assert r.quad == pytest.approx(float(e @ e), rel=1e-10)
