@@ -49,6 +49,9 @@ struct exageo_ctx {
   Layout L;
   bool have_matrix = false;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  // lookahead schedule: two prioritised internal streams and their events
+  cudaStream_t s_la = nullptr, s_main = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_F = nullptr, ev_U2 = nullptr, ev_join[2] = {nullptr, nullptr};
   int64_t kernels = 0;
   std::string err;
 };
@@ -183,31 +186,58 @@ exageo_status do_generate(exageo_ctx* c, const exageo_theta* t, int64_t n, const
   return check_launch(c);
 }
 
+// Factor panel k (left-looking over PB-wide column blocks) on stream s.
+void factor_panel(exageo_ctx* c, int k, cudaStream_t s) {
+  const Layout& L = c->L;
+  const int nsub = L.nb / PB;
+  double* Pk = c->ws + L.off(k);
+  const int64_t ldk = L.ld(k);
+  for (int sb = 0; sb < nsub; ++sb) {
+    const int64_t c0 = (int64_t)sb * PB;
+    if (sb > 0) {
+      launch_gemm_panel(ldk - c0, PB, (int)c0, Pk + c0, ldk, Pk + c0, ldk, Pk + c0 * ldk + c0, ldk, true, c->info, s);
+      c->kernels += 1;
+    }
+    launch_potrf_block(Pk + c0 * ldk + c0, ldk, c->W, c->slots + (int64_t)k * nsub + sb, c->info,
+                       (int64_t)k * L.nb + c0, s);
+    double* below = Pk + c0 * ldk + c0 + PB;
+    launch_gemm_panel(ldk - c0 - PB, PB, PB, below, ldk, c->W, PB, below, ldk, false, c->info, s);
+    c->kernels += 2;
+  }
+}
+
+// Right-looking tile Cholesky with depth-1 lookahead (the paper's "updates of the
+// trailing submatrix may be triggered before the current panel factorization is
+// complete"), as two prioritised CUDA streams instead of a runtime DAG:
+//   s_la  (high priority): U1(k) = update of tile column k+1 by panel k, then F(k+1)
+//   s_main (low priority): U2(k) = update of tile columns >= k+2 by panel k
+// Dependencies: U1(k) after U2(k-1); U2(k) after F(k). F(k+1) overlaps U2(k).
 exageo_status do_factor(exageo_ctx* c) {
   if (!c->have_matrix) return fail(c, EXAGEO_EINVAL, "no generated matrix in the workspace");
   const Layout& L = c->L;
-  const int nsub = L.nb / PB;
-  for (int k = 0; k < L.T; ++k) {
-    double* Pk = c->ws + L.off(k);
-    const int64_t ldk = L.ld(k);
-    for (int s = 0; s < nsub; ++s) {
-      const int64_t c0 = (int64_t)s * PB;
-      if (s > 0) {
-        launch_gemm_panel(ldk - c0, PB, (int)c0, Pk + c0, ldk, Pk + c0, ldk, Pk + c0 * ldk + c0, ldk, true, c->info,
-                          c->stream);
-        c->kernels += 1;
-      }
-      launch_potrf_block(Pk + c0 * ldk + c0, ldk, c->W, c->slots + (int64_t)k * nsub + s, c->info,
-                         (int64_t)k * L.nb + c0, c->stream);
-      double* below = Pk + c0 * ldk + c0 + PB;
-      launch_gemm_panel(ldk - c0 - PB, PB, PB, below, ldk, c->W, PB, below, ldk, false, c->info, c->stream);
-      c->kernels += 2;
-    }
-    if (k + 1 < L.T) {
-      launch_syrk_trailing(L, c->ws, k, c->info, c->stream);
+  const int cpt = L.nb / 128;  // 128-column blocks per tile column
+  CUDA_TRY(c, cudaEventRecord(c->ev_fork, c->stream));
+  CUDA_TRY(c, cudaStreamWaitEvent(c->s_la, c->ev_fork, 0));
+  CUDA_TRY(c, cudaStreamWaitEvent(c->s_main, c->ev_fork, 0));
+  factor_panel(c, 0, c->s_la);
+  CUDA_TRY(c, cudaEventRecord(c->ev_F, c->s_la));
+  for (int k = 0; k + 1 < L.T; ++k) {
+    CUDA_TRY(c, cudaStreamWaitEvent(c->s_main, c->ev_F, 0));    // U2(k) needs F(k)
+    if (k > 0) CUDA_TRY(c, cudaStreamWaitEvent(c->s_la, c->ev_U2, 0));  // U1(k) needs U2(k-1)
+    launch_syrk_trailing(L, c->ws, k, 0, cpt, c->info, c->s_la);       // U1(k)
+    factor_panel(c, k + 1, c->s_la);                                   // F(k+1)
+    CUDA_TRY(c, cudaEventRecord(c->ev_F, c->s_la));
+    c->kernels += 1;
+    if (k + 2 < L.T) {
+      launch_syrk_trailing(L, c->ws, k, cpt, -1, c->info, c->s_main);  // U2(k)
       c->kernels += 1;
     }
+    CUDA_TRY(c, cudaEventRecord(c->ev_U2, c->s_main));
   }
+  CUDA_TRY(c, cudaEventRecord(c->ev_join[0], c->s_la));
+  CUDA_TRY(c, cudaEventRecord(c->ev_join[1], c->s_main));
+  CUDA_TRY(c, cudaStreamWaitEvent(c->stream, c->ev_join[0], 0));
+  CUDA_TRY(c, cudaStreamWaitEvent(c->stream, c->ev_join[1], 0));
   return check_launch(c);
 }
 
@@ -329,6 +359,16 @@ exageo_status exageo_create(exageo_ctx** out, const exageo_opts* opts) {
   }
   for (auto& ev : c->ev)
     if ((e = cudaEventCreate(&ev)) != cudaSuccess) return bail(e, "cudaEventCreate");
+  {
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);  // hi = numerically smallest = highest priority
+    if ((e = cudaStreamCreateWithPriority(&c->s_la, cudaStreamNonBlocking, hi)) != cudaSuccess)
+      return bail(e, "cudaStreamCreateWithPriority");
+    if ((e = cudaStreamCreateWithPriority(&c->s_main, cudaStreamNonBlocking, lo)) != cudaSuccess)
+      return bail(e, "cudaStreamCreateWithPriority");
+    for (cudaEvent_t* ev : {&c->ev_fork, &c->ev_F, &c->ev_U2, &c->ev_join[0], &c->ev_join[1]})
+      if ((e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming)) != cudaSuccess) return bail(e, "cudaEventCreate");
+  }
   if ((e = cudaMalloc(&c->W, sizeof(double) * PB * PB)) != cudaSuccess) return bail(e, "cudaMalloc");
   if ((e = cudaMalloc(&c->out, sizeof(double) * kOutDoubles)) != cudaSuccess) return bail(e, "cudaMalloc");
   if ((e = cudaMalloc(&c->info, sizeof(int))) != cudaSuccess) return bail(e, "cudaMalloc");
@@ -349,6 +389,10 @@ void exageo_destroy(exageo_ctx* c) {
   cudaFree(c->part);
   for (auto& ev : c->ev)
     if (ev) cudaEventDestroy(ev);
+  for (cudaEvent_t ev : {c->ev_fork, c->ev_F, c->ev_U2, c->ev_join[0], c->ev_join[1]})
+    if (ev) cudaEventDestroy(ev);
+  if (c->s_la) cudaStreamDestroy(c->s_la);
+  if (c->s_main) cudaStreamDestroy(c->s_main);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }

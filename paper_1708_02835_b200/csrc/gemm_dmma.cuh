@@ -1,0 +1,248 @@
+// gemm_dmma.cuh -- the FP64 tensor-core (DMMA) contraction kernel family of the
+// tiled Cholesky (K3 TRSM-by-inverse, K4 SYRK/GEMM trailing update, and the
+// left-looking panel update). Included by gemm_dmma.cu (the product) and by
+// tools/gemm_tune.cu (the tuning harness).
+//
+//     C (M x N) <- C - A (M x K) * B (N x K)^T      (ACC = true)
+//     C (M x N) <-     A (M x K) * B (N x K)^T      (ACC = false; C may alias A when
+//                                                    one CTA owns all N columns)
+// A, B, C column-major. Paper: tile DAG of Fig. 2; the trailing
+// update is the compute-intensive Level-3 BLAS phase.
+//
+// sm_100a FP64: tcgen05.mma has no f64 kind; the FP64 tensor path is the
+// warp-level mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4 = 256 FMA; chip peak measured
+// 37.2 TFLOP/s at 1965 MHz, tools/probes/fp64_peak.cu). Operands are staged
+// global -> shared by a STAGES-deep cp.async (LDGSTS.128, L2-only) ring;
+// fragments are read with conflict-free LDS.64 (shared leading dimension
+// = 4 mod 16 doubles); accumulators live in registers.
+#pragma once
+#include <cstdint>
+
+#include "internal.h"
+
+namespace exageo {
+namespace gemm {
+
+struct GemmTile {
+  const double* A;
+  const double* B;
+  double* C;
+  int64_t lda, ldb, ldc;
+  int K;
+  int m_valid, n_valid;
+};
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+// D = A(8x4) B(4x8) + C(8x8); lane l holds A[l/4][l%4], B[l%4][l/4], C[l/4][2(l%4)+{0,1}].
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+// Dense problem: CTA (bm, bn) of a ceil(M/BM) x ceil(N/BN) grid.
+struct DenseMap {
+  const double* A;
+  const double* B;
+  double* C;
+  int64_t lda, ldb, ldc;
+  int64_t M;
+  int N, K;
+  int mblocks;
+  template <int BM, int BN>
+  __device__ __forceinline__ bool operator()(int64_t bid, GemmTile& t) const {
+    const int64_t bm = bid % mblocks, bn = bid / mblocks;
+    t.A = A + bm * BM;
+    t.B = B + bn * BN;
+    t.C = C + bn * BN * ldc + bm * BM;
+    t.lda = lda;
+    t.ldb = ldb;
+    t.ldc = ldc;
+    t.K = K;
+    const int64_t mv = M - bm * BM;
+    t.m_valid = mv > BM ? BM : (int)mv;
+    t.n_valid = (N - (int)bn * BN) > BN ? BN : (N - (int)bn * BN);
+    return true;
+  }
+  __host__ int64_t blocks(int BM, int BN) const { return (int64_t)((M + BM - 1) / BM) * ((N + BN - 1) / BN); }
+};
+
+// Trailing update of step k over the lower block-column panels (internal.h).
+// Square 128-blocks (rb >= cb) of the trailing matrix, rows/cols >= c0 = (k+1) nb;
+// row block rb == Mb is the z row block. A 128-col block is split into
+// 128/BN CTA tiles (consecutive bids share the row block).
+// Enumeration: column by column, row blocks top to bottom.
+struct SyrkMap {
+  Layout L;
+  double* ws;
+  int k;
+  int Mb;      // number of square 128-blocks in the trailing matrix
+  int cb_lo;   // first 128-column block of this launch (0 = column (k+1) nb)
+  int cb_hi;   // one past the last 128-column block (<= Mb)
+  __host__ __device__ static int64_t S(int64_t c, int Mb) { return c * (Mb + 1) - c * (c - 1) / 2; }
+  template <int BM, int BN>
+  __device__ __forceinline__ bool operator()(int64_t bid, GemmTile& t) const {
+    static_assert(BM == 128 && (BN == 128 || BN == 64), "SyrkMap: 128 x {64,128} tiles");
+    constexpr int SPLIT = 128 / BN;
+    const int half = (int)(bid % SPLIT);
+    // column cb holds (Mb + 1 - cb) blocks; S(cb) = cb (Mb + 1) - cb (cb - 1) / 2
+    const int64_t q = bid / SPLIT + S(cb_lo, Mb);
+    const double a = (double)Mb + 1.5;
+    int64_t cb = (int64_t)(a - sqrt(a * a - 2.0 * (double)q));
+    while (cb > 0 && S(cb, Mb) > q) --cb;
+    while (S(cb + 1, Mb) <= q) ++cb;
+    const int64_t rb = cb + (q - S(cb, Mb));
+    const int64_t c0 = (int64_t)(k + 1) * L.nb;
+    const int64_t gc = c0 + cb * 128 + half * BN;  // global column of the tile
+    const int64_t gr = c0 + rb * 128;              // global row of the tile (N.. = z block)
+    const int64_t kb = (int64_t)k * L.nb;
+    const double* Pk = ws + L.off(k);
+    const int64_t ldk = L.ld(k);
+    t.A = Pk + (gr - kb);
+    t.B = Pk + (gc - kb);
+    t.lda = ldk;
+    t.ldb = ldk;
+    const int J = (int)(gc / L.nb);
+    const int64_t Jb = (int64_t)J * L.nb;
+    t.ldc = L.ld(J);
+    t.C = ws + L.off(J) + (gc - Jb) * t.ldc + (gr - Jb);
+    t.K = L.nb;
+    t.m_valid = BM;
+    t.n_valid = BN;
+    return true;
+  }
+  __host__ int64_t blocks(int /*BM*/, int BN) const { return (S(cb_hi, Mb) - S(cb_lo, Mb)) * (128 / BN); }
+};
+
+template <int BM_, int BN_, int BK_, int WARPS_M_, int WARPS_N_, int STAGES_, int MINB_>
+struct Cfg {
+  static constexpr int BM = BM_, BN = BN_, BK = BK_, WARPS_M = WARPS_M_, WARPS_N = WARPS_N_, STAGES = STAGES_,
+                       MINB = MINB_;
+  static constexpr int NT = WARPS_M * WARPS_N * 32;
+  static constexpr int LDA_S = BM + 4, LDB_S = BN + 4;  // = 4 (mod 16) doubles
+  static constexpr int SMEM = STAGES * BK * (LDA_S + LDB_S) * (int)sizeof(double);
+};
+
+template <class C, bool ACC, class Map>
+__global__ void __launch_bounds__(C::NT, C::MINB) gemm_nt_dmma(Map map, const int* __restrict__ info) {
+  constexpr int BM = C::BM, BN = C::BN, BK = C::BK, STAGES = C::STAGES, NT = C::NT;
+  constexpr int LDA_S = C::LDA_S, LDB_S = C::LDB_S;
+  constexpr int WM = BM / C::WARPS_M, WN = BN / C::WARPS_N;
+  constexpr int MI = WM / 8, NI = WN / 8;
+  static_assert(BK % 4 == 0 && WM % 8 == 0 && WN % 8 == 0, "tile shape");
+  static_assert((LDA_S % 16) == 4 && (LDB_S % 16) == 4, "conflict-free fragment loads");
+
+  GemmTile t;
+  if (!map.template operator()<BM, BN>((int64_t)blockIdx.x, t)) return;
+
+  extern __shared__ __align__(16) double smem[];
+  double* sA = smem;
+  double* sB = smem + STAGES * BK * LDA_S;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp % C::WARPS_M, wn = warp / C::WARPS_M;
+  const int KT = t.K / BK;
+
+  auto load_stage = [&](int slot, int kt) {
+    double* a_s = sA + slot * BK * LDA_S;
+    double* b_s = sB + slot * BK * LDB_S;
+    constexpr int CA = BK * BM / 2;  // 16-byte chunks
+#pragma unroll
+    for (int c = tid; c < CA; c += NT) {
+      const int col = c / (BM / 2), row = (c % (BM / 2)) * 2;
+      cp_async16(a_s + col * LDA_S + row, t.A + (int64_t)(kt * BK + col) * t.lda + row);
+    }
+    constexpr int CB = BK * BN / 2;
+#pragma unroll
+    for (int c = tid; c < CB; c += NT) {
+      const int col = c / (BN / 2), row = (c % (BN / 2)) * 2;
+      cp_async16(b_s + col * LDB_S + row, t.B + (int64_t)(kt * BK + col) * t.ldb + row);
+    }
+  };
+
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < KT) load_stage(s, s);
+    cp_async_commit();
+  }
+  // A failed pivot upstream makes the rest of the factorization meaningless: exit
+  // (checked after the prologue loads are in flight, to hide the load latency).
+  if (info != nullptr && *(volatile const int*)info != 0) {
+    cp_async_wait<0>();
+    return;
+  }
+
+  double acc[MI][NI][2];
+#pragma unroll
+  for (int i = 0; i < MI; ++i)
+#pragma unroll
+    for (int j = 0; j < NI; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  const int fr = lane >> 2, fk = lane & 3;
+  for (int kt = 0; kt < KT; ++kt) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    {
+      const int nk = kt + STAGES - 1;
+      if (nk < KT) load_stage(nk % STAGES, nk);
+      cp_async_commit();
+    }
+    const double* a_s = sA + (kt % STAGES) * BK * LDA_S + wm * WM + fr;
+    const double* b_s = sB + (kt % STAGES) * BK * LDB_S + wn * WN + fr;
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      double af[MI], bf[NI];
+#pragma unroll
+      for (int i = 0; i < MI; ++i) af[i] = a_s[(kk + fk) * LDA_S + i * 8];
+#pragma unroll
+      for (int j = 0; j < NI; ++j) bf[j] = b_s[(kk + fk) * LDB_S + j * 8];
+#pragma unroll
+      for (int i = 0; i < MI; ++i)
+#pragma unroll
+        for (int j = 0; j < NI; ++j) dmma(acc[i][j], af[i], bf[j]);
+    }
+  }
+  cp_async_wait<0>();
+  if (!ACC) __syncthreads();  // C may alias A: every warp must be done reading
+
+#pragma unroll
+  for (int i = 0; i < MI; ++i) {
+    const int r = wm * WM + i * 8 + fr;
+    if (r >= t.m_valid) continue;
+#pragma unroll
+    for (int j = 0; j < NI; ++j) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int c = wn * WN + j * 8 + fk * 2 + e;
+        if (c >= t.n_valid) continue;
+        double* p = t.C + (int64_t)c * t.ldc + r;
+        if (ACC) *p = *p - acc[i][j][e];
+        else *p = acc[i][j][e];
+      }
+    }
+  }
+}
+
+template <class C, bool ACC, class Map>
+cudaError_t set_smem() {
+  return cudaFuncSetAttribute(gemm_nt_dmma<C, ACC, Map>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+}
+
+template <class C, bool ACC, class Map>
+void launch(const Map& map, const int* info, cudaStream_t s) {
+  const int64_t nblk = map.blocks(C::BM, C::BN);
+  if (nblk <= 0) return;
+  gemm_nt_dmma<C, ACC, Map><<<(unsigned)nblk, C::NT, C::SMEM, s>>>(map, info);
+}
+
+}  // namespace gemm
+}  // namespace exageo

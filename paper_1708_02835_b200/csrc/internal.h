@@ -63,9 +63,11 @@ void launch_matern_dense(const MaternConsts& mc, int64_t m, const double* x1, co
 // Variant tuned for N = 64 panel columns.
 void launch_gemm_panel(int64_t M, int N, int K, const double* A, int64_t lda, const double* B, int64_t ldb,
                        double* C, int64_t ldc, bool accumulate, const int* info, cudaStream_t s);
-// Trailing update of step k: for all 128x128 blocks (rb >= cb) of columns >= (k+1) nb,
+// Trailing update of step k: for the 128x128 blocks (rb >= cb) of columns >= (k+1) nb,
 // rows >= (k+1) nb including the z row block: A_rc -= sum_t L_rt L_ct over panel k.
-void launch_syrk_trailing(const Layout& L, double* ws, int k, const int* info, cudaStream_t s);
+// Restricted to 128-column blocks cb in [cb_lo, cb_hi) (cb_hi < 0: to the end).
+void launch_syrk_trailing(const Layout& L, double* ws, int k, int cb_lo, int cb_hi, const int* info,
+                          cudaStream_t s);
 // Factor the PB x PB diagonal block at `a` (ld) in place, write W = L^{-1} (PB x PB,
 // ld PB) and slot = sum log L_ii; info = first bad global pivot + 1.
 void launch_potrf_block(double* a, int64_t lda, double* W, double* logdet_slot, int* info, int64_t pivot_base,
