@@ -1,0 +1,314 @@
+#!/usr/bin/env python3
+"""bench.py -- exact Gaussian log-likelihood evaluations per second on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--n 100000] [--impl reference]
+
+One "step" = one whole evaluation of the hot path (Alg. 2): Matern
+generation + tiled Cholesky with fused forward solve + log-det/dot reduction,
+at BASELINE.json's headline workload (n = 100k jittered-grid locations,
+theta = (1, 0.1, 0.5), z = L(theta) e from a fixed seed; configs[2]).
+Inputs (40.6 GB of tiles) are far larger than L2, so no flush is needed.
+
+Prints ONE JSON line (rank 0). `value` = evaluations/s of the whole job with
+inputs resident in HBM (exageo_loglik_dev); `e2e` = the same through the
+host-pointer API exageo_loglik with pinned host buffers (H2D of x, y, z and
+D2H of the result inside the timed region). `roofline` reports the dominant
+kernel (the bulk DMMA trailing update) against the measured FP64 DMMA peak.
+`--impl reference` times the CPU oracle (oracle/, the reference arm of this
+tier) on a bounded sample and scales it to the same metric.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "loglik evals/sec at n=100k (1 GPU)"
+UNIT = "evals/s"
+THETA = (1.0, 0.1, 0.5)
+SEED = 1
+# Peak FP64 (DMMA) of this B200: measured by tools/probes/fp64_peak.cu (sustained
+# DMMA.8x8x4 loop, 148 SMs at 1965 MHz) = 148 * 128 flop/clk * 1.965 GHz.
+FP64_PEAK_TFLOPS = 37.2
+FP64_PEAK_SOURCE = "measured: tools/probes/fp64_peak.cu sustained DMMA (= 148 SM x 128 flop/clk x 1.965 GHz)"
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi sampling of SM clock / throttle reasons during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.f = tempfile.NamedTemporaryFile("w+", delete=False, suffix=".csv")
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.f.flush()
+        rows = []
+        with open(self.f.name) as fh:
+            for line in fh:
+                p = [v.strip() for v in line.split(",")]
+                if len(p) >= 7:
+                    try:
+                        rows.append((float(p[0]), float(p[1]), float(p[2]), p[3:7]))
+                    except ValueError:
+                        pass
+        os.unlink(self.f.name)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        loaded = [r for r in rows if r[2] > 300.0] or rows
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in loaded for i, v in enumerate(r[3]) if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(r[0] for r in loaded), "sm_max_mhz": max(r[1] for r in rows),
+                "power_w_max": max(r[2] for r in rows), "samples": len(rows), "reasons": reasons}
+
+
+# ----------------------------------------------------------------------------- oracle baseline
+def oracle_sample(n_sample: int, n_target: int):
+    """Time the CPU oracle on a bounded sample and scale to one evaluation at n_target.
+
+    Generation (O(n^2) Matern/Bessel evaluations) and factorization+solve (O(n^3))
+    are timed separately and scaled by (n_target/n_sample)^2 and ^3."""
+    import numpy as np
+
+    import oracle
+    import synth_inputs as si
+
+    x, y = oracle.gen_locations(n_sample, SEED)
+    z = si.normals(n_sample, SEED)
+    t0 = time.perf_counter()
+    S = oracle.cov(x, y, x, y, THETA)
+    t1 = time.perf_counter()
+    L = oracle.cholesky(S)
+    w = oracle.forward(L, z)
+    _ = float(2 * np.log(np.diag(L)).sum() + w @ w)
+    t2 = time.perf_counter()
+    r = n_target / n_sample
+    t_target = (t1 - t0) * r**2 + (t2 - t1) * r**3
+    return {"t_gen": t1 - t0, "t_chol": t2 - t1, "t_total": t2 - t0, "t_target": t_target,
+            "cores": oracle.num_threads()}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    n_sample = args.ref_sample
+    for _ in range(args.warmup):
+        oracle_sample(max(64, n_sample // 4), args.n)
+    vals, t_steps = [], []
+    last = None
+    for _ in range(args.steps):
+        last = oracle_sample(n_sample, args.n)
+        vals.append(1.0 / last["t_target"])
+        t_steps.append(last["t_total"])
+    value = statistics.mean(vals)
+    sample = (f"oracle Alg. 2 at n={n_sample} (same jittered grid, theta={THETA}); generation timed and scaled "
+              f"by (n/{n_sample})^2, Cholesky+solve by (n/{n_sample})^3 to n={args.n}")
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * statistics.mean(t_steps), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "impl": "reference",
+        "config": {"workload": f"loglik n={args.n} theta={THETA} (BASELINE configs[2])", "n": args.n,
+                   "sample_n": n_sample},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": last["cores"], "kind": "oracle", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------- GPU arm
+def run_gpu(args):
+    import numpy as np
+    import torch
+
+    import paper_1708_02835_b200 as ex
+    import synth_inputs as si
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.gpus != world:
+        log(f"note: --gpus {args.gpus} but WORLD_SIZE={world}; using WORLD_SIZE")
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    stream = torch.cuda.Stream(device=local)
+    ctx = ex.Context(device=local, stream=stream)
+    n = args.n
+    # inputs: jittered grid (Sec. 7.1) and z = L(theta) e (Alg. 1) -- untimed
+    x, y = ex.gen_locations(n, SEED)
+    e = si.normals(n, SEED + rank)
+    t0 = time.time()
+    z = ctx.simulate(x, y, e, THETA)
+    log(f"[rank {rank}] inputs ready (simulate {time.time() - t0:.1f}s)")
+    X, Y, Z = (torch.from_numpy(a).to(f"cuda:{local}") for a in (x, y, z))
+    torch.cuda.synchronize()
+
+    # ---- device-resident arm (value) ----
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            r = ctx.loglik_dev(X, Y, Z, THETA)
+    barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    infos = []
+    with torch.cuda.stream(stream):
+        ev0.record(stream)
+        for _ in range(args.steps):
+            r = ctx.loglik_dev(X, Y, Z, THETA)
+            infos.append(r.info)
+        ev1.record(stream)
+    barrier()
+    clk = clocks.stop()
+    ms = ev0.elapsed_time(ev1)
+    ms_max = ms
+    if dist is not None:
+        t = torch.tensor([ms], device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_max = float(t.item())
+    ms_per_step = ms_max / args.steps
+    value = world * args.steps / (ms_max / 1e3)
+
+    # ---- end-to-end arm (host pointers, pinned buffers, H2D + D2H per step) ----
+    hx, hy, hz = (torch.from_numpy(a).pin_memory() for a in (x, y, z))
+    with torch.cuda.stream(stream):
+        r_e2e = ctx.loglik(hx.numpy(), hy.numpy(), hz.numpy(), THETA)
+    barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e2e_steps = max(1, min(args.steps, 3))
+    with torch.cuda.stream(stream):
+        e0.record(stream)
+        for _ in range(e2e_steps):
+            r_e2e = ctx.loglik(hx.numpy(), hy.numpy(), hz.numpy(), THETA)
+        e1.record(stream)
+    barrier()
+    ms_e2e = e0.elapsed_time(e1)
+    if dist is not None:
+        t = torch.tensor([ms_e2e], device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_e2e = float(t.item())
+    e2e_value = world * e2e_steps / (ms_e2e / 1e3)
+
+    # ---- per-evaluation breakdown and roofline of the dominant kernel ----
+    tr_ms = sum(i["ms_trailing"] for i in infos)
+    tr_fl = sum(i["trailing_flops"] for i in infos)
+    tr_n = sum(i["trailing_launches"] for i in infos)
+    achieved = tr_fl / (tr_ms * 1e-3) / 1e12 if tr_ms > 0 else None
+    chol_ms = statistics.mean(i["ms_chol"] for i in infos)
+    chol_tf = (n**3 / 3.0) / (chol_ms * 1e-3) / 1e12
+    launches = sum(i["kernels"] for i in infos)
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "trailing_dram_bytes.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    result = None
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            s = oracle_sample(args.cpu_sample, n)
+            cpu = {"value": 1.0 / s["t_target"], "unit": UNIT, "cores": s["cores"], "kind": "oracle",
+                   "sample": (f"oracle Alg. 2 at n={args.cpu_sample} on host cores ({s['t_total']:.1f}s: "
+                              f"gen {s['t_gen']:.1f}s scaled (n/{args.cpu_sample})^2, chol+solve "
+                              f"{s['t_chol']:.1f}s scaled (n/{args.cpu_sample})^3 to n={n})")}
+        result = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"loglik n={n} theta={THETA} jittered grid, z=L e (BASELINE configs[2])",
+                       "n": n, "nb": infos[-1]["nb"], "tiles": infos[-1]["ntiles"],
+                       "parallelism": "replicas" if world > 1 else "single",
+                       "l2": "inputs (40.6 GB tiles) >> L2; no flush needed"},
+            "loglik": r.loglik,
+            "phase_ms": {"gen": statistics.mean(i["ms_gen"] for i in infos), "chol_and_solve": chol_ms,
+                         "reduce": statistics.mean(i["ms_reduce"] for i in infos)},
+            "cholesky_tflops": chol_tf,
+            "cholesky_frac_fp64_peak": chol_tf / FP64_PEAK_TFLOPS,
+            "roofline": {"bound": "tensor", "kernel": "gemm_nt_dmma<SyrkMap> (bulk trailing update U2)",
+                         "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                         "frac": (achieved / FP64_PEAK_TFLOPS) if achieved else None, "traffic": traffic,
+                         "launches": tr_n, "share_of_step": (tr_ms / args.steps) / ms_per_step,
+                         "peak_source": FP64_PEAK_SOURCE,
+                         "flops_per_launch": "2*nb per (row, col) pair of the true lower triangle updated "
+                                             "(+ z row), see DESIGN.md"},
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 3 * 8 * n,
+                    "d2h_bytes_per_step": 3 * 8 + 4, "steps": e2e_steps},
+            "gpu_launches": launches,
+            "clocks": clk,
+        }
+        print(json.dumps(result), flush=True)
+    ctx.close()
+    if dist is not None:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--n", type=int, default=100_000)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-sample", type=int, default=3000)
+    ap.add_argument("--ref-sample", type=int, default=2000)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_gpu(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -72,6 +72,11 @@ typedef struct {
   double ms_chol;     /* device time of factorization + fused forward solve   */
   double ms_reduce;   /* device time of the log-det / dot reduction            */
   int64_t kernels;    /* number of kernel launches this evaluation issued     */
+  /* dominant kernel (the bulk trailing update U2 of each step): */
+  int64_t trailing_launches; /* launches of the bulk trailing-update kernel          */
+  double ms_trailing;        /* sum of their durations (CUDA events on their stream) */
+  double trailing_flops;     /* algorithmic flops of those launches: 2 nb per (row, column)
+                                pair of the true lower triangle updated, incl. the z row */
 } exageo_loglik_info;
 
 /* Human-readable name of a status. Never NULL. */

@@ -17,6 +17,7 @@
 #include <cstring>
 #include <limits>
 #include <string>
+#include <vector>
 
 #include "../../include/exageo.h"
 #include "internal.h"
@@ -52,6 +53,10 @@ struct exageo_ctx {
   // lookahead schedule: two prioritised internal streams and their events
   cudaStream_t s_la = nullptr, s_main = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_F = nullptr, ev_U2 = nullptr, ev_join[2] = {nullptr, nullptr};
+  // timing of the dominant kernel (bulk trailing update U2): one event pair per launch
+  std::vector<cudaEvent_t> ev_u2_beg, ev_u2_end;
+  int n_u2 = 0;
+  double u2_flops = 0.0;
   int64_t kernels = 0;
   std::string err;
 };
@@ -216,6 +221,8 @@ exageo_status do_factor(exageo_ctx* c) {
   if (!c->have_matrix) return fail(c, EXAGEO_EINVAL, "no generated matrix in the workspace");
   const Layout& L = c->L;
   const int cpt = L.nb / 128;  // 128-column blocks per tile column
+  c->n_u2 = 0;
+  c->u2_flops = 0.0;
   CUDA_TRY(c, cudaEventRecord(c->ev_fork, c->stream));
   CUDA_TRY(c, cudaStreamWaitEvent(c->s_la, c->ev_fork, 0));
   CUDA_TRY(c, cudaStreamWaitEvent(c->s_main, c->ev_fork, 0));
@@ -229,7 +236,19 @@ exageo_status do_factor(exageo_ctx* c) {
     CUDA_TRY(c, cudaEventRecord(c->ev_F, c->s_la));
     c->kernels += 1;
     if (k + 2 < L.T) {
+      if ((int)c->ev_u2_beg.size() <= c->n_u2) {
+        cudaEvent_t b, e;
+        CUDA_TRY(c, cudaEventCreate(&b));
+        CUDA_TRY(c, cudaEventCreate(&e));
+        c->ev_u2_beg.push_back(b);
+        c->ev_u2_end.push_back(e);
+      }
+      CUDA_TRY(c, cudaEventRecord(c->ev_u2_beg[c->n_u2], c->s_main));
       launch_syrk_trailing(L, c->ws, k, cpt, -1, c->info, c->s_main);  // U2(k)
+      CUDA_TRY(c, cudaEventRecord(c->ev_u2_end[c->n_u2], c->s_main));
+      ++c->n_u2;
+      const double m = (double)(L.n - (int64_t)(k + 2) * L.nb);  // true columns updated
+      if (m > 0) c->u2_flops += 2.0 * L.nb * (m * (m + 1) / 2 + m);
       c->kernels += 1;
     }
     CUDA_TRY(c, cudaEventRecord(c->ev_U2, c->s_main));
@@ -302,6 +321,14 @@ exageo_status loglik_device(exageo_ctx* c, const exageo_theta* t, int64_t n, con
     cudaEventElapsedTime(&ms, c->ev[2], c->ev[3]);
     info->ms_reduce = ms;
     info->kernels = c->kernels - k0;
+    info->trailing_launches = c->n_u2;
+    info->trailing_flops = c->u2_flops;
+    double tr = 0.0;
+    for (int i = 0; i < c->n_u2; ++i) {
+      cudaEventElapsedTime(&ms, c->ev_u2_beg[i], c->ev_u2_end[i]);
+      tr += ms;
+    }
+    info->ms_trailing = tr;
   }
   return st;
 }
@@ -391,6 +418,8 @@ void exageo_destroy(exageo_ctx* c) {
     if (ev) cudaEventDestroy(ev);
   for (cudaEvent_t ev : {c->ev_fork, c->ev_F, c->ev_U2, c->ev_join[0], c->ev_join[1]})
     if (ev) cudaEventDestroy(ev);
+  for (cudaEvent_t ev : c->ev_u2_beg) cudaEventDestroy(ev);
+  for (cudaEvent_t ev : c->ev_u2_end) cudaEventDestroy(ev);
   if (c->s_la) cudaStreamDestroy(c->s_la);
   if (c->s_main) cudaStreamDestroy(c->s_main);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
