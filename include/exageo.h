@@ -162,6 +162,12 @@ exageo_status exageo_read_lower(exageo_ctx* ctx, double* dst, int64_t ld);
 /* Copy the current z row (z after generate, y = L^{-1} z after factor) to the
  * host array dst (n doubles). Synchronises. */
 exageo_status exageo_read_zrow(exageo_ctx* ctx, double* dst);
+/* Gather count entries (rows[i], cols[i]) of the current workspace matrix,
+ * 0 <= cols[i] <= rows[i] < n (host int64 arrays), into host out[count]
+ * (sampled full-size checks). EXAGEO_EINVAL on an index outside the lower
+ * triangle. Synchronises. */
+exageo_status exageo_read_entries(exageo_ctx* ctx, int64_t count, const int64_t* rows, const int64_t* cols,
+                                  double* out);
 
 #ifdef __cplusplus
 }

@@ -70,6 +70,7 @@ SIGNATURES = [
     ("exageo_stage_finish", ctypes.c_int, [_C, _f64p, _i64p]),
     ("exageo_read_lower", ctypes.c_int, [_C, _f64p, ctypes.c_int64]),
     ("exageo_read_zrow", ctypes.c_int, [_C, _f64p]),
+    ("exageo_read_entries", ctypes.c_int, [_C, ctypes.c_int64, _i64p, _i64p, _f64p]),
 ]
 
 _lib = None
@@ -264,6 +265,15 @@ class Context:
         buf = np.empty(n, np.float64)
         self._check(self._lib.exageo_read_zrow(self._ctx, _p(buf)))
         return buf
+
+    def read_entries(self, rows, cols) -> np.ndarray:
+        """Entries (rows[i], cols[i]), cols <= rows, of the workspace matrix."""
+        r = np.ascontiguousarray(rows, dtype=np.int64)
+        c = np.ascontiguousarray(cols, dtype=np.int64)
+        out = np.empty(r.size, np.float64)
+        self._check(self._lib.exageo_read_entries(self._ctx, r.size, r.ctypes.data_as(_i64p),
+                                                  c.ctypes.data_as(_i64p), _p(out)))
+        return out
 
 
 LOG2PI = math.log(2.0 * math.pi)

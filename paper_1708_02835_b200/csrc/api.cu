@@ -592,4 +592,33 @@ exageo_status exageo_read_zrow(exageo_ctx* c, double* dst) {
   return EXAGEO_OK;
 }
 
+exageo_status exageo_read_entries(exageo_ctx* c, int64_t count, const int64_t* rows, const int64_t* cols,
+                                  double* out) {
+  if (!c) return fail(nullptr, EXAGEO_EINVAL, "NULL ctx");
+  if (!c->have_matrix || count < 0 || (count > 0 && (!rows || !cols || !out)))
+    return fail(c, EXAGEO_EINVAL, "no matrix or NULL arrays");
+  if (count == 0) return EXAGEO_OK;
+  for (int64_t i = 0; i < count; ++i)
+    if (cols[i] < 0 || cols[i] > rows[i] || rows[i] >= c->L.n)
+      return fail(c, EXAGEO_EINVAL, "entry outside the lower triangle");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  void* d = nullptr;
+  CUDA_TRY(c, cudaMalloc(&d, sizeof(int64_t) * 2 * (size_t)count + sizeof(double) * (size_t)count));
+  int64_t* drc = (int64_t*)d;
+  double* dout = (double*)(drc + 2 * count);
+  cudaError_t e = cudaMemcpyAsync(drc, rows, sizeof(int64_t) * count, cudaMemcpyHostToDevice, c->stream);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(drc + count, cols, sizeof(int64_t) * count, cudaMemcpyHostToDevice, c->stream);
+  if (e == cudaSuccess) {
+    launch_read_entries(c->L, c->ws, count, drc, dout, c->stream);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(out, dout, sizeof(double) * count, cudaMemcpyDeviceToHost, c->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  cudaFree(d);
+  if (e != cudaSuccess) return fail(c, EXAGEO_ECUDA, std::string("read_entries: ") + cudaGetErrorString(e));
+  return EXAGEO_OK;
+}
+
 }  // extern "C"

@@ -79,6 +79,9 @@ void launch_finish(const Layout& L, const double* ws, const double* slots, int n
 // Copy the lower triangle of the workspace matrix to dense column-major dst (device).
 void launch_read_lower(const Layout& L, const double* ws, double* dst, int64_t ld, cudaStream_t s);
 void launch_read_zrow(const Layout& L, const double* ws, double* dst, cudaStream_t s);
+// out[i] = entry (rc[i], rc[count + i]) of the workspace matrix (lower triangle / z row).
+void launch_read_entries(const Layout& L, const double* ws, int64_t count, const int64_t* rc, double* out,
+                         cudaStream_t s);
 // z = L e with L the factor in the workspace (Alg. 1 l.7, dtrmm): lower TRMV.
 // part: scratch of T * N doubles.
 void launch_trmv_lower(const Layout& L, const double* ws, const double* e, double* z, double* part,

@@ -154,6 +154,16 @@ __global__ void read_zrow_kernel(Layout L, const double* __restrict__ ws, double
   }
 }
 
+__global__ void read_entries_kernel(Layout L, const double* __restrict__ ws, int64_t count,
+                                    const int64_t* __restrict__ rc, double* __restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = rc[i], c = rc[count + i];
+    const int j = (int)(c / L.nb);
+    const int64_t jb = (int64_t)j * L.nb;
+    out[i] = ws[L.off(j) + (c - jb) * L.ld(j) + (r - jb)];
+  }
+}
+
 // TRMV stage 1: part[j][r] = sum_{c in panel j, c <= r} L[r][c] e[c]  (grid: row blocks x panels).
 __global__ void __launch_bounds__(256) trmv_partial_kernel(Layout L, const double* __restrict__ ws,
                                                            const double* __restrict__ e, double* __restrict__ part) {
@@ -208,6 +218,14 @@ void launch_read_lower(const Layout& L, const double* ws, double* dst, int64_t l
 
 void launch_read_zrow(const Layout& L, const double* ws, double* dst, cudaStream_t s) {
   read_zrow_kernel<<<128, 256, 0, s>>>(L, ws, dst);
+}
+
+void launch_read_entries(const Layout& L, const double* ws, int64_t count, const int64_t* rc, double* out,
+                         cudaStream_t s) {
+  int g = (int)((count + 255) / 256);
+  if (g > 1024) g = 1024;
+  if (g < 1) g = 1;
+  read_entries_kernel<<<g, 256, 0, s>>>(L, ws, count, rc, out);
 }
 
 void launch_trmv_lower(const Layout& L, const double* ws, const double* e, double* z, double* part,

@@ -1,0 +1,95 @@
+"""Full-size GPU parity at BASELINE's headline size (n = 100k, nb = 512, the launch
+configuration bench.py times), where the O(n^3) oracle cannot run:
+
+  * AR(1) / Kac-Murdock-Szego closed form of l (exact in O(n), nu = 1/2, collinear sites);
+  * sampled generated entries vs the oracle's Matern function;
+  * sampled entries of L L^T vs the oracle's Sigma_rc (O(n) per sample, from read-back rows of L);
+  * Alg. 1 -> Alg. 2 round trip at theta_true: y = L^{-1} (L e) = e, so quad = e^T e.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+import synth_inputs as si
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_1708_02835_b200 as ex  # noqa: E402
+
+LOG2PI = math.log(2 * math.pi)
+N = 100_000
+THETA = (1.0, 0.1, 0.5)
+
+
+def ll_tol(ll, logdet, quad, n):
+    return 1e-10 * max(abs(ll), 0.5 * abs(logdet), 0.5 * abs(quad), 0.5 * n * LOG2PI)
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    c = ex.Context(device=0)
+    yield c
+    c.close()
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).cuda()
+
+
+def test_ar1_closed_form_full_size(ctx):
+    h, t1, t2 = 2.0**-12, 1.0, 0.05
+    x, y = si.collinear_sites(N, h)
+    z = si.normals(N, 5)
+    r = ctx.loglik(x, y, z, (t1, t2, 0.5))
+    assert r.info["nb"] == 512 and r.info["ntiles"] == 196
+    rho = math.exp(-h / t2)
+    logdet = N * math.log(t1) + (N - 1) * math.log1p(-rho * rho)
+    w = np.empty(N)
+    w[0] = z[0] / math.sqrt(t1)
+    w[1:] = (z[1:] - rho * z[:-1]) / math.sqrt(t1 * (1 - rho * rho))
+    quad = float(w @ w)
+    ll = -0.5 * quad - 0.5 * logdet - 0.5 * N * LOG2PI
+    assert abs(r.loglik - ll) <= ll_tol(ll, logdet, quad, N), (r.loglik, ll)
+    assert r.logdet == pytest.approx(logdet, rel=1e-11)
+    assert r.quad == pytest.approx(quad, rel=1e-10)
+
+
+def test_sampled_entries_and_factor_residual_full_size(ctx):
+    x, y = ex.gen_locations(N, 1)
+    z = si.normals(N, 1)
+    ctx.stage_generate_dev(dev(x), dev(y), dev(z), THETA)
+    rng = np.random.default_rng(0)
+    rows = rng.integers(0, N, 3000)
+    cols = (rng.random(3000) * (rows + 1)).astype(np.int64)
+    got = ctx.read_entries(rows, cols)
+    ref = np.array([oracle.matern(math.hypot(x[r] - x[c], y[r] - y[c]) if r != c else 0.0, THETA)
+                    for r, c in zip(rows, cols)])
+    mask = ref > 1e-290
+    assert np.all(np.abs(got[mask] - ref[mask]) <= 5e-14 * ref[mask] + 1e-300)
+    ctx.stage_factor()
+    # (L L^T)_{rc} = sum_{t <= c} L_rt L_ct must reproduce Sigma_rc (the oracle's Matern value)
+    for r, c in [(99_999, 99_998), (99_999, 0), (51_234, 51_000), (77_777, 12_345), (511, 512 - 1),
+                 (512, 511), (99_000, 98_990)]:
+        t = np.arange(c + 1, dtype=np.int64)
+        Lr = ctx.read_entries(np.full(c + 1, r, np.int64), t)
+        Lc = ctx.read_entries(np.full(c + 1, c, np.int64), t)
+        s = math.fsum(Lr * Lc)
+        d = math.hypot(x[r] - x[c], y[r] - y[c]) if r != c else 0.0
+        sig = oracle.matern(d, THETA)
+        assert abs(s - sig) <= 1e-12, (r, c, s, sig)
+    ll, logdet, quad = ctx.stage_finish()
+    assert np.isfinite(ll)
+
+
+def test_simulate_roundtrip_full_size(ctx):
+    x, y = ex.gen_locations(N, 1)
+    e = si.normals(N, 3)
+    z = ctx.simulate(x, y, e, THETA)
+    r = ctx.loglik(x, y, z, THETA)
+    assert r.quad == pytest.approx(float(e @ e), rel=1e-9)
