@@ -6,10 +6,13 @@ namespace exageo {
 
 namespace {
 using namespace gemm;
-// Panel update / TRSM: 128 x 64 tiles, 8 warps of 32 x 32, 2 CTAs per SM.
-using PanelCfg = Cfg<128, 64, 16, 4, 2, 4, 2>;
-// Trailing update: 128 x 64 tiles, 8 warps of 32 x 32, 2 CTAs per SM.
-using TrailCfg = Cfg<128, 64, 16, 4, 2, 4, 2>;
+// Panel update / TRSM: 64 x 64 tiles, 4 warps of 32 x 32, BK 8 x 4 stages, 4 CTAs per SM.
+using PanelCfg = Cfg<64, 64, 8, 2, 2, 4, 4>;
+// Trailing update: 64 x 64 tiles, 4 warps of 32 x 32, BK 8 x 4 stages, 4 CTAs per SM
+// (tools/gemm_tune.cu at n=100k: 33.8 TF vs 30.3 for 128x64 at 2 CTAs/SM).
+using TrailCfg = Cfg<64, 64, 8, 2, 2, 4, 4>;
+// Rasterization band (128-column blocks swept together, see SyrkMap).
+constexpr int kTrailBand = 8;
 }  // namespace
 
 cudaError_t gemm_init() {
@@ -49,6 +52,7 @@ void launch_syrk_trailing(const Layout& L, double* ws, int k, int cb_lo, int cb_
   map.cb_lo = cb_lo < 0 ? 0 : cb_lo;
   map.cb_hi = (cb_hi < 0 || cb_hi > map.Mb) ? map.Mb : cb_hi;
   if (map.cb_hi <= map.cb_lo) return;
+  map.band = kTrailBand;
   launch<TrailCfg, true>(map, info, s);
 }
 

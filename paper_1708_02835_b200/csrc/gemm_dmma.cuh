@@ -59,7 +59,7 @@ struct DenseMap {
   int N, K;
   int mblocks;
   template <int BM, int BN>
-  __device__ __forceinline__ bool operator()(int64_t bid, GemmTile& t) const {
+  __host__ __device__ __forceinline__ bool operator()(int64_t bid, GemmTile& t) const {
     const int64_t bm = bid % mblocks, bn = bid / mblocks;
     t.A = A + bm * BM;
     t.B = B + bn * BN;
@@ -80,7 +80,10 @@ struct DenseMap {
 // Square 128-blocks (rb >= cb) of the trailing matrix, rows/cols >= c0 = (k+1) nb;
 // row block rb == Mb is the z row block. A 128-col block is split into
 // 128/BN CTA tiles (consecutive bids share the row block).
-// Enumeration: column by column, row blocks top to bottom.
+// Rasterization: the column blocks [cb_lo, cb_hi) are cut into bands of `band`
+// column blocks; a band is swept row block by row block (the rows' A operand is
+// reused `band` times back to back, the band's B operands stay L2-resident for
+// the whole sweep), bands left to right.
 struct SyrkMap {
   Layout L;
   double* ws;
@@ -88,22 +91,51 @@ struct SyrkMap {
   int Mb;      // number of square 128-blocks in the trailing matrix
   int cb_lo;   // first 128-column block of this launch (0 = column (k+1) nb)
   int cb_hi;   // one past the last 128-column block (<= Mb)
-  __host__ __device__ static int64_t S(int64_t c, int Mb) { return c * (Mb + 1) - c * (c - 1) / 2; }
+  int band;    // column blocks per band (>= 1)
+
+  __host__ __device__ int64_t band_count(int64_t b) const {
+    const int64_t bs = cb_lo + b * band;
+    const int64_t w = (cb_hi - bs) < band ? (cb_hi - bs) : band;
+    return w * (w + 1) / 2 + ((int64_t)Mb - bs - w + 1) * w;
+  }
+  __host__ __device__ int nbands() const { return (cb_hi - cb_lo + band - 1) / band; }
+
   template <int BM, int BN>
-  __device__ __forceinline__ bool operator()(int64_t bid, GemmTile& t) const {
-    static_assert(BM == 128 && (BN == 128 || BN == 64), "SyrkMap: 128 x {64,128} tiles");
-    constexpr int SPLIT = 128 / BN;
-    const int half = (int)(bid % SPLIT);
-    // column cb holds (Mb + 1 - cb) blocks; S(cb) = cb (Mb + 1) - cb (cb - 1) / 2
-    const int64_t q = bid / SPLIT + S(cb_lo, Mb);
-    const double a = (double)Mb + 1.5;
-    int64_t cb = (int64_t)(a - sqrt(a * a - 2.0 * (double)q));
-    while (cb > 0 && S(cb, Mb) > q) --cb;
-    while (S(cb + 1, Mb) <= q) ++cb;
-    const int64_t rb = cb + (q - S(cb, Mb));
+  __host__ __device__ __forceinline__ bool operator()(int64_t bid, GemmTile& t) const {
+    static_assert((BM == 128 || BM == 64) && (BN == 128 || BN == 64), "SyrkMap: {64,128} x {64,128} tiles");
+    constexpr int SPLIT_C = 128 / BN, SPLIT = (128 / BM) * SPLIT_C;
+    const int sub = (int)(bid % SPLIT);
+    const int half = sub % SPLIT_C, rhalf = sub / SPLIT_C;
+    const int64_t q = bid / SPLIT;
+    // band index: largest b with Sfull(b) <= q (exact integer fix-up after a sqrt guess)
+    const int nb_ = nbands();
+    const double G = (double)band, A0 = (double)Mb - cb_lo - band + 1;
+    const double beta = G * (A0 + G + 0.5);
+    const double disc = beta * beta - 2.0 * G * G * (double)q;
+    int64_t b = (int64_t)((beta - sqrt(disc > 0.0 ? disc : 0.0)) / (G * G));
+    if (b >= nb_) b = nb_ - 1;
+    if (b < 0) b = 0;
+    while (b > 0 && Sfull(b) > q) --b;
+    while (b + 1 < nb_ && Sfull(b + 1) <= q) ++b;
+    int64_t qq = q - Sfull(b);
+    const int64_t bs = cb_lo + b * band;
+    const int64_t w = (cb_hi - bs) < band ? (cb_hi - bs) : band;
+    int64_t rb, cb;
+    const int64_t head = w * (w + 1) / 2;
+    if (qq < head) {
+      int64_t i = (int64_t)((sqrt(8.0 * (double)qq + 1.0) - 1.0) * 0.5);
+      while (i > 0 && i * (i + 1) / 2 > qq) --i;
+      while ((i + 1) * (i + 2) / 2 <= qq) ++i;
+      rb = bs + i;
+      cb = bs + (qq - i * (i + 1) / 2);
+    } else {
+      qq -= head;
+      rb = bs + w + qq / w;
+      cb = bs + qq % w;
+    }
     const int64_t c0 = (int64_t)(k + 1) * L.nb;
     const int64_t gc = c0 + cb * 128 + half * BN;  // global column of the tile
-    const int64_t gr = c0 + rb * 128;              // global row of the tile (N.. = z block)
+    const int64_t gr = c0 + rb * 128 + rhalf * BM; // global row of the tile (N.. = z block)
     const int64_t kb = (int64_t)k * L.nb;
     const double* Pk = ws + L.off(k);
     const int64_t ldk = L.ld(k);
@@ -120,7 +152,17 @@ struct SyrkMap {
     t.n_valid = BN;
     return true;
   }
-  __host__ int64_t blocks(int /*BM*/, int BN) const { return (S(cb_hi, Mb) - S(cb_lo, Mb)) * (128 / BN); }
+  // number of 128x128 blocks of all bands before band b, every one of them full
+  __host__ __device__ int64_t Sfull(int64_t b) const {
+    const int64_t G = band, A0 = (int64_t)Mb - cb_lo - G + 1;
+    // sum_{b'<b} [G(G+1)/2 + (A0 - b' G) G]
+    return b * (G * (G + 1) / 2) + G * (b * A0 - G * (b * (b - 1) / 2));
+  }
+  __host__ int64_t blocks(int BM, int BN) const {
+    int64_t tot = 0;
+    for (int b = 0; b < nbands(); ++b) tot += band_count(b);
+    return tot * (128 / BN) * (128 / BM);
+  }
 };
 
 template <int BM_, int BN_, int BK_, int WARPS_M_, int WARPS_N_, int STAGES_, int MINB_>
@@ -189,6 +231,14 @@ __global__ void __launch_bounds__(C::NT, C::MINB) gemm_nt_dmma(Map map, const in
 
   const int fr = lane >> 2, fk = lane & 3;
   for (int kt = 0; kt < KT; ++kt) {
+    if (ACC && kt == KT / 2) {
+      // pull this tile's C into L2 ahead of the read-modify-write epilogue (128-byte lines)
+      constexpr int LPC = BM / 16;  // lines per column
+      for (int l = tid; l < BN * LPC; l += NT) {
+        const double* p = t.C + (int64_t)(l / LPC) * t.ldc + (l % LPC) * 16;
+        asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p));
+      }
+    }
     cp_async_wait<STAGES - 2>();
     __syncthreads();
     {

@@ -22,64 +22,76 @@ namespace {
 
 constexpr int LDS_P = PB + 1;
 
+// 256 threads: thread t owns row r = t / 4 and the 16 slots c = (t % 4) + 4 s of it, in
+// registers. Slot c holds a_rc (the Schur complement, unscaled) while c > j and, from step
+// c on, w_rc of W = L^{-1} (unscaled). Step j: the owners of row j publish W's row j to
+// shared memory (column j of A was published at step j-1), one barrier, then every row
+// r > j applies, with d_j = a_jj and f = a_rj / d_j,
+//   c >  j: a_rc -= f a_cj        (right-looking Cholesky; L_jj = sqrt d_j, L_rj = a_rj / L_jj)
+//   c <= j: w_rc -= f w_jc        (right-looking L W = I;  W_jc = w_jc / L_jj, w_jj = 1)
+// and the owner of column j+1 publishes a_r,j+1. Scaling is deferred to the write-out.
 __global__ void __launch_bounds__(256) potrf_block_kernel(double* __restrict__ a, int64_t lda, double* __restrict__ W,
                                                           double* __restrict__ slot, int* __restrict__ info,
                                                           int64_t pivot_base) {
   if (*(volatile int*)info != 0) return;
   extern __shared__ double smem_p[];
-  double* s = smem_p;               // column-major, s[c * LDS_P + r]
-  double* w = smem_p + PB * LDS_P;  // W = L^{-1}, same layout
-  __shared__ int bad;
+  double* colA = smem_p;               // colA[j * LDS_P + r] = a_rj at step j (unscaled)
+  double* rowW = smem_p + PB * LDS_P;  // rowW[j * LDS_P + c] = w_jc at step j (unscaled)
   const int tid = threadIdx.x;
-  for (int idx = tid; idx < PB * PB; idx += blockDim.x) {
-    const int r = idx % PB, c = idx / PB;
-    s[c * LDS_P + r] = (r >= c) ? a[(int64_t)c * lda + r] : 0.0;
+  const int r = tid >> 2, q = tid & 3;
+  double v[16];
+#pragma unroll
+  for (int s = 0; s < 16; ++s) {
+    const int c = q + 4 * s;
+    v[s] = (c <= r) ? a[(int64_t)c * lda + r] : 0.0;
   }
-  if (tid == 0) bad = -1;
-  __syncthreads();
+  if (q == 0) colA[r] = v[0];  // column 0
+  int bad = -1;
   for (int j = 0; j < PB; ++j) {
-    if (tid == 0) {
-      const double d = s[j * LDS_P + j];
-      if (!(d > 0.0)) bad = j;
-      else s[j * LDS_P + j] = sqrt(d);
+    if (r == j) {
+#pragma unroll
+      for (int s = 0; s < 16; ++s) {
+        const int c = q + 4 * s;
+        rowW[j * LDS_P + c] = (c < j) ? v[s] : (c == j ? 1.0 : 0.0);
+      }
     }
     __syncthreads();
-    if (bad >= 0) break;
-    const double ljj = s[j * LDS_P + j];
-    if (tid > j && tid < PB) s[j * LDS_P + tid] /= ljj;
-    __syncthreads();
-    const int m = PB - 1 - j;
-    for (int idx = tid; idx < m * m; idx += blockDim.x) {
-      const int r = j + 1 + idx % m, c = j + 1 + idx / m;
-      if (r >= c) s[c * LDS_P + r] -= s[j * LDS_P + r] * s[j * LDS_P + c];
+    const double d = colA[j * LDS_P + j];
+    if (!(d > 0.0)) {
+      bad = j;
+      break;
     }
-    __syncthreads();
+    if (r > j) {
+      const double f = colA[j * LDS_P + r] * (1.0 / d);
+#pragma unroll
+      for (int s = 0; s < 16; ++s) {
+        const int c = q + 4 * s;
+        if (c < j) {
+          v[s] -= f * rowW[j * LDS_P + c];
+        } else if (c == j) {
+          v[s] = -f;  // w_rj = 0 - f * w_jj
+        } else if (c <= r) {
+          v[s] -= f * colA[j * LDS_P + c];
+          if (c == j + 1) colA[(j + 1) * LDS_P + r] = v[s];
+        }
+      }
+    }
   }
   if (bad >= 0) {
     if (tid == 0) *info = (int)(pivot_base + bad + 1);
     return;
   }
-  // W = L^{-1}: thread t < PB owns column t (forward substitution on e_t).
-  if (tid < PB) {
-    const int t = tid;
-    for (int r = 0; r < t; ++r) w[t * LDS_P + r] = 0.0;
-    w[t * LDS_P + t] = 1.0 / s[t * LDS_P + t];
-    for (int i = t + 1; i < PB; ++i) {
-      double acc = 0.0;
-      for (int p = t; p < i; ++p) acc += s[p * LDS_P + i] * w[t * LDS_P + p];
-      w[t * LDS_P + i] = -acc / s[i * LDS_P + i];
-    }
-  }
+  __syncthreads();
   if (tid == 0) {
     double ld = 0.0;
-    for (int i = 0; i < PB; ++i) ld += log(s[i * LDS_P + i]);
+    for (int i = 0; i < PB; ++i) ld += log(sqrt(colA[i * LDS_P + i]));
     *slot = ld;
   }
-  __syncthreads();
   for (int idx = tid; idx < PB * PB; idx += blockDim.x) {
-    const int r = idx % PB, c = idx / PB;
-    a[(int64_t)c * lda + r] = (r >= c) ? s[c * LDS_P + r] : 0.0;
-    W[c * PB + r] = w[c * LDS_P + r];
+    const int rr = idx % PB, c = idx / PB;
+    const double lc = sqrt(colA[c * LDS_P + c]);
+    a[(int64_t)c * lda + rr] = (rr > c) ? colA[c * LDS_P + rr] / lc : (rr == c ? lc : 0.0);
+    W[c * PB + rr] = (rr >= c) ? rowW[rr * LDS_P + c] / sqrt(colA[rr * LDS_P + rr]) : 0.0;
   }
 }
 

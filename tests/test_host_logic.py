@@ -1,0 +1,23 @@
+"""Host-side logic of the CUDA path that needs no GPU: the trailing-update tile
+enumeration (SyrkMap: every lower 128-block of the requested column range exactly
+once, pointers consistent with the panel layout), compiled with nvcc as host code."""
+import os
+import shutil
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.mark.skipif(shutil.which("nvcc") is None and not os.path.exists("/usr/local/cuda/bin/nvcc"),
+                    reason="nvcc not available")
+def test_syrkmap_enumeration(tmp_path):
+    nvcc = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
+    exe = str(tmp_path / "test_syrkmap")
+    subprocess.check_call([nvcc, "-O2", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-I",
+                           os.path.join(ROOT, "paper_1708_02835_b200", "csrc"), "-o", exe,
+                           os.path.join(ROOT, "tools", "test_syrkmap.cu")])
+    out = subprocess.run([exe], capture_output=True, text=True)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert out.stdout.startswith("OK")

@@ -16,7 +16,7 @@ __global__ void fill(double* p, int64_t n) {
 }
 
 template <class C>
-void run(const char* name, const Layout& L, double* ws, int k, int reps) {
+void run(const char* name, const Layout& L, double* ws, int k, int reps, int band = 1) {
   if (set_smem<C, true, SyrkMap>() != cudaSuccess) {
     printf("%-40s smem attr failed\n", name);
     return;
@@ -28,6 +28,7 @@ void run(const char* name, const Layout& L, double* ws, int k, int reps) {
   map.Mb = (int)((L.N - (int64_t)(k + 1) * L.nb) / 128);
   map.cb_lo = 0;
   map.cb_hi = map.Mb;
+  map.band = band;
   const double flops = (double)map.blocks(C::BM, C::BN) * 2.0 * C::BM * C::BN * L.nb;
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
@@ -46,7 +47,7 @@ void run(const char* name, const Layout& L, double* ws, int k, int reps) {
     tot += ms;
   }
   cudaError_t err = cudaGetLastError();
-  printf("%-44s k=%d blocks=%8lld best %8.3f ms  %6.2f TF  (avg %6.2f TF) %s\n", name, k,
+  printf("%-44s band=%2d k=%d blocks=%8lld best %8.3f ms  %6.2f TF  (avg %6.2f TF) %s\n", name, band, k,
          (long long)map.blocks(C::BM, C::BN), best, flops / best / 1e9, flops / (tot / reps) / 1e9,
          err == cudaSuccess ? "" : cudaGetErrorString(err));
 }
@@ -67,14 +68,13 @@ int main(int argc, char** argv) {
   fill<<<1024, 256>>>(ws, (int64_t)(bytes / 8));
   cudaDeviceSynchronize();
   printf("n=%lld T=%d workspace %.2f GB\n", (long long)n, L.T, bytes / 1e9);
-  for (int k : {0, L.T / 2}) {
-    run<Cfg<128, 128, 16, 2, 4, 4, 1>>("128x128x16 w2x4 st4 minb1 (64x32)", L, ws, k, 3);
-    run<Cfg<128, 128, 16, 4, 4, 4, 1>>("128x128x16 w4x4 st4 minb1 (32x32)", L, ws, k, 3);
-    run<Cfg<128, 64, 16, 4, 2, 4, 2>>("128x64x16 w4x2 st4 minb2 (32x32)", L, ws, k, 3);
-    run<Cfg<128, 64, 16, 4, 2, 3, 2>>("128x64x16 w4x2 st3 minb2 (32x32)", L, ws, k, 3);
-    run<Cfg<128, 64, 32, 4, 2, 2, 2>>("128x64x32 w4x2 st2 minb2 (32x32)", L, ws, k, 3);
-    run<Cfg<128, 64, 16, 2, 2, 4, 2>>("128x64x16 w2x2 st4 minb2 (64x32)", L, ws, k, 3);
-    run<Cfg<128, 128, 32, 2, 4, 3, 1>>("128x128x32 w2x4 st3 minb1 (64x32)", L, ws, k, 3);
+  for (int k : {0}) {
+    run<Cfg<64, 64, 8, 2, 2, 4, 4>>("64x64x8 w2x2 st4 minb4 (32x32)", L, ws, k, 3, 8);
+    run<Cfg<64, 64, 8, 2, 2, 5, 4>>("64x64x8 w2x2 st5 minb4 (32x32)", L, ws, k, 3, 8);
+    run<Cfg<64, 64, 8, 2, 2, 6, 4>>("64x64x8 w2x2 st6 minb4 (32x32)", L, ws, k, 3, 8);
+    run<Cfg<64, 64, 4, 2, 2, 8, 4>>("64x64x4 w2x2 st8 minb4 (32x32)", L, ws, k, 3, 8);
+    run<Cfg<64, 64, 4, 2, 2, 12, 4>>("64x64x4 w2x2 st12 minb4 (32x32)", L, ws, k, 3, 8);
+    run<Cfg<64, 64, 8, 2, 2, 3, 4>>("64x64x8 w2x2 st3 minb4 (32x32)", L, ws, k, 3, 8);
   }
   return 0;
 }
