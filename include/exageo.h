@@ -57,6 +57,16 @@ typedef struct {
   int device;   /* CUDA device ordinal                                               */
   int nb;       /* tile size (multiple of 128); 0 = automatic (512 for n >= 10000, else 128/256) */
   void* stream; /* cudaStream_t to run on; NULL = the library creates its own stream */
+  /* Distribution: the tile panels are dealt 1-D block-cyclically over
+   * `world` ranks (panel j on rank j % world), factored with a panel broadcast per step
+   * and finished with an all-reduce. world <= 1: single GPU. */
+  int world;            /* number of ranks (one process per GPU, NCCL over NVLink)      */
+  int rank;             /* this process's rank, 0 <= rank < world                        */
+  const void* nccl_id;  /* 128-byte ncclUniqueId from exageo_nccl_unique_id on rank 0,
+                           identical on every rank (world > 1)                           */
+  int virtual_ranks;    /* > 1: run that many ranks inside this process on one device,
+                           panel broadcasts as device copies (tests the distributed
+                           schedule on one GPU); excludes world > 1                      */
 } exageo_opts;
 
 /* Per-evaluation details of exageo_loglik*. */
@@ -86,8 +96,16 @@ const char* exageo_strerror(exageo_status s);
  * when ctx is NULL). Valid until the next call on ctx. Never NULL. */
 const char* exageo_last_error(const exageo_ctx* ctx);
 
+/* Write a fresh NCCL unique id (128 bytes) to out (len >= 128). Call on rank 0 and
+ * hand the bytes to every rank's exageo_opts.nccl_id (e.g. over torch.distributed). */
+exageo_status exageo_nccl_unique_id(void* out, size_t len);
+
 /* Create a context on opts->device. opts may be NULL (device 0, automatic nb,
- * own stream). Fails with EXAGEO_ECUDA if no CUDA device is usable. */
+ * own stream, single GPU). Fails with EXAGEO_ECUDA if no CUDA device is usable.
+ * With opts->world > 1 the call is collective: every rank must call it (NCCL
+ * communicator initialisation). Every later call on a distributed context is
+ * collective too, with identical arguments on all ranks; results (l, info) are
+ * returned on every rank. */
 exageo_status exageo_create(exageo_ctx** ctx, const exageo_opts* opts);
 void exageo_destroy(exageo_ctx* ctx);
 
@@ -157,7 +175,8 @@ exageo_status exageo_stage_finish(exageo_ctx* ctx, double* out3, int64_t* npd_pi
 /* Copy the lower triangle (incl. diagonal) of the current workspace matrix
  * (Sigma after generate, L after factor) to host dense column-major
  * dst[i + j*ld], 0 <= j <= i < n; the strict upper triangle of dst is not
- * written. Synchronises. */
+ * written. Synchronises. The read_* functions return the columns held by this
+ * process (all of them unless world > 1 with NCCL; other columns read as 0). */
 exageo_status exageo_read_lower(exageo_ctx* ctx, double* dst, int64_t ld);
 /* Copy the current z row (z after generate, y = L^{-1} z after factor) to the
  * host array dst (n doubles). Synchronises. */

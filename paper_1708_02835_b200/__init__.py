@@ -32,7 +32,9 @@ class Theta(ctypes.Structure):
 
 
 class Opts(ctypes.Structure):
-    _fields_ = [("device", ctypes.c_int), ("nb", ctypes.c_int), ("stream", ctypes.c_void_p)]
+    _fields_ = [("device", ctypes.c_int), ("nb", ctypes.c_int), ("stream", ctypes.c_void_p),
+                ("world", ctypes.c_int), ("rank", ctypes.c_int), ("nccl_id", ctypes.c_void_p),
+                ("virtual_ranks", ctypes.c_int)]
 
 
 class LoglikInfo(ctypes.Structure):
@@ -52,6 +54,7 @@ _C = ctypes.c_void_p
 SIGNATURES = [
     ("exageo_strerror", ctypes.c_char_p, [ctypes.c_int]),
     ("exageo_last_error", ctypes.c_char_p, [_C]),
+    ("exageo_nccl_unique_id", ctypes.c_int, [ctypes.c_void_p, ctypes.c_size_t]),
     ("exageo_create", ctypes.c_int, [ctypes.POINTER(_C), ctypes.POINTER(Opts)]),
     ("exageo_destroy", None, [_C]),
     ("exageo_workspace_bytes", ctypes.c_size_t, [ctypes.c_int64, ctypes.c_int]),
@@ -143,16 +146,49 @@ class Result:
     info: dict
 
 
-class Context:
-    """An exageo_ctx on one CUDA device (own stream unless `stream` is given)."""
+def nccl_unique_id() -> bytes:
+    """A fresh 128-byte NCCL unique id (create on rank 0, share with every rank)."""
+    buf = ctypes.create_string_buffer(128)
+    st = load_library().exageo_nccl_unique_id(buf, 128)
+    if st != OK:
+        raise ExageoError(st, load_library().exageo_last_error(None).decode())
+    return buf.raw
 
-    def __init__(self, device: int = 0, nb: int = 0, stream=None):
+
+def exchange_nccl_id(rank: int, world: int) -> bytes:
+    """NCCL id of rank 0, broadcast to every rank over the default torch.distributed group."""
+    import torch
+    import torch.distributed as dist
+
+    t = torch.zeros(128, dtype=torch.uint8)
+    if rank == 0:
+        t = torch.frombuffer(bytearray(nccl_unique_id()), dtype=torch.uint8).clone()
+    if dist.get_backend() == "nccl":
+        tt = t.cuda()
+        dist.broadcast(tt, 0)
+        t = tt.cpu()
+    else:
+        dist.broadcast(t, 0)
+    return bytes(t.tolist())
+
+
+class Context:
+    """An exageo_ctx on one CUDA device (own stream unless `stream` is given).
+
+    Distribution: world > 1 with rank and nccl_id (bytes, identical on every rank)
+    makes a collective NCCL context; virtual_ranks > 1 runs that many ranks of the
+    distributed schedule inside this process on one device."""
+
+    def __init__(self, device: int = 0, nb: int = 0, stream=None, world: int = 1, rank: int = 0,
+                 nccl_id: bytes | None = None, virtual_ranks: int = 0):
         self._lib = load_library()
         self._ctx = ctypes.c_void_p()
         sp = None
         if stream is not None:
             sp = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
-        o = Opts(int(device), int(nb), sp)
+        self._id_buf = ctypes.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
+        idp = ctypes.cast(self._id_buf, ctypes.c_void_p) if self._id_buf is not None else None
+        o = Opts(int(device), int(nb), sp, int(world), int(rank), idp, int(virtual_ranks))
         st = self._lib.exageo_create(ctypes.byref(self._ctx), ctypes.byref(o))
         if st != OK:
             raise ExageoError(st, self._lib.exageo_last_error(None).decode())

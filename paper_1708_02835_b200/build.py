@@ -75,7 +75,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     with ThreadPoolExecutor(max_workers=min(8, max(1, len(jobs)))) as ex:
         list(ex.map(run, jobs))
     if force or jobs or _stale(objs, LIB):
-        cmd = [nvcc(), "-shared"] + ARCH + ["-cudart", "static", "-o", LIB] + objs
+        cmd = [nvcc(), "-shared"] + ARCH + ["-cudart", "static", "-o", LIB] + objs + ["-lnccl"]
         run(cmd)
     return LIB
 

@@ -3,14 +3,19 @@
 //
 //   K1 gen_panels                       Sigma(theta) lower panels + z row   (l.2)
 //   for k = 0 .. T-1                    right-looking tile Cholesky          (l.3)
-//     for s = 0 .. nb/64 - 1            left-looking factorization of panel k
+//     F(k): for s = 0 .. nb/64 - 1      left-looking factorization of panel k
 //       gemm_panel  (s > 0)             P[c0:, c0:c0+64] -= P[c0:, :c0] P[c0:c0+64, :c0]^T
 //       potrf_block                     L_ss, W = L_ss^{-1}, sum log L_ii, pivot check
 //       gemm_panel  (TRSM)              P[c0+64:, c0:c0+64] = P[c0+64:, c0:c0+64] W^T
-//     syrk_trailing(k)                  A_ij -= L_ik L_jk^T, i >= j > k (incl. z row -> forward solve, l.4)
-//   finish                              logdet, dot, l                        (l.5-7)
+//     broadcast panel k                 (world > 1: NCCL, or device copies for virtual ranks)
+//     U1/U2: syrk_panels                A_ij -= L_ik L_jk^T on owned panels > k (incl. z row ->
+//                                       forward solve of l.4)
+//   local partials + all-reduce + combine                                 (l.5-7)
 //
-// All launches are stream-ordered on the context stream.
+// Distribution: panels 1-D block-cyclic over `world` ranks; each rank
+// stores its panels, receives panel k before its step-k update. Lookahead depth 1 on
+// two prioritised streams per rank: the owner of panel k+1 updates it first (U1) and
+// factors it (F(k+1)) while every rank applies the bulk update U2(k).
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -19,47 +24,13 @@
 #include <string>
 #include <vector>
 
-#include "../../include/exageo.h"
-#include "internal.h"
+#include "context.h"
 
 namespace exageo {
 int gen_locations_host(int64_t n, uint64_t seed, double* x, double* y);
 }
 
 using namespace exageo;
-
-struct exageo_ctx {
-  int device = 0;
-  cudaStream_t stream = nullptr;
-  bool own_stream = false;
-  int nb_opt = 0;
-  // tile workspace
-  double* ws = nullptr;
-  size_t ws_bytes = 0;
-  bool ws_external = false;
-  // small device buffers
-  double* W = nullptr;      // PB x PB inverse of the current diagonal block
-  double* slots = nullptr;  // log-det partials, one per potrf block
-  int64_t slots_cap = 0;
-  double* out = nullptr;    // kOutDoubles
-  int* info = nullptr;      // 0 or first bad pivot + 1
-  double* vec = nullptr;    // 4 * n staging for host-pointer entry points
-  int64_t vec_cap = 0;
-  double* part = nullptr;   // TRMV scratch
-  size_t part_cap = 0;
-  Layout L;
-  bool have_matrix = false;
-  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
-  // lookahead schedule: two prioritised internal streams and their events
-  cudaStream_t s_la = nullptr, s_main = nullptr;
-  cudaEvent_t ev_fork = nullptr, ev_F = nullptr, ev_U2 = nullptr, ev_join[2] = {nullptr, nullptr};
-  // timing of the dominant kernel (bulk trailing update U2): one event pair per launch
-  std::vector<cudaEvent_t> ev_u2_beg, ev_u2_end;
-  int n_u2 = 0;
-  double u2_flops = 0.0;
-  int64_t kernels = 0;
-  std::string err;
-};
 
 namespace {
 
@@ -78,6 +49,13 @@ exageo_status fail(exageo_ctx* c, exageo_status s, const std::string& msg) {
       return fail((ctx), EXAGEO_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_));          \
   } while (0)
 
+#define NCCL_TRY(ctx, call)                                                                          \
+  do {                                                                                               \
+    ncclResult_t r_ = (call);                                                                        \
+    if (r_ != ncclSuccess)                                                                           \
+      return fail((ctx), EXAGEO_ENCCL, std::string(#call) + ": " + ncclGetErrorString(r_));         \
+  } while (0)
+
 bool theta_ok(const exageo_theta* t) {
   return t && std::isfinite(t->sigma2) && std::isfinite(t->beta) && std::isfinite(t->nu) && t->sigma2 > 0 &&
          t->beta > 0 && t->nu > 0;
@@ -89,12 +67,14 @@ int auto_nb(int64_t n) {
   return 128;
 }
 
-Layout make_layout(int64_t n, int nb) {
+Layout make_layout(int64_t n, int nb, int rank = 0, int world = 1) {
   Layout L;
   L.n = n;
   L.nb = nb;
   L.T = (int)((n + nb - 1) / nb);
   L.N = (int64_t)L.T * nb;
+  L.rank = rank;
+  L.world = world;
   return L;
 }
 
@@ -127,157 +107,315 @@ MaternConsts make_consts(const exageo_theta& t) {
   return c;
 }
 
-exageo_status ensure_vec(exageo_ctx* c, int64_t n) {
-  if (c->vec_cap >= n) return EXAGEO_OK;
-  if (c->vec) cudaFree(c->vec);
-  c->vec = nullptr;
-  c->vec_cap = 0;
-  CUDA_TRY(c, cudaMalloc(&c->vec, sizeof(double) * 4 * (size_t)n));
-  c->vec_cap = n;
-  return EXAGEO_OK;
-}
-
-exageo_status ensure_workspace(exageo_ctx* c, const Layout& L) {
-  const size_t need = (size_t)L.total() * sizeof(double) + 256 * sizeof(double);  // slack: masked tail reads
-  const int64_t nslots = (int64_t)L.T * (L.nb / PB);
-  if (c->slots_cap < nslots) {
-    if (c->slots) cudaFree(c->slots);
-    c->slots = nullptr;
-    CUDA_TRY(c, cudaMalloc(&c->slots, sizeof(double) * (size_t)nslots));
-    c->slots_cap = nslots;
-  }
-  if (c->ws_external) {
-    if (c->ws_bytes < need)
-      return fail(c, EXAGEO_ENOMEM, "external workspace too small: need " + std::to_string(need) + " bytes");
-    return EXAGEO_OK;
-  }
-  if (c->ws_bytes >= need) return EXAGEO_OK;
-  if (c->ws) cudaFree(c->ws);
-  c->ws = nullptr;
-  c->ws_bytes = 0;
-  size_t free_b = 0, total_b = 0;
-  CUDA_TRY(c, cudaMemGetInfo(&free_b, &total_b));
-  if (need > free_b)
-    return fail(c, EXAGEO_ENOMEM,
-                "tile workspace needs " + std::to_string(need) + " bytes, " + std::to_string(free_b) + " free");
-  cudaError_t e = cudaMalloc(&c->ws, need);
-  if (e != cudaSuccess) {
-    cudaGetLastError();
-    return fail(c, EXAGEO_ENOMEM, std::string("cudaMalloc workspace: ") + cudaGetErrorString(e));
-  }
-  c->ws_bytes = need;
-  return EXAGEO_OK;
-}
-
 exageo_status check_launch(exageo_ctx* c) {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(c, EXAGEO_ECUDA, std::string("kernel launch: ") + cudaGetErrorString(e));
   return EXAGEO_OK;
 }
 
+exageo_status ensure_vec(exageo_ctx* c, int64_t n) {
+  if (c->vec_cap >= n) return EXAGEO_OK;
+  cudaFree(c->vec);
+  cudaFree(c->zsum);
+  c->vec = c->zsum = nullptr;
+  c->vec_cap = 0;
+  CUDA_TRY(c, cudaMalloc(&c->vec, sizeof(double) * 4 * (size_t)n));
+  CUDA_TRY(c, cudaMalloc(&c->zsum, sizeof(double) * (size_t)n));
+  c->vec_cap = n;
+  return EXAGEO_OK;
+}
+
+size_t local_bytes(const Layout& L) { return (size_t)L.total() * sizeof(double) + 256 * sizeof(double); }
+
+// Allocate (or check) every rank state's panel storage, receive buffers and slots.
+exageo_status ensure_buffers(exageo_ctx* c) {
+  size_t need_all = 0;
+  for (auto& R : c->rs) {
+    need_all += R.ws_external ? 0 : (R.ws_bytes >= local_bytes(R.L) ? 0 : local_bytes(R.L));
+    if (c->world > 1 && R.recv_bytes < (size_t)R.L.ld(0) * R.L.nb * sizeof(double))
+      need_all += 2 * (size_t)R.L.ld(0) * R.L.nb * sizeof(double);
+  }
+  if (need_all > 0) {
+    size_t free_b = 0, total_b = 0;
+    CUDA_TRY(c, cudaMemGetInfo(&free_b, &total_b));
+    size_t reclaim = 0;
+    for (auto& R : c->rs) reclaim += (R.ws_external ? 0 : R.ws_bytes) + 2 * R.recv_bytes;
+    if (need_all > free_b + reclaim)
+      return fail(c, EXAGEO_ENOMEM,
+                  "tile workspace needs " + std::to_string(need_all) + " bytes, " + std::to_string(free_b) + " free");
+  }
+  for (auto& R : c->rs) {
+    const Layout& L = R.L;
+    const int64_t nslots = (int64_t)L.owned() * (L.nb / PB);
+    if (R.slots_cap < nslots || R.slots == nullptr) {
+      cudaFree(R.slots);
+      R.slots = nullptr;
+      CUDA_TRY(c, cudaMalloc(&R.slots, sizeof(double) * (size_t)(nslots > 0 ? nslots : 1)));
+      R.slots_cap = nslots;
+    }
+    if (R.ws_external) {
+      if (R.ws_bytes < local_bytes(L))
+        return fail(c, EXAGEO_ENOMEM, "external workspace too small: need " + std::to_string(local_bytes(L)));
+    } else if (R.ws_bytes < local_bytes(L)) {
+      cudaFree(R.ws);
+      R.ws = nullptr;
+      R.ws_bytes = 0;
+      cudaError_t e = cudaMalloc(&R.ws, local_bytes(L));
+      if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(c, EXAGEO_ENOMEM, std::string("cudaMalloc workspace: ") + cudaGetErrorString(e));
+      }
+      R.ws_bytes = local_bytes(L);
+    }
+    if (c->world > 1) {
+      const size_t rb = (size_t)L.ld(0) * L.nb * sizeof(double);
+      if (R.recv_bytes < rb) {
+        for (auto& p : R.recv) {
+          cudaFree(p);
+          p = nullptr;
+        }
+        R.recv_bytes = 0;
+        for (auto& p : R.recv) {
+          cudaError_t e = cudaMalloc(&p, rb);
+          if (e != cudaSuccess) {
+            cudaGetLastError();
+            return fail(c, EXAGEO_ENOMEM, std::string("cudaMalloc receive buffer: ") + cudaGetErrorString(e));
+          }
+        }
+        R.recv_bytes = rb;
+      }
+    }
+  }
+  return EXAGEO_OK;
+}
+
+// ---------------------------------------------------------------------------- generation
 exageo_status do_generate(exageo_ctx* c, const exageo_theta* t, int64_t n, const double* x, const double* y,
                           const double* z) {
   if (!theta_ok(t)) return fail(c, EXAGEO_EINVAL, "theta must be finite and > 0");
   if (n < 1 || !x || !y) return fail(c, EXAGEO_EINVAL, "n < 1 or NULL location array");
   const int nb = c->nb_opt > 0 ? c->nb_opt : auto_nb(n);
-  c->L = make_layout(n, nb);
-  exageo_status st = ensure_workspace(c, c->L);
+  c->G = make_layout(n, nb);
+  for (size_t i = 0; i < c->rs.size(); ++i) {
+    const int rank = c->virt ? (int)i : c->rank;
+    c->rs[i].L = make_layout(n, nb, rank, c->world);
+  }
+  exageo_status st = ensure_buffers(c);
   if (st != EXAGEO_OK) return st;
-  CUDA_TRY(c, cudaMemsetAsync(c->info, 0, sizeof(int), c->stream));
   const MaternConsts mc = make_consts(*t);
-  launch_gen_panels(c->L, c->ws, mc, x, y, z, c->stream);
-  c->kernels += 1;
+  for (auto& R : c->rs) {
+    CUDA_TRY(c, cudaMemsetAsync(R.info, 0, sizeof(int), c->stream));
+    launch_gen_panels(R.L, R.ws, mc, x, y, z, c->stream);
+    c->kernels += 1;
+  }
   c->have_matrix = true;
   return check_launch(c);
 }
 
-// Factor panel k (left-looking over PB-wide column blocks) on stream s.
-void factor_panel(exageo_ctx* c, int k, cudaStream_t s) {
-  const Layout& L = c->L;
+// ---------------------------------------------------------------------------- factorization
+// Factor owned panel k (left-looking over PB-wide column blocks) on stream s.
+void factor_panel(exageo_ctx* c, RankState& R, int k, cudaStream_t s) {
+  const Layout& L = R.L;
   const int nsub = L.nb / PB;
-  double* Pk = c->ws + L.off(k);
+  double* Pk = R.ws + L.off(k);
   const int64_t ldk = L.ld(k);
+  const int m = (k - L.rank) / L.world;  // local panel index
   for (int sb = 0; sb < nsub; ++sb) {
     const int64_t c0 = (int64_t)sb * PB;
     if (sb > 0) {
-      launch_gemm_panel(ldk - c0, PB, (int)c0, Pk + c0, ldk, Pk + c0, ldk, Pk + c0 * ldk + c0, ldk, true, c->info, s);
+      launch_gemm_panel(ldk - c0, PB, (int)c0, Pk + c0, ldk, Pk + c0, ldk, Pk + c0 * ldk + c0, ldk, true, R.info, s);
       c->kernels += 1;
     }
-    launch_potrf_block(Pk + c0 * ldk + c0, ldk, c->W, c->slots + (int64_t)k * nsub + sb, c->info,
+    launch_potrf_block(Pk + c0 * ldk + c0, ldk, R.W, R.slots + (int64_t)m * nsub + sb, R.info,
                        (int64_t)k * L.nb + c0, s);
     double* below = Pk + c0 * ldk + c0 + PB;
-    launch_gemm_panel(ldk - c0 - PB, PB, PB, below, ldk, c->W, PB, below, ldk, false, c->info, s);
+    launch_gemm_panel(ldk - c0 - PB, PB, PB, below, ldk, R.W, PB, below, ldk, false, R.info, s);
     c->kernels += 2;
   }
 }
 
+RankState* local_state(exageo_ctx* c, int rank) {
+  if (c->virt) return &c->rs[rank];
+  return rank == c->rank ? &c->rs[0] : nullptr;
+}
+
+const double* panel_src(const RankState& R, int k) {
+  return R.L.owns(k) ? R.ws + R.L.off(k) : R.recv[k & 1];
+}
+
+// algorithmic flops of updating panels J0, J0 + world, ... (npan) by one panel:
+// 2 nb per (row, column) pair of the true lower triangle, plus the z row
+double update_flops(const Layout& L, int J0, int npan) {
+  double f = 0.0;
+  for (int i = 0; i < npan; ++i) {
+    const int64_t c0 = (int64_t)(J0 + i * L.world) * L.nb;
+    const int64_t c1 = (c0 + L.nb) < L.n ? (c0 + L.nb) : L.n;
+    for (int64_t cc = c0; cc < c1; ++cc) f += 2.0 * L.nb * (double)(L.n - cc + 1);
+  }
+  return f;
+}
+
+// Make panel j (factored by its owner) available to every rank: NCCL broadcast, or
+// device copies between virtual ranks. Buffer j % 2 of a receiver was last read by
+// U1(j-2) / U2(j-2); those events gate the overwrite.
+exageo_status broadcast_panel(exageo_ctx* c, int j) {
+  if (c->world == 1) return EXAGEO_OK;
+  const int o = j % c->world;
+  const size_t bytes = (size_t)c->G.ld(j) * c->G.nb * sizeof(double);
+  if (!c->virt) {
+    RankState& R = c->rs[0];
+    double* buf;
+    if (R.L.owns(j)) {
+      CUDA_TRY(c, cudaStreamWaitEvent(R.s_comm, R.ev_F, 0));
+      buf = R.ws + R.L.off(j);
+    } else {
+      if (j >= 2) {
+        CUDA_TRY(c, cudaStreamWaitEvent(R.s_comm, R.ev_U2[j & 1], 0));
+        CUDA_TRY(c, cudaStreamWaitEvent(R.s_comm, R.ev_U1[j & 1], 0));
+      }
+      buf = R.recv[j & 1];
+    }
+    NCCL_TRY(c, ncclBroadcast(buf, buf, bytes / sizeof(double), ncclDouble, o, c->comm, R.s_comm));
+    CUDA_TRY(c, cudaEventRecord(R.ev_recv[j & 1], R.s_comm));
+    return EXAGEO_OK;
+  }
+  RankState& Ro = c->rs[o];
+  const double* src = Ro.ws + Ro.L.off(j);
+  for (int r = 0; r < c->world; ++r) {
+    if (r == o) continue;
+    RankState& R = c->rs[r];
+    CUDA_TRY(c, cudaStreamWaitEvent(R.s_comm, Ro.ev_F, 0));
+    if (j >= 2) {
+      CUDA_TRY(c, cudaStreamWaitEvent(R.s_comm, R.ev_U2[j & 1], 0));
+      CUDA_TRY(c, cudaStreamWaitEvent(R.s_comm, R.ev_U1[j & 1], 0));
+    }
+    CUDA_TRY(c, cudaMemcpyAsync(R.recv[j & 1], src, bytes, cudaMemcpyDeviceToDevice, R.s_comm));
+    CUDA_TRY(c, cudaEventRecord(R.ev_recv[j & 1], R.s_comm));
+  }
+  return EXAGEO_OK;
+}
+
 // Right-looking tile Cholesky with depth-1 lookahead (the paper's "updates of the
 // trailing submatrix may be triggered before the current panel factorization is
-// complete"), as two prioritised CUDA streams instead of a runtime DAG:
-//   s_la  (high priority): U1(k) = update of tile column k+1 by panel k, then F(k+1)
-//   s_main (low priority): U2(k) = update of tile columns >= k+2 by panel k
-// Dependencies: U1(k) after U2(k-1); U2(k) after F(k). F(k+1) overlaps U2(k).
+// complete"), as prioritised CUDA streams instead of a runtime DAG:
+//   s_la  (high priority): on the owner of panel k+1, U1(k) = update of panel k+1 by
+//                          panel k, then F(k+1)
+//   s_main (low priority): U2(k) = update of the rank's other panels > k by panel k
+//   s_comm:                broadcast of panel k+1 once factored
+// Dependencies: U1(k) after U2(k-1) and panel k; U2(k) after panel k. F(k+1) and the
+// broadcast overlap U2(k).
 exageo_status do_factor(exageo_ctx* c) {
   if (!c->have_matrix) return fail(c, EXAGEO_EINVAL, "no generated matrix in the workspace");
-  const Layout& L = c->L;
-  const int cpt = L.nb / 128;  // 128-column blocks per tile column
-  c->n_u2 = 0;
-  c->u2_flops = 0.0;
+  const Layout& G = c->G;
   CUDA_TRY(c, cudaEventRecord(c->ev_fork, c->stream));
-  CUDA_TRY(c, cudaStreamWaitEvent(c->s_la, c->ev_fork, 0));
-  CUDA_TRY(c, cudaStreamWaitEvent(c->s_main, c->ev_fork, 0));
-  factor_panel(c, 0, c->s_la);
-  CUDA_TRY(c, cudaEventRecord(c->ev_F, c->s_la));
-  for (int k = 0; k + 1 < L.T; ++k) {
-    CUDA_TRY(c, cudaStreamWaitEvent(c->s_main, c->ev_F, 0));    // U2(k) needs F(k)
-    if (k > 0) CUDA_TRY(c, cudaStreamWaitEvent(c->s_la, c->ev_U2, 0));  // U1(k) needs U2(k-1)
-    launch_syrk_trailing(L, c->ws, k, 0, cpt, c->info, c->s_la);       // U1(k)
-    factor_panel(c, k + 1, c->s_la);                                   // F(k+1)
-    CUDA_TRY(c, cudaEventRecord(c->ev_F, c->s_la));
-    c->kernels += 1;
-    if (k + 2 < L.T) {
-      if ((int)c->ev_u2_beg.size() <= c->n_u2) {
-        cudaEvent_t b, e;
-        CUDA_TRY(c, cudaEventCreate(&b));
-        CUDA_TRY(c, cudaEventCreate(&e));
-        c->ev_u2_beg.push_back(b);
-        c->ev_u2_end.push_back(e);
-      }
-      CUDA_TRY(c, cudaEventRecord(c->ev_u2_beg[c->n_u2], c->s_main));
-      launch_syrk_trailing(L, c->ws, k, cpt, -1, c->info, c->s_main);  // U2(k)
-      CUDA_TRY(c, cudaEventRecord(c->ev_u2_end[c->n_u2], c->s_main));
-      ++c->n_u2;
-      const double m = (double)(L.n - (int64_t)(k + 2) * L.nb);  // true columns updated
-      if (m > 0) c->u2_flops += 2.0 * L.nb * (m * (m + 1) / 2 + m);
-      c->kernels += 1;
-    }
-    CUDA_TRY(c, cudaEventRecord(c->ev_U2, c->s_main));
+  for (auto& R : c->rs) {
+    for (cudaStream_t s : {R.s_la, R.s_main, R.s_comm}) CUDA_TRY(c, cudaStreamWaitEvent(s, c->ev_fork, 0));
+    R.n_u2 = 0;
+    R.u2_flops = 0.0;
   }
-  CUDA_TRY(c, cudaEventRecord(c->ev_join[0], c->s_la));
-  CUDA_TRY(c, cudaEventRecord(c->ev_join[1], c->s_main));
-  CUDA_TRY(c, cudaStreamWaitEvent(c->stream, c->ev_join[0], 0));
-  CUDA_TRY(c, cudaStreamWaitEvent(c->stream, c->ev_join[1], 0));
+  if (RankState* R0 = local_state(c, 0)) {
+    factor_panel(c, *R0, 0, R0->s_la);
+    CUDA_TRY(c, cudaEventRecord(R0->ev_F, R0->s_la));
+  }
+  exageo_status st = broadcast_panel(c, 0);
+  if (st != EXAGEO_OK) return st;
+  for (int k = 0; k + 1 < G.T; ++k) {
+    for (auto& R : c->rs) {
+      const Layout& L = R.L;
+      const double* Pk = panel_src(R, k);
+      cudaEvent_t avail = L.owns(k) ? R.ev_F : R.ev_recv[k & 1];
+      const bool owns_next = L.owns(k + 1);
+      // U2(k) needs panel k: wait now, before ev_F is re-recorded for F(k+1) below
+      CUDA_TRY(c, cudaStreamWaitEvent(R.s_main, avail, 0));
+      if (owns_next) {
+        CUDA_TRY(c, cudaStreamWaitEvent(R.s_la, avail, 0));
+        if (k > 0) CUDA_TRY(c, cudaStreamWaitEvent(R.s_la, R.ev_U2[(k - 1) & 1], 0));
+        launch_syrk_panels(L, R.ws, Pk, k, k + 1, 1, R.info, R.s_la);  // U1(k)
+        CUDA_TRY(c, cudaEventRecord(R.ev_U1[k & 1], R.s_la));
+        factor_panel(c, R, k + 1, R.s_la);  // F(k+1)
+        CUDA_TRY(c, cudaEventRecord(R.ev_F, R.s_la));
+        c->kernels += 1;
+      } else {
+        CUDA_TRY(c, cudaEventRecord(R.ev_U1[k & 1], R.s_la));  // nothing read on s_la this step
+      }
+      const int J0 = L.first_owned_from(owns_next ? k + 2 : k + 1);
+      const int npan = J0 < L.T ? (L.T - 1 - J0) / L.world + 1 : 0;
+      if (npan > 0) {
+        if ((int)R.u2b.size() <= R.n_u2) {
+          cudaEvent_t b, e;
+          CUDA_TRY(c, cudaEventCreate(&b));
+          CUDA_TRY(c, cudaEventCreate(&e));
+          R.u2b.push_back(b);
+          R.u2e.push_back(e);
+        }
+        CUDA_TRY(c, cudaEventRecord(R.u2b[R.n_u2], R.s_main));
+        launch_syrk_panels(L, R.ws, Pk, k, J0, npan, R.info, R.s_main);  // U2(k)
+        CUDA_TRY(c, cudaEventRecord(R.u2e[R.n_u2], R.s_main));
+        ++R.n_u2;
+        R.u2_flops += update_flops(L, J0, npan);
+        c->kernels += 1;
+      }
+      CUDA_TRY(c, cudaEventRecord(R.ev_U2[k & 1], R.s_main));
+    }
+    st = broadcast_panel(c, k + 1);
+    if (st != EXAGEO_OK) return st;
+  }
+  for (auto& R : c->rs) {
+    CUDA_TRY(c, cudaEventRecord(R.ev_join[0], R.s_la));
+    CUDA_TRY(c, cudaEventRecord(R.ev_join[1], R.s_main));
+    CUDA_TRY(c, cudaEventRecord(R.ev_join[2], R.s_comm));
+    for (auto& ev : R.ev_join) CUDA_TRY(c, cudaStreamWaitEvent(c->stream, ev, 0));
+  }
   return check_launch(c);
 }
 
+// ---------------------------------------------------------------------------- reductions
+// First failing global pivot over all ranks (-1 if none). Synchronises.
+exageo_status first_pivot(exageo_ctx* c, int64_t* pivot) {
+  int64_t best = std::numeric_limits<int64_t>::max();
+  for (auto& R : c->rs) {
+    int info = 0;
+    CUDA_TRY(c, cudaMemcpyAsync(&info, R.info, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    if (info > 0 && (int64_t)info - 1 < best) best = (int64_t)info - 1;
+  }
+  if (!c->virt && c->world > 1) {
+    CUDA_TRY(c, cudaMemcpyAsync(c->pivbuf, &best, sizeof(int64_t), cudaMemcpyHostToDevice, c->stream));
+    NCCL_TRY(c, ncclAllReduce(c->pivbuf, c->pivbuf, 1, ncclInt64, ncclMin, c->comm, c->stream));
+    CUDA_TRY(c, cudaMemcpyAsync(&best, c->pivbuf, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  }
+  *pivot = best == std::numeric_limits<int64_t>::max() ? -1 : best;
+  return EXAGEO_OK;
+}
+
 exageo_status do_finish(exageo_ctx* c, double* out3, int64_t* pivot) {
-  const Layout& L = c->L;
-  launch_finish(L, c->ws, c->slots, L.T * (L.nb / PB), c->out, c->stream);
-  c->kernels += 2;
+  for (size_t i = 0; i < c->rs.size(); ++i) {
+    RankState& R = c->rs[i];
+    launch_local_partials(R.L, R.ws, R.slots, R.L.owned() * (R.L.nb / PB), R.scratch, c->parts + 2 * i, c->stream);
+    c->kernels += 2;
+  }
+  int nparts = (int)c->rs.size();
+  if (!c->virt && c->world > 1) {
+    NCCL_TRY(c, ncclAllReduce(c->parts, c->parts, 2, ncclDouble, ncclSum, c->comm, c->stream));
+    nparts = 1;
+  }
+  launch_combine(c->parts, nparts, c->G.n, c->out3, c->stream);
+  c->kernels += 1;
   exageo_status st = check_launch(c);
   if (st != EXAGEO_OK) return st;
   double h[3];
-  int info = 0;
-  CUDA_TRY(c, cudaMemcpyAsync(h, c->out, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
-  CUDA_TRY(c, cudaMemcpyAsync(&info, c->info, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
-  if (pivot) *pivot = info > 0 ? (int64_t)info - 1 : -1;
-  if (info > 0) {
+  CUDA_TRY(c, cudaMemcpyAsync(h, c->out3, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+  int64_t piv = -1;
+  st = first_pivot(c, &piv);  // synchronises
+  if (st != EXAGEO_OK) return st;
+  if (pivot) *pivot = piv;
+  if (piv >= 0) {
     if (out3) {
       out3[0] = -std::numeric_limits<double>::infinity();
       out3[1] = out3[2] = std::numeric_limits<double>::quiet_NaN();
     }
-    return fail(c, EXAGEO_ENOTPD, "covariance not positive definite at pivot " + std::to_string(info - 1));
+    return fail(c, EXAGEO_ENOTPD, "covariance not positive definite at pivot " + std::to_string(piv));
   }
   if (out3) memcpy(out3, h, sizeof(h));
   return EXAGEO_OK;
@@ -296,7 +434,7 @@ exageo_status loglik_device(exageo_ctx* c, const exageo_theta* t, int64_t n, con
   CUDA_TRY(c, cudaEventRecord(c->ev[2], c->stream));
   double r3[3];
   int64_t piv = -1;
-  st = do_finish(c, r3, &piv);  // records nothing after; ev[3] below
+  st = do_finish(c, r3, &piv);
   if (st != EXAGEO_OK && st != EXAGEO_ENOTPD) return st;
   CUDA_TRY(c, cudaEventRecord(c->ev[3], c->stream));
   CUDA_TRY(c, cudaEventSynchronize(c->ev[3]));
@@ -308,8 +446,8 @@ exageo_status loglik_device(exageo_ctx* c, const exageo_theta* t, int64_t n, con
     info->quad = r3[2];
     info->npd_pivot = piv;
     info->n = n;
-    info->nb = c->L.nb;
-    info->ntiles = c->L.T;
+    info->nb = c->G.nb;
+    info->ntiles = c->G.T;
     info->flops = (double)n * (double)n * (double)n / 3.0;
     float ms = 0.f;
     cudaEventElapsedTime(&ms, c->ev[0], c->ev[3]);
@@ -321,16 +459,50 @@ exageo_status loglik_device(exageo_ctx* c, const exageo_theta* t, int64_t n, con
     cudaEventElapsedTime(&ms, c->ev[2], c->ev[3]);
     info->ms_reduce = ms;
     info->kernels = c->kernels - k0;
-    info->trailing_launches = c->n_u2;
-    info->trailing_flops = c->u2_flops;
+    const RankState& R = c->rs[0];  // dominant-kernel timing of (the first) local rank
+    info->trailing_launches = R.n_u2;
+    info->trailing_flops = R.u2_flops;
     double tr = 0.0;
-    for (int i = 0; i < c->n_u2; ++i) {
-      cudaEventElapsedTime(&ms, c->ev_u2_beg[i], c->ev_u2_end[i]);
+    for (int i = 0; i < R.n_u2; ++i) {
+      cudaEventElapsedTime(&ms, R.u2b[i], R.u2e[i]);
       tr += ms;
     }
     info->ms_trailing = tr;
   }
   return st;
+}
+
+void destroy_rank(RankState& R) {
+  if (R.ws && !R.ws_external) cudaFree(R.ws);
+  for (auto p : R.recv) cudaFree(p);
+  cudaFree(R.W);
+  cudaFree(R.slots);
+  cudaFree(R.scratch);
+  cudaFree(R.info);
+  cudaFree(R.part);
+  for (cudaEvent_t ev : {R.ev_F, R.ev_U2[0], R.ev_U2[1], R.ev_U1[0], R.ev_U1[1], R.ev_recv[0], R.ev_recv[1],
+                         R.ev_join[0], R.ev_join[1], R.ev_join[2]})
+    if (ev) cudaEventDestroy(ev);
+  for (cudaEvent_t ev : R.u2b) cudaEventDestroy(ev);
+  for (cudaEvent_t ev : R.u2e) cudaEventDestroy(ev);
+  for (cudaStream_t s : {R.s_la, R.s_main, R.s_comm})
+    if (s) cudaStreamDestroy(s);
+}
+
+cudaError_t init_rank(RankState& R) {
+  cudaError_t e;
+  int lo = 0, hi = 0;
+  cudaDeviceGetStreamPriorityRange(&lo, &hi);  // hi = numerically smallest = highest priority
+  if ((e = cudaStreamCreateWithPriority(&R.s_la, cudaStreamNonBlocking, hi)) != cudaSuccess) return e;
+  if ((e = cudaStreamCreateWithPriority(&R.s_main, cudaStreamNonBlocking, lo)) != cudaSuccess) return e;
+  if ((e = cudaStreamCreateWithPriority(&R.s_comm, cudaStreamNonBlocking, hi)) != cudaSuccess) return e;
+  for (cudaEvent_t* ev : {&R.ev_F, &R.ev_U2[0], &R.ev_U2[1], &R.ev_U1[0], &R.ev_U1[1], &R.ev_recv[0], &R.ev_recv[1],
+                          &R.ev_join[0], &R.ev_join[1], &R.ev_join[2]})
+    if ((e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming)) != cudaSuccess) return e;
+  if ((e = cudaMalloc(&R.W, sizeof(double) * PB * PB)) != cudaSuccess) return e;
+  if ((e = cudaMalloc(&R.scratch, sizeof(double) * kQuadBlocks)) != cudaSuccess) return e;
+  if ((e = cudaMalloc(&R.info, sizeof(int))) != cudaSuccess) return e;
+  return cudaMemset(R.info, 0, sizeof(int));
 }
 
 }  // namespace
@@ -352,6 +524,15 @@ const char* exageo_strerror(exageo_status s) {
 
 const char* exageo_last_error(const exageo_ctx* ctx) { return ctx ? ctx->err.c_str() : g_create_err.c_str(); }
 
+exageo_status exageo_nccl_unique_id(void* out, size_t len) {
+  if (!out || len < sizeof(ncclUniqueId)) return fail(nullptr, EXAGEO_EINVAL, "need a 128-byte buffer");
+  ncclUniqueId id;
+  ncclResult_t r = ncclGetUniqueId(&id);
+  if (r != ncclSuccess) return fail(nullptr, EXAGEO_ENCCL, std::string("ncclGetUniqueId: ") + ncclGetErrorString(r));
+  memcpy(out, &id, sizeof(id));
+  return EXAGEO_OK;
+}
+
 exageo_status exageo_create(exageo_ctx** out, const exageo_opts* opts) {
   if (!out) return fail(nullptr, EXAGEO_EINVAL, "NULL ctx pointer");
   *out = nullptr;
@@ -359,6 +540,9 @@ exageo_status exageo_create(exageo_ctx** out, const exageo_opts* opts) {
   if (opts) o = *opts;
   if (o.nb != 0 && (o.nb < 128 || o.nb % 128 != 0))
     return fail(nullptr, EXAGEO_EINVAL, "nb must be 0 (auto) or a positive multiple of 128");
+  if (o.world < 0 || o.virtual_ranks < 0 || (o.world > 1 && o.virtual_ranks > 1) ||
+      (o.world > 1 && (o.rank < 0 || o.rank >= o.world || !o.nccl_id)))
+    return fail(nullptr, EXAGEO_EINVAL, "bad distribution options (world/rank/nccl_id/virtual_ranks)");
   int ndev = 0;
   cudaError_t e = cudaGetDeviceCount(&ndev);
   if (e != cudaSuccess || ndev == 0) {
@@ -369,6 +553,9 @@ exageo_status exageo_create(exageo_ctx** out, const exageo_opts* opts) {
   exageo_ctx* c = new exageo_ctx();
   c->device = o.device;
   c->nb_opt = o.nb;
+  c->virt = o.virtual_ranks > 1;
+  c->world = c->virt ? o.virtual_ranks : (o.world > 1 ? o.world : 1);
+  c->rank = (!c->virt && o.world > 1) ? o.rank : 0;
   auto bail = [&](cudaError_t err, const char* what) {
     g_create_err = std::string(what) + ": " + cudaGetErrorString(err);
     exageo_destroy(c);
@@ -386,19 +573,25 @@ exageo_status exageo_create(exageo_ctx** out, const exageo_opts* opts) {
   }
   for (auto& ev : c->ev)
     if ((e = cudaEventCreate(&ev)) != cudaSuccess) return bail(e, "cudaEventCreate");
-  {
-    int lo = 0, hi = 0;
-    cudaDeviceGetStreamPriorityRange(&lo, &hi);  // hi = numerically smallest = highest priority
-    if ((e = cudaStreamCreateWithPriority(&c->s_la, cudaStreamNonBlocking, hi)) != cudaSuccess)
-      return bail(e, "cudaStreamCreateWithPriority");
-    if ((e = cudaStreamCreateWithPriority(&c->s_main, cudaStreamNonBlocking, lo)) != cudaSuccess)
-      return bail(e, "cudaStreamCreateWithPriority");
-    for (cudaEvent_t* ev : {&c->ev_fork, &c->ev_F, &c->ev_U2, &c->ev_join[0], &c->ev_join[1]})
-      if ((e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming)) != cudaSuccess) return bail(e, "cudaEventCreate");
+  if ((e = cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming)) != cudaSuccess)
+    return bail(e, "cudaEventCreate");
+  c->rs.resize(c->virt ? c->world : 1);
+  for (auto& R : c->rs)
+    if ((e = init_rank(R)) != cudaSuccess) return bail(e, "rank state");
+  if ((e = cudaMalloc(&c->parts, sizeof(double) * 2 * c->world)) != cudaSuccess) return bail(e, "cudaMalloc");
+  if ((e = cudaMalloc(&c->out3, sizeof(double) * 4)) != cudaSuccess) return bail(e, "cudaMalloc");
+  if ((e = cudaMalloc(&c->pivbuf, sizeof(int64_t))) != cudaSuccess) return bail(e, "cudaMalloc");
+  if (!c->virt && c->world > 1) {
+    ncclUniqueId id;
+    memcpy(&id, o.nccl_id, sizeof(id));
+    ncclResult_t r = ncclCommInitRank(&c->comm, c->world, id, c->rank);
+    if (r != ncclSuccess) {
+      g_create_err = std::string("ncclCommInitRank: ") + ncclGetErrorString(r);
+      c->comm = nullptr;
+      exageo_destroy(c);
+      return EXAGEO_ENCCL;
+    }
   }
-  if ((e = cudaMalloc(&c->W, sizeof(double) * PB * PB)) != cudaSuccess) return bail(e, "cudaMalloc");
-  if ((e = cudaMalloc(&c->out, sizeof(double) * kOutDoubles)) != cudaSuccess) return bail(e, "cudaMalloc");
-  if ((e = cudaMalloc(&c->info, sizeof(int))) != cudaSuccess) return bail(e, "cudaMalloc");
   *out = c;
   return EXAGEO_OK;
 }
@@ -407,21 +600,16 @@ void exageo_destroy(exageo_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
-  if (c->ws && !c->ws_external) cudaFree(c->ws);
-  cudaFree(c->W);
-  cudaFree(c->slots);
-  cudaFree(c->out);
-  cudaFree(c->info);
+  if (c->comm) ncclCommDestroy(c->comm);
+  for (auto& R : c->rs) destroy_rank(R);
+  cudaFree(c->parts);
+  cudaFree(c->out3);
+  cudaFree(c->pivbuf);
   cudaFree(c->vec);
-  cudaFree(c->part);
+  cudaFree(c->zsum);
   for (auto& ev : c->ev)
     if (ev) cudaEventDestroy(ev);
-  for (cudaEvent_t ev : {c->ev_fork, c->ev_F, c->ev_U2, c->ev_join[0], c->ev_join[1]})
-    if (ev) cudaEventDestroy(ev);
-  for (cudaEvent_t ev : c->ev_u2_beg) cudaEventDestroy(ev);
-  for (cudaEvent_t ev : c->ev_u2_end) cudaEventDestroy(ev);
-  if (c->s_la) cudaStreamDestroy(c->s_la);
-  if (c->s_main) cudaStreamDestroy(c->s_main);
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }
@@ -429,18 +617,19 @@ void exageo_destroy(exageo_ctx* c) {
 size_t exageo_workspace_bytes(int64_t n, int nb) {
   if (n < 1) return 0;
   if (nb <= 0) nb = auto_nb(n);
-  const Layout L = make_layout(n, nb);
-  return (size_t)L.total() * sizeof(double) + 256 * sizeof(double);
+  return local_bytes(make_layout(n, nb));
 }
 
 exageo_status exageo_set_workspace(exageo_ctx* c, void* ptr, size_t bytes) {
   if (!c) return EXAGEO_EINVAL;
+  if (c->virt) return fail(c, EXAGEO_EINVAL, "external workspace is not supported with virtual ranks");
   CUDA_TRY(c, cudaSetDevice(c->device));
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
-  if (c->ws && !c->ws_external) cudaFree(c->ws);
-  c->ws = (double*)ptr;
-  c->ws_bytes = ptr ? bytes : 0;
-  c->ws_external = ptr != nullptr;
+  RankState& R = c->rs[0];
+  if (R.ws && !R.ws_external) cudaFree(R.ws);
+  R.ws = (double*)ptr;
+  R.ws_bytes = ptr ? bytes : 0;
+  R.ws_external = ptr != nullptr;
   c->have_matrix = false;
   return EXAGEO_OK;
 }
@@ -456,7 +645,7 @@ exageo_status exageo_matern_cov(exageo_ctx* c, const exageo_theta* t, int64_t m,
   if (!theta_ok(t)) return fail(c, EXAGEO_EINVAL, "theta must be finite and > 0");
   if (m < 1 || n < 1 || !x1 || !y1 || !x2 || !y2 || !C || ldc < m) return fail(c, EXAGEO_EINVAL, "bad sizes/pointers");
   CUDA_TRY(c, cudaSetDevice(c->device));
-  double *d = nullptr;
+  double* d = nullptr;
   const size_t bytes = sizeof(double) * (2 * (size_t)m + 2 * (size_t)n + (size_t)m * (size_t)n);
   CUDA_TRY(c, cudaMalloc(&d, bytes));
   double *dx1 = d, *dy1 = d + m, *dx2 = d + 2 * m, *dy2 = d + 2 * m + n, *dC = d + 2 * m + 2 * n;
@@ -512,19 +701,33 @@ exageo_status exageo_simulate(exageo_ctx* c, const exageo_theta* t, int64_t n, c
   if (st != EXAGEO_OK) return st;
   st = do_factor(c);
   if (st != EXAGEO_OK) return st;
-  int info = 0;
-  CUDA_TRY(c, cudaMemcpyAsync(&info, c->info, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
-  if (info > 0) return fail(c, EXAGEO_ENOTPD, "covariance not positive definite at pivot " + std::to_string(info - 1));
-  const size_t need = sizeof(double) * (size_t)c->L.T * (size_t)c->L.N;
-  if (c->part_cap < need) {
-    cudaFree(c->part);
-    c->part = nullptr;
-    CUDA_TRY(c, cudaMalloc(&c->part, need));
-    c->part_cap = need;
+  int64_t piv = -1;
+  st = first_pivot(c, &piv);
+  if (st != EXAGEO_OK) return st;
+  if (piv >= 0) return fail(c, EXAGEO_ENOTPD, "covariance not positive definite at pivot " + std::to_string(piv));
+  // Alg. 1 l.7: z = L e -- per-panel partial products, summed over all panels (and ranks)
+  const Layout& G = c->G;
+  const size_t need = sizeof(double) * (size_t)G.T * (size_t)G.N;
+  RankState& R0 = c->rs[0];
+  if (R0.part_cap < need) {
+    cudaFree(R0.part);
+    R0.part = nullptr;
+    CUDA_TRY(c, cudaMalloc(&R0.part, need));
+    R0.part_cap = need;
   }
-  launch_trmv_lower(c->L, c->ws, de, dz, c->part, c->stream);
-  c->kernels += 2;
+  int slices = 0;
+  for (auto& R : c->rs) {
+    launch_trmv_partial(R.L, R.ws, de, R0.part + (size_t)slices * G.N, c->stream);
+    slices += R.L.owned();
+    c->kernels += 1;
+  }
+  if (!c->virt && c->world > 1) {
+    launch_trmv_sum(n, G.N, R0.part, slices, c->zsum, c->stream);
+    NCCL_TRY(c, ncclAllReduce(c->zsum, dz, n, ncclDouble, ncclSum, c->comm, c->stream));
+  } else {
+    launch_trmv_sum(n, G.N, R0.part, slices, dz, c->stream);
+  }
+  c->kernels += 1;
   st = check_launch(c);
   if (st != EXAGEO_OK) return st;
   CUDA_TRY(c, cudaMemcpyAsync(z, dz, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
@@ -554,15 +757,14 @@ exageo_status exageo_stage_finish(exageo_ctx* c, double* out3, int64_t* pivot) {
 
 exageo_status exageo_read_lower(exageo_ctx* c, double* dst, int64_t ld) {
   if (!c) return fail(nullptr, EXAGEO_EINVAL, "NULL ctx");
-  if (!c->have_matrix || !dst || ld < c->L.n) return fail(c, EXAGEO_EINVAL, "no matrix or bad ld");
+  if (!c->have_matrix || !dst || ld < c->G.n) return fail(c, EXAGEO_EINVAL, "no matrix or bad ld");
   CUDA_TRY(c, cudaSetDevice(c->device));
-  const int64_t n = c->L.n;
+  const int64_t n = c->G.n;
   double* d = nullptr;
   CUDA_TRY(c, cudaMalloc(&d, sizeof(double) * (size_t)n * (size_t)n));
-  cudaMemsetAsync(d, 0, sizeof(double) * (size_t)n * (size_t)n, c->stream);
-  launch_read_lower(c->L, c->ws, d, n, c->stream);
-  cudaError_t e = cudaGetLastError();
-  // copy only the lower triangle column by column would be slow; copy all and mask on host
+  cudaError_t e = cudaMemsetAsync(d, 0, sizeof(double) * (size_t)n * (size_t)n, c->stream);
+  for (auto& R : c->rs) launch_read_lower(R.L, R.ws, d, n, c->stream);
+  if (e == cudaSuccess) e = cudaGetLastError();
   double* h = (double*)malloc(sizeof(double) * (size_t)n * (size_t)n);
   if (e == cudaSuccess && h)
     e = cudaMemcpyAsync(h, d, sizeof(double) * (size_t)n * (size_t)n, cudaMemcpyDeviceToHost, c->stream);
@@ -581,13 +783,14 @@ exageo_status exageo_read_zrow(exageo_ctx* c, double* dst) {
   if (!c) return fail(nullptr, EXAGEO_EINVAL, "NULL ctx");
   if (!c->have_matrix || !dst) return fail(c, EXAGEO_EINVAL, "no matrix or NULL dst");
   CUDA_TRY(c, cudaSetDevice(c->device));
-  exageo_status st = ensure_vec(c, c->L.n);
+  exageo_status st = ensure_vec(c, c->G.n);
   if (st != EXAGEO_OK) return st;
-  launch_read_zrow(c->L, c->ws, c->vec + 3 * c->L.n, c->stream);
+  double* d = c->vec + 3 * c->G.n;
+  CUDA_TRY(c, cudaMemsetAsync(d, 0, sizeof(double) * (size_t)c->G.n, c->stream));
+  for (auto& R : c->rs) launch_read_zrow(R.L, R.ws, d, c->stream);
   st = check_launch(c);
   if (st != EXAGEO_OK) return st;
-  CUDA_TRY(c, cudaMemcpyAsync(dst, c->vec + 3 * c->L.n, sizeof(double) * (size_t)c->L.n, cudaMemcpyDeviceToHost,
-                              c->stream));
+  CUDA_TRY(c, cudaMemcpyAsync(dst, d, sizeof(double) * (size_t)c->G.n, cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   return EXAGEO_OK;
 }
@@ -599,7 +802,7 @@ exageo_status exageo_read_entries(exageo_ctx* c, int64_t count, const int64_t* r
     return fail(c, EXAGEO_EINVAL, "no matrix or NULL arrays");
   if (count == 0) return EXAGEO_OK;
   for (int64_t i = 0; i < count; ++i)
-    if (cols[i] < 0 || cols[i] > rows[i] || rows[i] >= c->L.n)
+    if (cols[i] < 0 || cols[i] > rows[i] || rows[i] >= c->G.n)
       return fail(c, EXAGEO_EINVAL, "entry outside the lower triangle");
   CUDA_TRY(c, cudaSetDevice(c->device));
   void* d = nullptr;
@@ -609,8 +812,9 @@ exageo_status exageo_read_entries(exageo_ctx* c, int64_t count, const int64_t* r
   cudaError_t e = cudaMemcpyAsync(drc, rows, sizeof(int64_t) * count, cudaMemcpyHostToDevice, c->stream);
   if (e == cudaSuccess)
     e = cudaMemcpyAsync(drc + count, cols, sizeof(int64_t) * count, cudaMemcpyHostToDevice, c->stream);
+  if (e == cudaSuccess) e = cudaMemsetAsync(dout, 0, sizeof(double) * count, c->stream);
   if (e == cudaSuccess) {
-    launch_read_entries(c->L, c->ws, count, drc, dout, c->stream);
+    for (auto& R : c->rs) launch_read_entries(R.L, R.ws, count, drc, dout, c->stream);
     e = cudaGetLastError();
   }
   if (e == cudaSuccess)

@@ -1,0 +1,66 @@
+// context.h -- the library context (exageo_ctx) and the per-rank state of the
+// distributed executor (schedule.cu). Internal; not part of the C ABI.
+#pragma once
+#include <nccl.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/exageo.h"
+#include "internal.h"
+
+namespace exageo {
+
+// Everything one rank needs: its panels, receive buffers for broadcast panels,
+// streams of the lookahead schedule and their events. In NCCL mode a process holds
+// one RankState; in virtual mode one process holds `world` of them on one device.
+struct RankState {
+  Layout L;                    // rank-local layout (rank, world)
+  double* ws = nullptr;        // owned panels
+  size_t ws_bytes = 0;
+  bool ws_external = false;
+  double* recv[2] = {nullptr, nullptr};  // copies of broadcast panels (world > 1)
+  size_t recv_bytes = 0;
+  double* W = nullptr;         // PB x PB inverse of the current diagonal block
+  double* slots = nullptr;     // log-det partials: (nb / PB) per owned panel
+  int64_t slots_cap = 0;
+  double* scratch = nullptr;   // kQuadBlocks doubles
+  int* info = nullptr;         // 0 or first failing global pivot + 1
+  double* part = nullptr;      // TRMV partial sums (owned * N doubles)
+  size_t part_cap = 0;
+  cudaStream_t s_la = nullptr, s_main = nullptr, s_comm = nullptr;
+  cudaEvent_t ev_F = nullptr;                    // F(k) done (panel k factored)
+  cudaEvent_t ev_U2[2] = {nullptr, nullptr};     // U2(k) done, by k % 2
+  cudaEvent_t ev_U1[2] = {nullptr, nullptr};     // U1(k) done, by k % 2
+  cudaEvent_t ev_recv[2] = {nullptr, nullptr};   // panel j received, by j % 2
+  cudaEvent_t ev_join[3] = {nullptr, nullptr, nullptr};
+  std::vector<cudaEvent_t> u2b, u2e;             // timing of the bulk trailing update
+  int n_u2 = 0;
+  double u2_flops = 0.0;
+};
+
+}  // namespace exageo
+
+struct exageo_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int nb_opt = 0;
+  int world = 1;       // ranks of the distribution (NCCL processes or virtual ranks)
+  int rank = 0;        // this process's rank (NCCL mode), 0 otherwise
+  bool virt = false;   // virtual ranks: all `world` ranks in this process on one device
+  ncclComm_t comm = nullptr;
+  std::vector<exageo::RankState> rs;
+  double* parts = nullptr;    // 2 * world doubles: per-rank {sum log L_ii, sum y^2}
+  double* out3 = nullptr;     // {loglik, logdet, quad}
+  int64_t* pivbuf = nullptr;  // NCCL mode: all-reduced first failing pivot
+  double* vec = nullptr;      // 4 n staging for host-pointer entry points
+  int64_t vec_cap = 0;
+  double* zsum = nullptr;     // NCCL TRMV: local partial z (n doubles)
+  exageo::Layout G;           // global geometry (n, nb, T, N); rank/world unset
+  bool have_matrix = false;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t ev_fork = nullptr;
+  int64_t kernels = 0;
+  std::string err;
+};

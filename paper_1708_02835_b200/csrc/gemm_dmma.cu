@@ -11,8 +11,6 @@ using PanelCfg = Cfg<64, 64, 8, 2, 2, 4, 4>;
 // Trailing update: 64 x 64 tiles, 4 warps of 32 x 32, BK 8 x 4 stages, 4 CTAs per SM
 // (tools/gemm_tune.cu at n=100k: 33.8 TF vs 30.3 for 128x64 at 2 CTAs/SM).
 using TrailCfg = Cfg<64, 64, 8, 2, 2, 4, 4>;
-// Rasterization band (128-column blocks swept together, see SyrkMap).
-constexpr int kTrailBand = 8;
 }  // namespace
 
 cudaError_t gemm_init() {
@@ -40,19 +38,16 @@ void launch_gemm_panel(int64_t M, int N, int K, const double* A, int64_t lda, co
   else launch<PanelCfg, false>(map, info, s);
 }
 
-void launch_syrk_trailing(const Layout& L, double* ws, int k, int cb_lo, int cb_hi, const int* info,
-                          cudaStream_t s) {
-  const int64_t c0 = (int64_t)(k + 1) * L.nb;
-  if (c0 >= L.N) return;
+void launch_syrk_panels(const Layout& L, double* ws, const double* Pk, int k, int J0, int npan, const int* info,
+                        cudaStream_t s) {
+  if (npan <= 0) return;
   SyrkMap map;
   map.L = L;
   map.ws = ws;
+  map.Pk = Pk;
   map.k = k;
-  map.Mb = (int)((L.N - c0) / 128);
-  map.cb_lo = cb_lo < 0 ? 0 : cb_lo;
-  map.cb_hi = (cb_hi < 0 || cb_hi > map.Mb) ? map.Mb : cb_hi;
-  if (map.cb_hi <= map.cb_lo) return;
-  map.band = kTrailBand;
+  map.J0 = J0;
+  map.npan = npan;
   launch<TrailCfg, true>(map, info, s);
 }
 

@@ -76,29 +76,36 @@ struct DenseMap {
   __host__ int64_t blocks(int BM, int BN) const { return (int64_t)((M + BM - 1) / BM) * ((N + BN - 1) / BN); }
 };
 
-// Trailing update of step k over the lower block-column panels (internal.h).
-// Square 128-blocks (rb >= cb) of the trailing matrix, rows/cols >= c0 = (k+1) nb;
-// row block rb == Mb is the z row block. A 128-col block is split into
-// 128/BN CTA tiles (consecutive bids share the row block).
-// Rasterization: the column blocks [cb_lo, cb_hi) are cut into bands of `band`
-// column blocks; a band is swept row block by row block (the rows' A operand is
-// reused `band` times back to back, the band's B operands stay L2-resident for
-// the whole sweep), bands left to right.
+// Trailing update by panel k of a set of panels owned by this rank (internal.h):
+// panels J_i = J0 + i * world, i < npan. Panel J's part of the trailing matrix is
+// its columns J nb .. J nb + nb - 1 and rows from its diagonal down to the z row
+// block, cut into 128 x 128 blocks: column block cb in [0, cpt), cpt = nb / 128,
+// row block rb in [cb, Mr] (rb = Mr = (N - J nb) / 128 is the z row block).
+// A 128-block is split into (128/BM) x (128/BN) CTA tiles; consecutive bids share
+// a 128-block. Order: panel by panel; inside a panel row block by row block
+// (the row's A operand is reused cpt times back to back; the panel's B operand,
+// nb rows of panel k, stays L2-resident for the whole sweep).
+// Operand: Pk = panel k (this rank's own storage or the received copy), ld(k).
 struct SyrkMap {
   Layout L;
-  double* ws;
+  double* ws;        // this rank's panel storage
+  const double* Pk;  // panel k operand
   int k;
-  int Mb;      // number of square 128-blocks in the trailing matrix
-  int cb_lo;   // first 128-column block of this launch (0 = column (k+1) nb)
-  int cb_hi;   // one past the last 128-column block (<= Mb)
-  int band;    // column blocks per band (>= 1)
+  int J0;            // first panel of this launch (owned)
+  int npan;          // number of panels (J0, J0 + world, ...)
 
-  __host__ __device__ int64_t band_count(int64_t b) const {
-    const int64_t bs = cb_lo + b * band;
-    const int64_t w = (cb_hi - bs) < band ? (cb_hi - bs) : band;
-    return w * (w + 1) / 2 + ((int64_t)Mb - bs - w + 1) * w;
+  __host__ __device__ int cpt() const { return L.nb / 128; }
+  __host__ __device__ int64_t Mr0() const { return (L.N - (int64_t)J0 * L.nb) / 128; }
+  // 128-blocks of panel i: cpt (Mr_i + 1) - cpt (cpt - 1) / 2, Mr_i = Mr0 - i world cpt
+  __host__ __device__ int64_t panel_blocks(int64_t i) const {
+    const int64_t c = cpt(), Mr = Mr0() - i * L.world * c;
+    return c * (Mr + 1) - c * (c - 1) / 2;
   }
-  __host__ __device__ int nbands() const { return (cb_hi - cb_lo + band - 1) / band; }
+  // 128-blocks of panels before panel i: i a - D i (i - 1) / 2, a = panel_blocks(0), D = world cpt^2
+  __host__ __device__ int64_t Sp(int64_t i) const {
+    const int64_t c = cpt(), D = (int64_t)L.world * c * c;
+    return i * panel_blocks(0) - D * (i * (i - 1) / 2);
+  }
 
   template <int BM, int BN>
   __host__ __device__ __forceinline__ bool operator()(int64_t bid, GemmTile& t) const {
@@ -107,61 +114,49 @@ struct SyrkMap {
     const int sub = (int)(bid % SPLIT);
     const int half = sub % SPLIT_C, rhalf = sub / SPLIT_C;
     const int64_t q = bid / SPLIT;
-    // band index: largest b with Sfull(b) <= q (exact integer fix-up after a sqrt guess)
-    const int nb_ = nbands();
-    const double G = (double)band, A0 = (double)Mb - cb_lo - band + 1;
-    const double beta = G * (A0 + G + 0.5);
-    const double disc = beta * beta - 2.0 * G * G * (double)q;
-    int64_t b = (int64_t)((beta - sqrt(disc > 0.0 ? disc : 0.0)) / (G * G));
-    if (b >= nb_) b = nb_ - 1;
-    if (b < 0) b = 0;
-    while (b > 0 && Sfull(b) > q) --b;
-    while (b + 1 < nb_ && Sfull(b + 1) <= q) ++b;
-    int64_t qq = q - Sfull(b);
-    const int64_t bs = cb_lo + b * band;
-    const int64_t w = (cb_hi - bs) < band ? (cb_hi - bs) : band;
-    int64_t rb, cb;
+    // panel: largest i with Sp(i) <= q  (quadratic guess, exact integer fix-up)
+    const double a = (double)panel_blocks(0), D = (double)L.world * cpt() * cpt();
+    const double beta = a + 0.5 * D;
+    const double disc = beta * beta - 2.0 * D * (double)q;
+    int64_t i = (int64_t)((beta - sqrt(disc > 0.0 ? disc : 0.0)) / D);
+    if (i >= npan) i = npan - 1;
+    if (i < 0) i = 0;
+    while (i > 0 && Sp(i) > q) --i;
+    while (i + 1 < npan && Sp(i + 1) <= q) ++i;
+    int64_t qq = q - Sp(i);
+    const int J = J0 + (int)i * L.world;
+    const int64_t w = cpt();
     const int64_t head = w * (w + 1) / 2;
-    if (qq < head) {
-      int64_t i = (int64_t)((sqrt(8.0 * (double)qq + 1.0) - 1.0) * 0.5);
-      while (i > 0 && i * (i + 1) / 2 > qq) --i;
-      while ((i + 1) * (i + 2) / 2 <= qq) ++i;
-      rb = bs + i;
-      cb = bs + (qq - i * (i + 1) / 2);
+    int64_t rb, cb;
+    if (qq < head) {  // diagonal 128-blocks of the panel: row rb holds columns 0..rb
+      int64_t r = 0;
+      while ((r + 1) * (r + 2) / 2 <= qq) ++r;
+      rb = r;
+      cb = qq - r * (r + 1) / 2;
     } else {
       qq -= head;
-      rb = bs + w + qq / w;
-      cb = bs + qq % w;
+      rb = w + qq / w;
+      cb = qq % w;
     }
-    const int64_t c0 = (int64_t)(k + 1) * L.nb;
-    const int64_t gc = c0 + cb * 128 + half * BN;  // global column of the tile
-    const int64_t gr = c0 + rb * 128 + rhalf * BM; // global row of the tile (N.. = z block)
+    const int64_t Jb = (int64_t)J * L.nb;
+    const int64_t gc = Jb + cb * 128 + half * BN;   // global column of the tile
+    const int64_t gr = Jb + rb * 128 + rhalf * BM;  // global row of the tile (N.. = z block)
     const int64_t kb = (int64_t)k * L.nb;
-    const double* Pk = ws + L.off(k);
     const int64_t ldk = L.ld(k);
     t.A = Pk + (gr - kb);
     t.B = Pk + (gc - kb);
     t.lda = ldk;
     t.ldb = ldk;
-    const int J = (int)(gc / L.nb);
-    const int64_t Jb = (int64_t)J * L.nb;
     t.ldc = L.ld(J);
     t.C = ws + L.off(J) + (gc - Jb) * t.ldc + (gr - Jb);
     t.K = L.nb;
     t.m_valid = BM;
     t.n_valid = BN;
-    return true;
-  }
-  // number of 128x128 blocks of all bands before band b, every one of them full
-  __host__ __device__ int64_t Sfull(int64_t b) const {
-    const int64_t G = band, A0 = (int64_t)Mb - cb_lo - G + 1;
-    // sum_{b'<b} [G(G+1)/2 + (A0 - b' G) G]
-    return b * (G * (G + 1) / 2) + G * (b * A0 - G * (b * (b - 1) / 2));
+    return gr + BM > gc;  // false: the tile lies strictly above the diagonal (skip it)
   }
   __host__ int64_t blocks(int BM, int BN) const {
-    int64_t tot = 0;
-    for (int b = 0; b < nbands(); ++b) tot += band_count(b);
-    return tot * (128 / BN) * (128 / BM);
+    if (npan <= 0) return 0;
+    return Sp(npan) * (128 / BN) * (128 / BM);
   }
 };
 

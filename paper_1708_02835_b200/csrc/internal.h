@@ -1,15 +1,19 @@
 // internal.h -- shared declarations of the sm_100a kernels and their host launchers.
 //
-// Data layout of the tile workspace ("lower block-column panels", DESIGN.md):
+// Data layout of the tile workspace ("lower block-column panels", DESIGN.md §5):
 //   n locations, tile size nb (multiple of 128), T = ceil(n/nb), N = T*nb.
 //   Panel j (0 <= j < T) holds global rows j*nb .. N-1 of columns j*nb .. j*nb+nb-1
 //   followed by ZR = 128 extra rows (the "z row block": its first row is z^T,
 //   the rest zeros), column-major with leading dimension ld_j = N - j*nb + ZR.
-//   Global element (r, c), c <= r < N + ZR, lives at
-//     base + off_j + (c - j*nb) * ld_j + (r - j*nb),   j = c / nb.
 //   Row r = N is the z row: after the factorization it holds y = L^{-1} z
 //   (the forward solve of Alg. 2 l.4 fused as an augmented row).
 //   Rows/cols n..N-1 are identity padding (exact for log|Sigma| and z^T Sigma^-1 z).
+//
+// Distribution: panels are dealt 1-D block-cyclically over `world`
+// ranks, panel j on rank j % world. A rank stores only its own panels, back to
+// back in increasing j; global element (r, c) of an owned panel j = c / nb lives at
+//     ws + off(j) + (c - j*nb) * ld_j + (r - j*nb).
+// world = 1 is the single-GPU case (every panel owned, off(j) = sum_{t<j} nb ld_t).
 #pragma once
 #include <cstddef>
 #include <cstdint>
@@ -19,19 +23,37 @@ namespace exageo {
 
 constexpr int ZR = 128;  // height of the z row block appended to every panel
 constexpr int PB = 64;   // inner panel block (POTRF block size)
-constexpr int kOutDoubles = 4 + 148;  // finish(): 3 results + scratch partials
+constexpr int kQuadBlocks = 148;  // CTAs of the local dot-product reduction
 
 struct Layout {
   int64_t n = 0;   // true problem size
   int nb = 0;      // tile size
   int T = 0;       // number of panels
   int64_t N = 0;   // padded size T*nb
+  int rank = 0;    // this rank
+  int world = 1;   // number of ranks (panel j lives on rank j % world)
+
   __host__ __device__ int64_t ld(int j) const { return N - (int64_t)j * nb + ZR; }
-  __host__ __device__ int64_t off(int j) const {
-    // sum_{t<j} nb * (N - t*nb + ZR)
-    return (int64_t)nb * ((int64_t)j * (N + ZR) - (int64_t)nb * ((int64_t)j * (j - 1) / 2));
+  __host__ __device__ bool owns(int j) const { return j % world == rank; }
+  __host__ __device__ int owner(int j) const { return j % world; }
+  // number of panels this rank owns
+  __host__ __device__ int owned() const { return T > rank ? (T - rank + world - 1) / world : 0; }
+  // j of the m-th owned panel
+  __host__ __device__ int owned_panel(int m) const { return rank + m * world; }
+  // first owned panel >= j
+  __host__ __device__ int first_owned_from(int j) const {
+    const int d = ((rank - j) % world + world) % world;
+    return j + d;
   }
-  __host__ __device__ int64_t total() const { return off(T); }
+  // local offset (doubles) of the m-th owned panel:
+  //   nb * sum_{i<m} ld(rank + i world) = nb [m (N + ZR - rank nb) - world nb m (m-1)/2]
+  __host__ __device__ int64_t off_m(int64_t m) const {
+    return (int64_t)nb * (m * (N + ZR - (int64_t)rank * nb) - (int64_t)world * nb * (m * (m - 1) / 2));
+  }
+  // local offset of owned panel j
+  __host__ __device__ int64_t off(int j) const { return off_m((j - rank) / world); }
+  // local storage (doubles)
+  __host__ __device__ int64_t total() const { return off_m(owned()); }
 };
 
 // Per-theta constants of the Matern evaluator (computed on the host in long
@@ -53,6 +75,7 @@ cudaError_t gemm_init();
 cudaError_t potrf_init();
 
 // ---- launchers (all asynchronous on `s`) ----
+// K1: generate this rank's panels of Sigma(theta) (identity padding, z in the z row block).
 void launch_gen_panels(const Layout& L, double* ws, const MaternConsts& mc, const double* x, const double* y,
                        const double* z, cudaStream_t s);
 void launch_matern_dense(const MaternConsts& mc, int64_t m, const double* x1, const double* y1, int64_t n,
@@ -63,28 +86,30 @@ void launch_matern_dense(const MaternConsts& mc, int64_t m, const double* x1, co
 // Variant tuned for N = 64 panel columns.
 void launch_gemm_panel(int64_t M, int N, int K, const double* A, int64_t lda, const double* B, int64_t ldb,
                        double* C, int64_t ldc, bool accumulate, const int* info, cudaStream_t s);
-// Trailing update of step k: for the 128x128 blocks (rb >= cb) of columns >= (k+1) nb,
-// rows >= (k+1) nb including the z row block: A_rc -= sum_t L_rt L_ct over panel k.
-// Restricted to 128-column blocks cb in [cb_lo, cb_hi) (cb_hi < 0: to the end).
-void launch_syrk_trailing(const Layout& L, double* ws, int k, int cb_lo, int cb_hi, const int* info,
-                          cudaStream_t s);
+// Trailing update by panel k (operand Pk, leading dimension ld(k): a rank's own panel k
+// or its received copy) of the owned panels J0, J0 + world, ..., (npan of them):
+// A_rc -= sum_t L_rt L_ct for every lower element and the z row of those panels.
+void launch_syrk_panels(const Layout& L, double* ws, const double* Pk, int k, int J0, int npan, const int* info,
+                        cudaStream_t s);
 // Factor the PB x PB diagonal block at `a` (ld) in place, write W = L^{-1} (PB x PB,
 // ld PB) and slot = sum log L_ii; info = first bad global pivot + 1.
 void launch_potrf_block(double* a, int64_t lda, double* W, double* logdet_slot, int* info, int64_t pivot_base,
                         cudaStream_t s);
-// out[0..2] = {loglik, logdet, quad}, from nslots logdet partial sums and the z row.
-// out must hold kOutDoubles doubles (the tail is scratch).
-void launch_finish(const Layout& L, const double* ws, const double* slots, int nslots, double* out,
-                   cudaStream_t s);
-// Copy the lower triangle of the workspace matrix to dense column-major dst (device).
+// out2 = {sum of this rank's log-det partials (nslots), sum of y_c^2 over this rank's columns};
+// scratch: kQuadBlocks doubles.
+void launch_local_partials(const Layout& L, const double* ws, const double* slots, int nslots, double* scratch,
+                           double* out2, cudaStream_t s);
+// out3 = {loglik, logdet, quad} from nparts pairs {logdet/2 partial, quad partial} summed in order.
+void launch_combine(const double* parts, int nparts, int64_t n, double* out3, cudaStream_t s);
+// Copy this rank's columns of the lower triangle to dense column-major dst (device).
 void launch_read_lower(const Layout& L, const double* ws, double* dst, int64_t ld, cudaStream_t s);
 void launch_read_zrow(const Layout& L, const double* ws, double* dst, cudaStream_t s);
-// out[i] = entry (rc[i], rc[count + i]) of the workspace matrix (lower triangle / z row).
+// out[i] = entry (rc[i], rc[count + i]) if this rank owns column rc[count + i] (else untouched).
 void launch_read_entries(const Layout& L, const double* ws, int64_t count, const int64_t* rc, double* out,
                          cudaStream_t s);
-// z = L e with L the factor in the workspace (Alg. 1 l.7, dtrmm): lower TRMV.
-// part: scratch of T * N doubles.
-void launch_trmv_lower(const Layout& L, const double* ws, const double* e, double* z, double* part,
-                       cudaStream_t s);
+// z (Alg. 1 l.7, dtrmm): part[m][r] = sum over the m-th owned panel's columns c <= r of L_rc e_c
+// (part: owned() * N doubles); then z[r] = sum of nparts slices of N doubles.
+void launch_trmv_partial(const Layout& L, const double* ws, const double* e, double* part, cudaStream_t s);
+void launch_trmv_sum(int64_t n, int64_t N, const double* part, int nparts, double* z, cudaStream_t s);
 
 }  // namespace exageo

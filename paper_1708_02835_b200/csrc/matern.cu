@@ -123,12 +123,12 @@ __device__ __forceinline__ double dist2d(double x1, double y1, double x2, double
   return sqrt(dx * dx + dy * dy);
 }
 
-// One CTA per (panel j = blockIdx.y, column cc = blockIdx.x) -> walks the rows
+// One CTA per (owned panel j = rank + world * blockIdx.y, column cc = blockIdx.x) -> walks the rows
 // of that column with coalesced double2 stores.
 __global__ void __launch_bounds__(256) gen_panels_kernel(Layout L, double* __restrict__ ws, MaternConsts mc,
                                                          const double* __restrict__ x, const double* __restrict__ y,
                                                          const double* __restrict__ z) {
-  const int j = blockIdx.y;
+  const int j = L.owned_panel(blockIdx.y);
   const int cc = blockIdx.x;
   const int64_t c = (int64_t)j * L.nb + cc;  // global column
   const int64_t ld = L.ld(j);
@@ -169,7 +169,8 @@ __global__ void __launch_bounds__(256) matern_dense_kernel(MaternConsts mc, int6
 
 void launch_gen_panels(const Layout& L, double* ws, const MaternConsts& mc, const double* x, const double* y,
                        const double* z, cudaStream_t s) {
-  dim3 grid(L.nb, L.T);
+  if (L.owned() == 0) return;
+  dim3 grid(L.nb, L.owned());
   gen_panels_kernel<<<grid, 256, 0, s>>>(L, ws, mc, x, y, z);
 }
 

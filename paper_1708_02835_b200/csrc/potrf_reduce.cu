@@ -9,9 +9,11 @@
 //    partial log-determinant sum_i log L_ii (R5). The first
 //    non-positive pivot is recorded as a global index (R14); every later
 //    kernel reads the info word and exits.
-//  * finish: logdet = 2 sum(partials), quad = sum y_i^2 over the z row
-//    (y = L^{-1} z, Alg. 2 l.4-6, R6-R7), l = -quad/2 - logdet/2 - n/2 log 2 pi
-//    (Alg. 2 l.7) -- fixed-order trees, bitwise reproducible.
+//  * reductions: per rank, logdet/2 = sum of its panels' partials and quad = sum y_c^2
+//    over its columns of the z row (y = L^{-1} z, Alg. 2 l.4-6, R6-R7); the ranks'
+//    pairs are combined (after an all-reduce when multi-GPU) into
+//    l = -quad/2 - logdet/2 - n/2 log 2 pi (Alg. 2 l.7). Fixed-order trees:
+//    bitwise reproducible for a fixed rank count.
 #include <cmath>
 
 #include "internal.h"
@@ -110,30 +112,38 @@ __device__ double block_sum(double v, double* red) {
   return r;  // valid in thread 0
 }
 
-constexpr int kFinishBlocks = 148;
+// y_c of owned column c (z row of its panel)
+__device__ __forceinline__ double zrow_value(const Layout& L, const double* ws, int64_t c) {
+  const int j = (int)(c / L.nb);
+  const int64_t jb = (int64_t)j * L.nb;
+  return ws[L.off(j) + (c - jb) * L.ld(j) + (L.N - jb)];
+}
 
-// Stage 1: kFinishBlocks CTAs, CTA b sums y_c^2 over its contiguous range of c.
+// Stage 1: kQuadBlocks CTAs; CTA b sums y_c^2 over a contiguous range of this rank's
+// columns (the owned panels' columns, in order, restricted to c < n).
 __global__ void __launch_bounds__(512) quad_partial_kernel(Layout L, const double* __restrict__ ws,
-                                                            double* __restrict__ part) {
+                                                           double* __restrict__ part) {
   __shared__ double red[32];
-  const int64_t per = (L.n + gridDim.x - 1) / gridDim.x;
+  const int64_t cols = (int64_t)L.owned() * L.nb;
+  const int64_t per = (cols + gridDim.x - 1) / gridDim.x;
   const int64_t lo = (int64_t)blockIdx.x * per;
-  const int64_t hi = (lo + per) < L.n ? (lo + per) : L.n;
+  const int64_t hi = (lo + per) < cols ? (lo + per) : cols;
   double v = 0.0;
-  for (int64_t c = lo + threadIdx.x; c < hi; c += blockDim.x) {
-    const int j = (int)(c / L.nb);
-    const int64_t jb = (int64_t)j * L.nb;
-    const double yv = ws[L.off(j) + (c - jb) * L.ld(j) + (L.N - jb)];
-    v += yv * yv;
+  for (int64_t idx = lo + threadIdx.x; idx < hi; idx += blockDim.x) {
+    const int64_t c = (int64_t)L.owned_panel((int)(idx / L.nb)) * L.nb + idx % L.nb;
+    if (c < L.n) {
+      const double yv = zrow_value(L, ws, c);
+      v += yv * yv;
+    }
   }
   const double s = block_sum(v, red);
   if (threadIdx.x == 0) part[blockIdx.x] = s;
 }
 
-// Stage 2: one CTA combines the partials in fixed order.
-__global__ void __launch_bounds__(1024) finish_kernel(Layout L, const double* __restrict__ slots, int nslots,
-                                                      const double* __restrict__ part, int nparts,
-                                                      double* __restrict__ out) {
+// Stage 2 (one CTA): out2 = {sum of log-det slots, sum of the quad partials}, fixed order.
+__global__ void __launch_bounds__(1024) local_partials_kernel(const double* __restrict__ slots, int nslots,
+                                                              const double* __restrict__ part, int nparts,
+                                                              double* __restrict__ out2) {
   __shared__ double red[32];
   double a = 0.0, b = 0.0;
   for (int i = threadIdx.x; i < nslots; i += blockDim.x) a += slots[i];
@@ -141,17 +151,31 @@ __global__ void __launch_bounds__(1024) finish_kernel(Layout L, const double* __
   const double sa = block_sum(a, red);
   const double sb = block_sum(b, red);
   if (threadIdx.x == 0) {
-    const double logdet = 2.0 * sa;
-    const double quad = sb;
-    const double log2pi = 1.8378770664093454835606594728112;
-    out[0] = -0.5 * quad - 0.5 * logdet - 0.5 * (double)L.n * log2pi;
-    out[1] = logdet;
-    out[2] = quad;
+    out2[0] = sa;
+    out2[1] = sb;
   }
 }
 
+// Combine the ranks' pairs in rank order: logdet = 2 sum(slots), quad = sum(y^2),
+// l = -quad/2 - logdet/2 - (n/2) log 2 pi (Alg. 2 l.7).
+__global__ void combine_kernel(const double* __restrict__ parts, int nparts, int64_t n, double* __restrict__ out3) {
+  if (threadIdx.x != 0) return;
+  double a = 0.0, b = 0.0;
+  for (int i = 0; i < nparts; ++i) {
+    a += parts[2 * i];
+    b += parts[2 * i + 1];
+  }
+  const double logdet = 2.0 * a;
+  const double log2pi = 1.8378770664093454835606594728112;
+  out3[0] = -0.5 * b - 0.5 * logdet - 0.5 * (double)n * log2pi;
+  out3[1] = logdet;
+  out3[2] = b;
+}
+
+// One CTA per owned column.
 __global__ void read_lower_kernel(Layout L, const double* __restrict__ ws, double* __restrict__ dst, int64_t ld) {
-  const int64_t c = blockIdx.x;
+  const int64_t c = (int64_t)L.owned_panel((int)(blockIdx.x / L.nb)) * L.nb + blockIdx.x % L.nb;
+  if (c >= L.n) return;
   const int j = (int)(c / L.nb);
   const int64_t jb = (int64_t)j * L.nb;
   const double* col = ws + L.off(j) + (c - jb) * L.ld(j) - jb;  // index by global row
@@ -159,10 +183,11 @@ __global__ void read_lower_kernel(Layout L, const double* __restrict__ ws, doubl
 }
 
 __global__ void read_zrow_kernel(Layout L, const double* __restrict__ ws, double* __restrict__ dst) {
-  for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < L.n; c += (int64_t)gridDim.x * blockDim.x) {
-    const int j = (int)(c / L.nb);
-    const int64_t jb = (int64_t)j * L.nb;
-    dst[c] = ws[L.off(j) + (c - jb) * L.ld(j) + (L.N - jb)];
+  const int64_t cols = (int64_t)L.owned() * L.nb;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < cols;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = (int64_t)L.owned_panel((int)(idx / L.nb)) * L.nb + idx % L.nb;
+    if (c < L.n) dst[c] = zrow_value(L, ws, c);
   }
 }
 
@@ -171,15 +196,17 @@ __global__ void read_entries_kernel(Layout L, const double* __restrict__ ws, int
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = rc[i], c = rc[count + i];
     const int j = (int)(c / L.nb);
+    if (!L.owns(j)) continue;
     const int64_t jb = (int64_t)j * L.nb;
     out[i] = ws[L.off(j) + (c - jb) * L.ld(j) + (r - jb)];
   }
 }
 
-// TRMV stage 1: part[j][r] = sum_{c in panel j, c <= r} L[r][c] e[c]  (grid: row blocks x panels).
+// TRMV stage 1: part[m][r] = sum_{c in owned panel m, c <= r, c < n} L_rc e_c  (grid: row blocks x owned panels).
 __global__ void __launch_bounds__(256) trmv_partial_kernel(Layout L, const double* __restrict__ ws,
                                                            const double* __restrict__ e, double* __restrict__ part) {
-  const int j = blockIdx.y;
+  const int m = blockIdx.y;
+  const int j = L.owned_panel(m);
   const int64_t jb = (int64_t)j * L.nb;
   const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= L.N) return;
@@ -193,14 +220,15 @@ __global__ void __launch_bounds__(256) trmv_partial_kernel(Layout L, const doubl
       if (c < L.n) acc += P[cc * ld] * e[c];
     }
   }
-  part[(int64_t)j * L.N + r] = acc;
+  part[(int64_t)m * L.N + r] = acc;
 }
 
-__global__ void trmv_sum_kernel(Layout L, const double* __restrict__ part, double* __restrict__ z) {
+__global__ void trmv_sum_kernel(int64_t n, int64_t N, const double* __restrict__ part, int nparts,
+                                double* __restrict__ z) {
   const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= L.n) return;
+  if (r >= n) return;
   double acc = 0.0;
-  for (int j = 0; j < L.T; ++j) acc += part[(int64_t)j * L.N + r];
+  for (int j = 0; j < nparts; ++j) acc += part[(int64_t)j * N + r];
   z[r] = acc;
 }
 
@@ -217,15 +245,19 @@ void launch_potrf_block(double* a, int64_t lda, double* W, double* slot, int* in
   potrf_block_kernel<<<1, 256, kPotrfSmem, s>>>(a, lda, W, slot, info, pivot_base);
 }
 
-void launch_finish(const Layout& L, const double* ws, const double* slots, int nslots, double* out, cudaStream_t s) {
-  // out[3 .. 3 + kFinishBlocks) is scratch for the partial dot products.
-  double* part = out + 4;
-  quad_partial_kernel<<<kFinishBlocks, 512, 0, s>>>(L, ws, part);
-  finish_kernel<<<1, 1024, 0, s>>>(L, slots, nslots, part, kFinishBlocks, out);
+void launch_local_partials(const Layout& L, const double* ws, const double* slots, int nslots, double* scratch,
+                           double* out2, cudaStream_t s) {
+  quad_partial_kernel<<<kQuadBlocks, 512, 0, s>>>(L, ws, scratch);
+  local_partials_kernel<<<1, 1024, 0, s>>>(slots, nslots, scratch, kQuadBlocks, out2);
+}
+
+void launch_combine(const double* parts, int nparts, int64_t n, double* out3, cudaStream_t s) {
+  combine_kernel<<<1, 32, 0, s>>>(parts, nparts, n, out3);
 }
 
 void launch_read_lower(const Layout& L, const double* ws, double* dst, int64_t ld, cudaStream_t s) {
-  read_lower_kernel<<<(unsigned)L.n, 256, 0, s>>>(L, ws, dst, ld);
+  if (L.owned() == 0) return;
+  read_lower_kernel<<<(unsigned)(L.owned() * L.nb), 256, 0, s>>>(L, ws, dst, ld);
 }
 
 void launch_read_zrow(const Layout& L, const double* ws, double* dst, cudaStream_t s) {
@@ -240,11 +272,14 @@ void launch_read_entries(const Layout& L, const double* ws, int64_t count, const
   read_entries_kernel<<<g, 256, 0, s>>>(L, ws, count, rc, out);
 }
 
-void launch_trmv_lower(const Layout& L, const double* ws, const double* e, double* z, double* part,
-                       cudaStream_t s) {
-  dim3 g1((unsigned)((L.N + 255) / 256), (unsigned)L.T);
+void launch_trmv_partial(const Layout& L, const double* ws, const double* e, double* part, cudaStream_t s) {
+  if (L.owned() == 0) return;
+  dim3 g1((unsigned)((L.N + 255) / 256), (unsigned)L.owned());
   trmv_partial_kernel<<<g1, 256, 0, s>>>(L, ws, e, part);
-  trmv_sum_kernel<<<(unsigned)((L.n + 255) / 256), 256, 0, s>>>(L, part, z);
+}
+
+void launch_trmv_sum(int64_t n, int64_t N, const double* part, int nparts, double* z, cudaStream_t s) {
+  trmv_sum_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, N, part, nparts, z);
 }
 
 }  // namespace exageo

@@ -1,6 +1,8 @@
-// test_syrkmap.cu -- host-side check of the trailing-update tile enumeration (SyrkMap):
-// every lower 128-block (rb >= cb, incl. the z row block rb == Mb) of the requested
-// column range is produced exactly once, and pointers match the panel layout formula.
+// test_syrkmap.cu -- host-side check of the trailing-update tile enumeration (SyrkMap)
+// and of the distributed layout: for every (world, rank, k, J0, npan) every lower
+// 128-block of the selected owned panels (incl. the z row block) is produced exactly
+// once (as BM x BN sub-tiles), and A/B/C pointers agree with the panel layout formula;
+// owned-panel offsets tile the rank's storage without overlap.
 #include <cstdio>
 #include <set>
 #include <tuple>
@@ -10,46 +12,113 @@
 using namespace exageo;
 using namespace exageo::gemm;
 
-int check(int T, int nb, int k, int cb_lo, int cb_hi, int band) {
+template <int BM, int BN>
+int check(int T, int nb, int world, int rank, int k, int J0, int npan) {
   Layout L;
   L.nb = nb;
   L.T = T;
   L.N = (int64_t)T * nb;
   L.n = L.N - 3;
-  static double dummy[1];
-  double* ws = dummy;
+  L.rank = rank;
+  L.world = world;
+  static double ws_dummy[1], pk_dummy[1];
   SyrkMap m;
   m.L = L;
-  m.ws = ws;
+  m.ws = ws_dummy;
+  m.Pk = pk_dummy;
   m.k = k;
-  m.Mb = (int)((L.N - (int64_t)(k + 1) * nb) / 128);
-  m.cb_lo = cb_lo;
-  m.cb_hi = cb_hi < 0 ? m.Mb : cb_hi;
-  m.band = band;
-  const int64_t nblk = m.blocks(128, 64);
+  m.J0 = J0;
+  m.npan = npan;
+  const int64_t nblk = m.blocks(BM, BN);
   std::set<std::tuple<int64_t, int64_t>> seen;
-  const int64_t c0 = (int64_t)(k + 1) * nb, kb = (int64_t)k * nb;
+  const int64_t kb = (int64_t)k * nb;
   for (int64_t b = 0; b < nblk; ++b) {
     GemmTile t;
-    m.operator()<128, 64>(b, t);
-    // recover (global row, global col) from the A and B pointers of panel k
-    const int64_t gr = (t.A - (ws + L.off(k))) + kb;
-    const int64_t gc = (t.B - (ws + L.off(k))) + kb;
+    const bool active = m.operator()<BM, BN>(b, t);
+    const int64_t gr = (t.A - pk_dummy) + kb;
+    const int64_t gc = (t.B - pk_dummy) + kb;
+    if (!active) {
+      if (gr + BM > gc) {
+        printf("lower tile skipped gr=%lld gc=%lld\n", (long long)gr, (long long)gc);
+        return 1;
+      }
+      continue;
+    }
     const int J = (int)(gc / nb);
     const int64_t Jb = (int64_t)J * nb;
-    if (t.C != ws + L.off(J) + (gc - Jb) * L.ld(J) + (gr - Jb)) { printf("bad C ptr\n"); return 1; }
-    const int64_t rb = (gr - c0) / 128, cb = (gc - c0) / 128;
-    if (rb < cb || rb > m.Mb || cb < m.cb_lo || cb >= m.cb_hi) {
-      printf("out of range rb=%lld cb=%lld\n", (long long)rb, (long long)cb);
+    if (!L.owns(J) || J < J0 || (J - J0) % world != 0 || (J - J0) / world >= npan) {
+      printf("panel %d not selected\n", J);
       return 1;
     }
-    if (!seen.insert({gr, gc}).second) { printf("duplicate\n"); return 1; }
+    if (t.C != ws_dummy + L.off(J) + (gc - Jb) * L.ld(J) + (gr - Jb)) {
+      printf("bad C ptr\n");
+      return 1;
+    }
+    if (t.lda != L.ld(k) || t.ldb != L.ld(k) || t.ldc != L.ld(J) || t.K != nb) {
+      printf("bad ld/K\n");
+      return 1;
+    }
+    // tile must intersect the lower triangle of panel J or be in the z block
+    if (gr + BM - 1 < gc || gr > L.N + ZR - BM) {
+      printf("out of range gr=%lld gc=%lld\n", (long long)gr, (long long)gc);
+      return 1;
+    }
+    if (!seen.insert({gr, gc}).second) {
+      printf("duplicate\n");
+      return 1;
+    }
   }
-  int64_t expect = 0;
-  for (int64_t cb = m.cb_lo; cb < m.cb_hi; ++cb) expect += (m.Mb + 1 - cb) * 2;
+  // expected: for each selected panel, each 128-col block cb, rows from cb to the z block
+  int64_t expect = 0;  // sub-tiles of the lower 128-blocks that reach the lower triangle
+  for (int i = 0; i < npan; ++i) {
+    const int J = J0 + i * world;
+    const int64_t Mr = (L.N - (int64_t)J * nb) / 128;
+    for (int cb = 0; cb < nb / 128; ++cb)
+      for (int64_t rb = cb; rb <= Mr; ++rb)
+        for (int rh = 0; rh < 128 / BM; ++rh)
+          for (int ch = 0; ch < 128 / BN; ++ch) {
+            const int64_t gr = (int64_t)J * nb + rb * 128 + rh * BM, gc = (int64_t)J * nb + cb * 128 + ch * BN;
+            if (gr + BM > gc) ++expect;
+          }
+  }
   if ((int64_t)seen.size() != expect) {
-    printf("count %lld != %lld (T=%d k=%d lo=%d hi=%d band=%d)\n", (long long)seen.size(), (long long)expect, T, k,
-           cb_lo, m.cb_hi, band);
+    printf("count %lld != %lld (T=%d nb=%d world=%d rank=%d k=%d J0=%d npan=%d)\n", (long long)seen.size(),
+           (long long)expect, T, nb, world, rank, k, J0, npan);
+    return 1;
+  }
+  return 0;
+}
+
+int check_offsets(int T, int nb, int world) {
+  // panels of all ranks: each rank's offsets are disjoint, increasing, and sum to total()
+  int64_t sum = 0;
+  for (int r = 0; r < world; ++r) {
+    Layout L;
+    L.nb = nb;
+    L.T = T;
+    L.N = (int64_t)T * nb;
+    L.rank = r;
+    L.world = world;
+    int64_t expect_off = 0;
+    for (int j = r; j < T; j += world) {
+      if (L.off(j) != expect_off) {
+        printf("offset mismatch world=%d rank=%d j=%d\n", world, r, j);
+        return 1;
+      }
+      expect_off += (int64_t)nb * L.ld(j);
+    }
+    if (L.total() != expect_off) {
+      printf("total mismatch\n");
+      return 1;
+    }
+    sum += L.total();
+  }
+  Layout G;
+  G.nb = nb;
+  G.T = T;
+  G.N = (int64_t)T * nb;
+  if (sum != G.total()) {
+    printf("ranks do not partition the matrix\n");
     return 1;
   }
   return 0;
@@ -59,17 +128,31 @@ int main() {
   int bad = 0, n = 0;
   for (int nb : {128, 256, 512})
     for (int T : {2, 3, 7, 20})
-      for (int k = 0; k + 1 < T; ++k)
-        for (int band : {1, 3, 4, 8, 16}) {
-          const int cpt = nb / 128;
-          const int Mb = (T - k - 1) * cpt;
-          bad += check(T, nb, k, 0, -1, band);
-          bad += check(T, nb, k, 0, cpt < Mb ? cpt : Mb, band);
-          if (cpt < Mb) bad += check(T, nb, k, cpt, -1, band);
-          n += 3;
-        }
-  bad += check(196, 512, 0, 4, -1, 8);
-  bad += check(196, 512, 100, 4, -1, 8);
+      for (int world : {1, 2, 3, 4, 8}) {
+        bad += check_offsets(T, nb, world);
+        ++n;
+        for (int rank = 0; rank < world; ++rank)
+          for (int k = 0; k + 1 < T; ++k) {
+            Layout L;
+            L.T = T;
+            L.rank = rank;
+            L.world = world;
+            // U1(k): panel k+1 on its owner; U2(k): owned panels from k+1 (or k+2)
+            if (L.owns(k + 1)) {
+              bad += check<64, 64>(T, nb, world, rank, k, k + 1, 1);
+              bad += check<128, 64>(T, nb, world, rank, k, k + 1, 1);
+            }
+            const int J0 = L.first_owned_from(L.owns(k + 1) ? k + 2 : k + 1);
+            const int npan = J0 < T ? (T - 1 - J0) / world + 1 : 0;
+            if (npan > 0) {
+              bad += check<64, 64>(T, nb, world, rank, k, J0, npan);
+              bad += check<128, 128>(T, nb, world, rank, k, J0, npan);
+            }
+            n += 2;
+          }
+      }
+  bad += check<64, 64>(196, 512, 1, 0, 0, 2, 194);
+  bad += check<64, 64>(586, 512, 8, 3, 5, 11, 72);
   printf("%s: %d failures in %d enumerations\n", bad ? "FAIL" : "OK", bad, n + 2);
   return bad ? 1 : 0;
 }
