@@ -159,6 +159,24 @@ exageo_status exageo_loglik_dev(exageo_ctx* ctx, const exageo_theta* theta, int6
 exageo_status exageo_simulate(exageo_ctx* ctx, const exageo_theta* theta, int64_t n, const double* x,
                               const double* y, const double* e, double* z);
 
+/* Maximum-likelihood estimate theta_hat = argmax_theta l(theta) over the box
+ * lo <= theta <= hi, the paper's optimization loop with a
+ * derivative-free bound-constrained search (R16): Nelder-Mead on log(theta), trial
+ * points projected onto the box, restarted from the best vertex while that improves;
+ * each evaluation is one exageo_loglik on inputs copied to the device once. A
+ * parameter with lo == hi is held fixed. Non-positive-definite evaluations count as
+ * l = -inf. Stops when the simplex diameter in log(theta) (= relative change
+ * of theta) is below xtol_rel, or after max_evals evaluations.
+ * x, y, z: host arrays of n doubles. Outputs: *theta_hat, *loglik = l(theta_hat)
+ * (may be NULL), *nevals (may be NULL), trace (may be NULL): 4 doubles
+ * {theta1, theta2, theta3, l} per evaluation, room for max_evals.
+ * EXAGEO_EINVAL unless 0 < lo <= start <= hi; EXAGEO_EFIT if every evaluation failed.
+ * Collective on distributed contexts: every rank runs the same deterministic search
+ * on the same (all-reduced) l values. */
+exageo_status exageo_mle(exageo_ctx* ctx, int64_t n, const double* x, const double* y, const double* z,
+                         const exageo_theta* lo, const exageo_theta* hi, const exageo_theta* start, double xtol_rel,
+                         int max_evals, exageo_theta* theta_hat, double* loglik, int* nevals, double* trace);
+
 /* --- Stage-level entry points (same kernels as exageo_loglik_dev, exposed
  *     so that each step of Alg. 2 can be checked on its own). ---------- */
 

@@ -206,3 +206,39 @@ def predict(x, y, z, xnew, ynew, theta) -> np.ndarray:
 
 def num_threads() -> int:
     return int(lib().oracle_num_threads())
+
+
+def mle(x, y, z, lo, hi, start, xtol: float = 1e-10, max_evals: int = 4000):
+    """Oracle MLE: maximise the oracle's l(theta) over lo <= theta <= hi.
+
+    Library optimisers as steps (R16: any derivative-free bound-constrained search):
+    scipy Nelder-Mead on log(theta) from `start`, polished by L-BFGS-B (finite
+    differences). Non-PD evaluations count as l = -inf. Returns (theta_hat, l, nevals)."""
+    import scipy.optimize as so
+
+    x, y, z = _f(x), _f(y), _f(z)
+    lo_u, hi_u = np.log(np.asarray(lo, float)), np.log(np.asarray(hi, float))
+    cnt = [0]
+
+    def f(u):
+        cnt[0] += 1
+        u = np.clip(u, lo_u, hi_u)
+        try:
+            return -loglik(x, y, z, np.exp(u))[0]
+        except NotPositiveDefinite:
+            return 1e300
+
+    b = list(zip(lo_u, hi_u))
+    r = so.minimize(f, np.log(np.asarray(start, float)), method="Nelder-Mead", bounds=b,
+                    options=dict(xatol=xtol, fatol=1e-13, maxfev=max_evals, adaptive=True))
+    r2 = so.minimize(f, r.x, method="L-BFGS-B", bounds=b, options=dict(ftol=1e-15, gtol=1e-10, maxfun=max_evals))
+    best = r2 if r2.fun <= r.fun else r
+    return tuple(np.exp(np.clip(best.x, lo_u, hi_u))), -float(best.fun), cnt[0]
+
+
+def profile_sigma2(x, y, z, beta: float, nu: float) -> float:
+    """theta1 maximising l for fixed (theta2, theta3): z^T R^{-1} z / n, R = Sigma(1, theta2, theta3).
+
+    From Eq. (1) with Sigma = theta1 R: dl/dtheta1 = -n/(2 theta1) + z^T R^{-1} z / (2 theta1^2) = 0."""
+    _, _, quad = loglik(x, y, z, (1.0, beta, nu))
+    return quad / len(z)

@@ -74,6 +74,9 @@ SIGNATURES = [
     ("exageo_read_lower", ctypes.c_int, [_C, _f64p, ctypes.c_int64]),
     ("exageo_read_zrow", ctypes.c_int, [_C, _f64p]),
     ("exageo_read_entries", ctypes.c_int, [_C, ctypes.c_int64, _i64p, _i64p, _f64p]),
+    ("exageo_mle", ctypes.c_int, [_C, ctypes.c_int64, _f64p, _f64p, _f64p, ctypes.POINTER(Theta),
+                                  ctypes.POINTER(Theta), ctypes.POINTER(Theta), ctypes.c_double, ctypes.c_int,
+                                  ctypes.POINTER(Theta), _f64p, ctypes.POINTER(ctypes.c_int), _f64p]),
 ]
 
 _lib = None
@@ -148,6 +151,8 @@ class Result:
 
 def nccl_unique_id() -> bytes:
     """A fresh 128-byte NCCL unique id (create on rank 0, share with every rank)."""
+    import torch  # noqa: F401  -- load torch's libnccl first; the library then reuses it
+
     buf = ctypes.create_string_buffer(128)
     st = load_library().exageo_nccl_unique_id(buf, 128)
     if st != OK:
@@ -264,6 +269,22 @@ class Context:
                                          ctypes.byref(out), ctypes.byref(info))
         self._check(st, info.npd_pivot)
         return Result(info.loglik, info.logdet, info.quad, info.as_dict())
+
+    def mle(self, x, y, z, lo, hi, start, xtol_rel: float = 1e-9, max_evals: int = 1000):
+        """Maximum-likelihood estimate over the box lo <= theta <= hi (exageo_mle).
+
+        Returns (theta_hat tuple, loglik, nevals, trace as an (nevals, 4) array)."""
+        x, y, z = _f(x), _f(y), _f(z)
+        tlo, thi, ts = _theta(lo), _theta(hi), _theta(start)
+        th = Theta()
+        ll = ctypes.c_double()
+        ne = ctypes.c_int()
+        trace = np.zeros((max_evals, 4), np.float64)
+        st = self._lib.exageo_mle(self._ctx, z.size, _p(x), _p(y), _p(z), ctypes.byref(tlo), ctypes.byref(thi),
+                                  ctypes.byref(ts), float(xtol_rel), int(max_evals), ctypes.byref(th),
+                                  ctypes.byref(ll), ctypes.byref(ne), _p(trace))
+        self._check(st)
+        return (th.sigma2, th.beta, th.nu), ll.value, ne.value, trace[: ne.value].copy()
 
     def simulate(self, x, y, e, theta) -> np.ndarray:
         """Alg. 1: z = L(theta) e for given normal variates e."""

@@ -22,7 +22,7 @@ CSRC = os.path.join(HERE, "csrc")
 OUT_DIR = os.path.join(HERE, "_lib")
 LIB = os.path.join(OUT_DIR, "libexageo.so")
 INCLUDE = os.path.join(ROOT, "include")
-SOURCES = ["api.cu", "matern.cu", "gemm_dmma.cu", "potrf_reduce.cu", "locations.cpp"]
+SOURCES = ["api.cu", "matern.cu", "gemm_dmma.cu", "potrf_reduce.cu", "locations.cpp", "mle.cpp", "nccl_dyn.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -75,7 +75,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     with ThreadPoolExecutor(max_workers=min(8, max(1, len(jobs)))) as ex:
         list(ex.map(run, jobs))
     if force or jobs or _stale(objs, LIB):
-        cmd = [nvcc(), "-shared"] + ARCH + ["-cudart", "static", "-o", LIB] + objs + ["-lnccl"]
+        # NCCL is resolved at run time (csrc/nccl_dyn.cpp), not linked
+        cmd = [nvcc(), "-shared"] + ARCH + ["-cudart", "static", "-o", LIB] + objs + ["-ldl"]
         run(cmd)
     return LIB
 

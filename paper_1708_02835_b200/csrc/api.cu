@@ -25,6 +25,7 @@
 #include <vector>
 
 #include "context.h"
+#include "nccl_dyn.h"
 
 namespace exageo {
 int gen_locations_host(int64_t n, uint64_t seed, double* x, double* y);
@@ -53,7 +54,7 @@ exageo_status fail(exageo_ctx* c, exageo_status s, const std::string& msg) {
   do {                                                                                               \
     ncclResult_t r_ = (call);                                                                        \
     if (r_ != ncclSuccess)                                                                           \
-      return fail((ctx), EXAGEO_ENCCL, std::string(#call) + ": " + ncclGetErrorString(r_));         \
+      return fail((ctx), EXAGEO_ENCCL, std::string(#call) + ": " + nccl::GetErrorString(r_));       \
   } while (0)
 
 bool theta_ok(const exageo_theta* t) {
@@ -275,7 +276,7 @@ exageo_status broadcast_panel(exageo_ctx* c, int j) {
       }
       buf = R.recv[j & 1];
     }
-    NCCL_TRY(c, ncclBroadcast(buf, buf, bytes / sizeof(double), ncclDouble, o, c->comm, R.s_comm));
+    NCCL_TRY(c, nccl::Broadcast(buf, buf, bytes / sizeof(double), ncclDouble, o, c->comm, R.s_comm));
     CUDA_TRY(c, cudaEventRecord(R.ev_recv[j & 1], R.s_comm));
     return EXAGEO_OK;
   }
@@ -381,7 +382,7 @@ exageo_status first_pivot(exageo_ctx* c, int64_t* pivot) {
   }
   if (!c->virt && c->world > 1) {
     CUDA_TRY(c, cudaMemcpyAsync(c->pivbuf, &best, sizeof(int64_t), cudaMemcpyHostToDevice, c->stream));
-    NCCL_TRY(c, ncclAllReduce(c->pivbuf, c->pivbuf, 1, ncclInt64, ncclMin, c->comm, c->stream));
+    NCCL_TRY(c, nccl::AllReduce(c->pivbuf, c->pivbuf, 1, ncclInt64, ncclMin, c->comm, c->stream));
     CUDA_TRY(c, cudaMemcpyAsync(&best, c->pivbuf, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   }
@@ -397,7 +398,7 @@ exageo_status do_finish(exageo_ctx* c, double* out3, int64_t* pivot) {
   }
   int nparts = (int)c->rs.size();
   if (!c->virt && c->world > 1) {
-    NCCL_TRY(c, ncclAllReduce(c->parts, c->parts, 2, ncclDouble, ncclSum, c->comm, c->stream));
+    NCCL_TRY(c, nccl::AllReduce(c->parts, c->parts, 2, ncclDouble, ncclSum, c->comm, c->stream));
     nparts = 1;
   }
   launch_combine(c->parts, nparts, c->G.n, c->out3, c->stream);
@@ -472,6 +473,23 @@ exageo_status loglik_device(exageo_ctx* c, const exageo_theta* t, int64_t n, con
   return st;
 }
 
+}  // namespace
+
+namespace exageo {
+exageo_status eval_loglik(exageo_ctx* c, const exageo_theta* t, int64_t n, const double* x_d, const double* y_d,
+                          const double* z_d, double* ll) {
+  return loglik_device(c, t, n, x_d, y_d, z_d, ll, nullptr);
+}
+exageo_status staging(exageo_ctx* c, int64_t n, double** buf) {
+  exageo_status st = ensure_vec(c, n);
+  *buf = c->vec;
+  return st;
+}
+exageo_status set_error(exageo_ctx* c, exageo_status s, const std::string& msg) { return fail(c, s, msg); }
+}  // namespace exageo
+
+namespace {
+
 void destroy_rank(RankState& R) {
   if (R.ws && !R.ws_external) cudaFree(R.ws);
   for (auto p : R.recv) cudaFree(p);
@@ -527,8 +545,11 @@ const char* exageo_last_error(const exageo_ctx* ctx) { return ctx ? ctx->err.c_s
 exageo_status exageo_nccl_unique_id(void* out, size_t len) {
   if (!out || len < sizeof(ncclUniqueId)) return fail(nullptr, EXAGEO_EINVAL, "need a 128-byte buffer");
   ncclUniqueId id;
-  ncclResult_t r = ncclGetUniqueId(&id);
-  if (r != ncclSuccess) return fail(nullptr, EXAGEO_ENCCL, std::string("ncclGetUniqueId: ") + ncclGetErrorString(r));
+  std::string lerr;
+  if (!nccl::load(&lerr)) return fail(nullptr, EXAGEO_ENCCL, lerr);
+  ncclResult_t r = nccl::GetUniqueId(&id);
+  if (r != ncclSuccess)
+    return fail(nullptr, EXAGEO_ENCCL, std::string("ncclGetUniqueId: ") + nccl::GetErrorString(r));
   memcpy(out, &id, sizeof(id));
   return EXAGEO_OK;
 }
@@ -584,9 +605,15 @@ exageo_status exageo_create(exageo_ctx** out, const exageo_opts* opts) {
   if (!c->virt && c->world > 1) {
     ncclUniqueId id;
     memcpy(&id, o.nccl_id, sizeof(id));
-    ncclResult_t r = ncclCommInitRank(&c->comm, c->world, id, c->rank);
+    std::string lerr;
+    if (!nccl::load(&lerr)) {
+      g_create_err = lerr;
+      exageo_destroy(c);
+      return EXAGEO_ENCCL;
+    }
+    ncclResult_t r = nccl::CommInitRank(&c->comm, c->world, id, c->rank);
     if (r != ncclSuccess) {
-      g_create_err = std::string("ncclCommInitRank: ") + ncclGetErrorString(r);
+      g_create_err = std::string("ncclCommInitRank: ") + nccl::GetErrorString(r);
       c->comm = nullptr;
       exageo_destroy(c);
       return EXAGEO_ENCCL;
@@ -600,7 +627,7 @@ void exageo_destroy(exageo_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
-  if (c->comm) ncclCommDestroy(c->comm);
+  if (c->comm) nccl::CommDestroy(c->comm);
   for (auto& R : c->rs) destroy_rank(R);
   cudaFree(c->parts);
   cudaFree(c->out3);
@@ -723,7 +750,7 @@ exageo_status exageo_simulate(exageo_ctx* c, const exageo_theta* t, int64_t n, c
   }
   if (!c->virt && c->world > 1) {
     launch_trmv_sum(n, G.N, R0.part, slices, c->zsum, c->stream);
-    NCCL_TRY(c, ncclAllReduce(c->zsum, dz, n, ncclDouble, ncclSum, c->comm, c->stream));
+    NCCL_TRY(c, nccl::AllReduce(c->zsum, dz, n, ncclDouble, ncclSum, c->comm, c->stream));
   } else {
     launch_trmv_sum(n, G.N, R0.part, slices, dz, c->stream);
   }

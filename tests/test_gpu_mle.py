@@ -1,0 +1,88 @@
+"""GPU exageo_mle (NEXT-1): theta_hat of the product's derivative-free search
+against the ORACLE's estimate (tests/golden/mle_n400.json, written by
+tools/make_golden_mle.py from oracle.mle) within 1e-4 relative (BASELINE north_star), and
+the stationarity pins evaluated with the oracle: profile identity in theta1 and
+coordinate-wise local maximum; BASELINE configs[1] (n = 1600, nu in {0.5, 1.0})."""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import synth_inputs as si
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_1708_02835_b200 as ex  # noqa: E402
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "mle_n400.json")
+LO, HI = (0.01, 0.01, 0.1), (5.0, 2.0, 2.0)
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    c = ex.Context(device=0)
+    yield c
+    c.close()
+
+
+def test_mle_matches_oracle_estimate(ctx):
+    g = json.load(open(GOLDEN))
+    n = g["n"]
+    x, y = ex.gen_locations(n, g["seed"])
+    z = oracle.simulate(x, y, tuple(g["theta_true"]), si.normals(n, g["seed"]))
+    th, ll, ne, trace = ctx.mle(x, y, z, tuple(g["lo"]), tuple(g["hi"]), tuple(g["start"]), xtol_rel=1e-10,
+                                max_evals=3000)
+    ref = g["theta_hat"]
+    for a, b in zip(th, ref):
+        assert a == pytest.approx(b, rel=1e-4), (th, ref)
+    assert ll == pytest.approx(g["loglik"], rel=1e-10)
+    assert ne == len(trace) and ne <= 3000
+    assert np.max(trace[:, 3]) == pytest.approx(ll, rel=1e-15)
+    # the oracle agrees that theta_hat is stationary in theta1 (profile identity)
+    assert th[0] == pytest.approx(oracle.profile_sigma2(x, y, z, th[1], th[2]), rel=1e-4)
+
+
+@pytest.mark.parametrize("nu_true", [0.5, 1.0])
+def test_mle_config2_n1600(ctx, nu_true):
+    n = 1600
+    theta_true = (1.0, 0.1, nu_true)
+    x, y = ex.gen_locations(n, 2)
+    z = ctx.simulate(x, y, si.normals(n, 2), theta_true)
+    start = tuple(math.sqrt(a * b) for a, b in zip(LO, HI))
+    th, ll, ne, trace = ctx.mle(x, y, z, LO, HI, start, xtol_rel=1e-9, max_evals=3000)
+    assert all(a <= t <= b for a, t, b in zip(LO, th, HI))
+    assert ll >= ctx.loglik(x, y, z, theta_true).loglik
+    # profile identity with the oracle at the product's (theta2, theta3)
+    assert th[0] == pytest.approx(oracle.profile_sigma2(x, y, z, th[1], th[2]), rel=1e-4)
+    # coordinate-wise local maximum on the GPU likelihood
+    for p in range(3):
+        for s in (1 - 1e-3, 1 + 1e-3):
+            t = list(th)
+            t[p] *= s
+            t[p] = min(max(t[p], LO[p]), HI[p])
+            assert ctx.loglik(x, y, z, t).loglik <= ll + 1e-9 * abs(ll)
+    # estimates near the truth (statistical sanity)
+    assert abs(th[2] - nu_true) < 0.25
+
+
+def test_mle_fixed_parameters(ctx):
+    n = 400
+    x, y = ex.gen_locations(n, 4)
+    z = oracle.simulate(x, y, (1.0, 0.1, 0.5), si.normals(n, 4))
+    lo, hi = (0.01, 0.1, 0.5), (5.0, 0.1, 0.5)  # only theta1 free
+    th, ll, ne, _ = ctx.mle(x, y, z, lo, hi, (1.0, 0.1, 0.5), xtol_rel=1e-11)
+    assert th[1] == 0.1 and th[2] == 0.5
+    assert th[0] == pytest.approx(oracle.profile_sigma2(x, y, z, 0.1, 0.5), rel=1e-8)
+
+
+def test_mle_invalid_bounds(ctx):
+    with pytest.raises(ex.ExageoError) as ei:
+        ctx.mle([0.1, 0.2], [0.1, 0.3], [1.0, 2.0], (1, 1, 1), (0.5, 2, 2), (1, 1, 1))
+    assert ei.value.status == ex.EINVAL
