@@ -177,6 +177,17 @@ exageo_status exageo_mle(exageo_ctx* ctx, int64_t n, const double* x, const doub
                          const exageo_theta* lo, const exageo_theta* hi, const exageo_theta* start, double xtol_rel,
                          int max_evals, exageo_theta* theta_hat, double* loglik, int* nevals, double* trace);
 
+/* Kriging prediction, Eq. (5) by Alg. 3 (R19):
+ *   Sigma22 = L L^T (with the forward solve y = L^{-1} z fused into the factorization),
+ *   L^T w = y (blocked backward solve), znew = Sigma12 w with the m x n block Sigma12
+ *   generated on the fly (never stored); zero mean (mu1 = mu2 = 0).
+ * x, y, z: the n observed locations and measurements; xnew, ynew: the m prediction
+ * locations; znew: m predictions. Host arrays. Non-PD -> EXAGEO_ENOTPD.
+ * Collective on distributed contexts (each w_j is broadcast from its panel's owner). */
+exageo_status exageo_predict(exageo_ctx* ctx, const exageo_theta* theta, int64_t n, const double* x,
+                             const double* y, const double* z, int64_t m, const double* xnew, const double* ynew,
+                             double* znew);
+
 /* --- Stage-level entry points (same kernels as exageo_loglik_dev, exposed
  *     so that each step of Alg. 2 can be checked on its own). ---------- */
 

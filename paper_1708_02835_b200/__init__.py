@@ -74,6 +74,8 @@ SIGNATURES = [
     ("exageo_read_lower", ctypes.c_int, [_C, _f64p, ctypes.c_int64]),
     ("exageo_read_zrow", ctypes.c_int, [_C, _f64p]),
     ("exageo_read_entries", ctypes.c_int, [_C, ctypes.c_int64, _i64p, _i64p, _f64p]),
+    ("exageo_predict", ctypes.c_int, [_C, ctypes.POINTER(Theta), ctypes.c_int64, _f64p, _f64p, _f64p, ctypes.c_int64,
+                                      _f64p, _f64p, _f64p]),
     ("exageo_mle", ctypes.c_int, [_C, ctypes.c_int64, _f64p, _f64p, _f64p, ctypes.POINTER(Theta),
                                   ctypes.POINTER(Theta), ctypes.POINTER(Theta), ctypes.c_double, ctypes.c_int,
                                   ctypes.POINTER(Theta), _f64p, ctypes.POINTER(ctypes.c_int), _f64p]),
@@ -285,6 +287,15 @@ class Context:
                                   ctypes.byref(ll), ctypes.byref(ne), _p(trace))
         self._check(st)
         return (th.sigma2, th.beta, th.nu), ll.value, ne.value, trace[: ne.value].copy()
+
+    def predict(self, x, y, z, xnew, ynew, theta) -> np.ndarray:
+        """Kriging predictions Z1 = Sigma12 Sigma22^{-1} Z2 at (xnew, ynew) (Eq. 5, Alg. 3)."""
+        x, y, z, xnew, ynew = _f(x), _f(y), _f(z), _f(xnew), _f(ynew)
+        out = np.empty(xnew.size, np.float64)
+        t = _theta(theta)
+        self._check(self._lib.exageo_predict(self._ctx, ctypes.byref(t), z.size, _p(x), _p(y), _p(z), xnew.size,
+                                             _p(xnew), _p(ynew), _p(out)))
+        return out
 
     def simulate(self, x, y, e, theta) -> np.ndarray:
         """Alg. 1: z = L(theta) e for given normal variates e."""

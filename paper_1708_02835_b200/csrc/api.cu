@@ -762,6 +762,68 @@ exageo_status exageo_simulate(exageo_ctx* c, const exageo_theta* t, int64_t n, c
   return EXAGEO_OK;
 }
 
+exageo_status exageo_predict(exageo_ctx* c, const exageo_theta* t, int64_t n, const double* x, const double* y,
+                             const double* z, int64_t m, const double* xnew, const double* ynew, double* znew) {
+  if (!c) return fail(nullptr, EXAGEO_EINVAL, "NULL ctx");
+  if (n < 1 || m < 1 || !x || !y || !z || !xnew || !ynew || !znew)
+    return fail(c, EXAGEO_EINVAL, "n < 1, m < 1 or NULL array");
+  if (!theta_ok(t)) return fail(c, EXAGEO_EINVAL, "theta must be finite and > 0");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  const int nb = c->nb_opt > 0 ? c->nb_opt : auto_nb(n);
+  const Layout G0 = make_layout(n, nb);
+  // device scratch: x, y, z (n each), xnew, ynew, znew (m each), w (N), solve and krige partials
+  const size_t nw = (size_t)G0.N;
+  const size_t ntr = (size_t)trsv_chunks(G0.N) * nb;
+  const size_t nkr = (size_t)krige_chunks(n) * (size_t)m;
+  const size_t total = 3 * (size_t)n + 3 * (size_t)m + nw + ntr + nkr;
+  double* d = nullptr;
+  CUDA_TRY(c, cudaMalloc(&d, sizeof(double) * total));
+  struct Free {
+    double* p;
+    ~Free() { cudaFree(p); }
+  } guard{d};
+  double *dx = d, *dy = dx + n, *dz = dy + n, *dxn = dz + n, *dyn = dxn + m, *dzn = dyn + m, *w = dzn + m,
+         *ptr = w + nw, *pkr = ptr + ntr;
+  CUDA_TRY(c, cudaMemcpyAsync(dx, x, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(c, cudaMemcpyAsync(dy, y, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(c, cudaMemcpyAsync(dz, z, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(c, cudaMemcpyAsync(dxn, xnew, sizeof(double) * m, cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(c, cudaMemcpyAsync(dyn, ynew, sizeof(double) * m, cudaMemcpyHostToDevice, c->stream));
+  // Alg. 3 l.3-7: Sigma22 = L L^T with the forward solve y = L^{-1} z2 fused (z row)
+  exageo_status st = do_generate(c, t, n, dx, dy, dz);
+  if (st != EXAGEO_OK) return st;
+  st = do_factor(c);
+  if (st != EXAGEO_OK) return st;
+  int64_t piv = -1;
+  st = first_pivot(c, &piv);
+  if (st != EXAGEO_OK) return st;
+  if (piv >= 0) return fail(c, EXAGEO_ENOTPD, "covariance not positive definite at pivot " + std::to_string(piv));
+  // backward solve L^T w = y, panel by panel from the last; each w_j is made available to
+  // every rank (NCCL broadcast from the panel's owner; virtual ranks share w)
+  const Layout& G = c->G;
+  for (int j = G.T - 1; j >= 0; --j) {
+    const int o = j % c->world;
+    if (RankState* R = local_state(c, o)) {
+      const double* P = R->ws + R->L.off(j);
+      const int64_t rows = G.N - (int64_t)(j + 1) * G.nb;
+      launch_backsolve_panel(P, G.ld(j), G.nb, (int64_t)(j + 1) * G.nb, rows, w, w + (int64_t)j * G.nb, ptr,
+                             c->stream);
+      c->kernels += rows > 0 ? 2 : 1;
+    }
+    if (!c->virt && c->world > 1)
+      NCCL_TRY(c, nccl::Broadcast(w + (int64_t)j * G.nb, w + (int64_t)j * G.nb, G.nb, ncclDouble, o, c->comm,
+                                  c->stream));
+  }
+  // Alg. 3 l.8 / Eq. (5): z1 = Sigma12 w with Sigma12 generated on the fly
+  launch_krige(make_consts(*t), m, dxn, dyn, n, dx, dy, w, pkr, dzn, c->stream);
+  c->kernels += 2;
+  st = check_launch(c);
+  if (st != EXAGEO_OK) return st;
+  CUDA_TRY(c, cudaMemcpyAsync(znew, dzn, sizeof(double) * m, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return EXAGEO_OK;
+}
+
 exageo_status exageo_stage_generate_dev(exageo_ctx* c, const exageo_theta* t, int64_t n, const double* x,
                                         const double* y, const double* z) {
   if (!c) return fail(nullptr, EXAGEO_EINVAL, "NULL ctx");

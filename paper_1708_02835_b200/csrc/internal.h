@@ -112,4 +112,17 @@ void launch_read_entries(const Layout& L, const double* ws, int64_t count, const
 void launch_trmv_partial(const Layout& L, const double* ws, const double* e, double* part, cudaStream_t s);
 void launch_trmv_sum(int64_t n, int64_t N, const double* part, int nparts, double* z, cudaStream_t s);
 
+// K5^T (trsv.cu): one panel step of the backward solve L^T w = y. P = panel j (ld), rows
+// local nb .. nb + rows - 1 are global rows row_after .. row_after + rows - 1; w is indexed
+// by global row (entries below the panel already solved); writes wj = w[j nb .. j nb + nb).
+// part: trsv_chunks(rows) * nb doubles of scratch.
+int trsv_chunks(int64_t rows);
+void launch_backsolve_panel(const double* P, int64_t ld, int nb, int64_t row_after, int64_t rows,
+                            const double* w, double* wj, double* part, cudaStream_t s);
+// K8 (matern.cu): znew_i = sum_j C(||snew_i - s_j||; theta) w_j (Eq. (5), Alg. 3 l.8), the
+// covariance block Sigma12 generated on the fly and never stored. part: krige_chunks(n) * m.
+int krige_chunks(int64_t n);
+void launch_krige(const MaternConsts& mc, int64_t m, const double* xn, const double* yn, int64_t n,
+                  const double* x, const double* y, const double* w, double* part, double* znew, cudaStream_t s);
+
 }  // namespace exageo

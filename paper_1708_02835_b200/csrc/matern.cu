@@ -167,6 +167,49 @@ __global__ void __launch_bounds__(256) matern_dense_kernel(MaternConsts mc, int6
     C[i + j * ldc] = matern_eval(dist2d(x1[i], y1[i], xj, yj), mc);
 }
 
+constexpr int kKrigeChunk = 8192;
+
+// K8: part[chunk][i] = sum over observed j in the chunk of C(||snew_i - s_j||) w_j.
+__global__ void __launch_bounds__(256) krige_partial_kernel(MaternConsts mc, int64_t m, const double* __restrict__ xn,
+                                                            const double* __restrict__ yn, int64_t n,
+                                                            const double* __restrict__ x,
+                                                            const double* __restrict__ y,
+                                                            const double* __restrict__ w, double* __restrict__ part) {
+  __shared__ double red[8];
+  const int64_t i = blockIdx.x;
+  const int64_t j0 = (int64_t)blockIdx.y * kKrigeChunk;
+  const int64_t j1 = (j0 + kKrigeChunk) < n ? (j0 + kKrigeChunk) : n;
+  const double xi = xn[i], yi = yn[i];
+  double acc = 0.0;
+  for (int64_t j = j0 + threadIdx.x; j < j1; j += blockDim.x) acc += matern_eval(dist2d(xi, yi, x[j], y[j]), mc) * w[j];
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int q = 0; q < 8; ++q) s += red[q];
+    part[(int64_t)blockIdx.y * m + i] = s;
+  }
+}
+
+__global__ void krige_sum_kernel(int64_t m, const double* __restrict__ part, int nchunks, double* __restrict__ znew) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  double s = 0.0;
+  for (int c = 0; c < nchunks; ++c) s += part[(int64_t)c * m + i];
+  znew[i] = s;
+}
+
+int krige_chunks(int64_t n) { return (int)((n + kKrigeChunk - 1) / kKrigeChunk); }
+
+void launch_krige(const MaternConsts& mc, int64_t m, const double* xn, const double* yn, int64_t n, const double* x,
+                  const double* y, const double* w, double* part, double* znew, cudaStream_t s) {
+  const int nch = krige_chunks(n);  // <= 65535 chunks (n < 5.3e8)
+  dim3 grid((unsigned)m, (unsigned)nch);
+  krige_partial_kernel<<<grid, 256, 0, s>>>(mc, m, xn, yn, n, x, y, w, part);
+  krige_sum_kernel<<<(unsigned)((m + 255) / 256), 256, 0, s>>>(m, part, nch, znew);
+}
+
 void launch_gen_panels(const Layout& L, double* ws, const MaternConsts& mc, const double* x, const double* y,
                        const double* z, cudaStream_t s) {
   if (L.owned() == 0) return;

@@ -1,0 +1,109 @@
+// trsv.cu -- K5^T: blocked backward triangular solve L^T w = y over the lower panels
+// (the second half of Alg. 3's dposv, P:720-721 / P:738, R19). The forward half
+// y = L^{-1} z2 is already in the z row of every panel (fused into the factorization).
+//
+// Panel by panel from the last (j = T-1 .. 0), in two launches per panel:
+//   gemv_t:     part[s][c] = sum over rows r in chunk s of the panel's sub-diagonal rows
+//               (global rows (j+1) nb .. N-1) of L_rc w_r         (reads the panel once,
+//               coalesced down columns; HBM-bound)
+//   tile_solve: rhs_c = y_c - sum_s part[s][c];  L_jj^T w_j = rhs  (one CTA, 64-column
+//               blocks from the last: shared-memory substitution with the 64 x 64 diagonal
+//               block, then the rank-64 update of the remaining right-hand side)
+// Fixed chunking and summation order: bitwise reproducible.
+#include "internal.h"
+
+namespace exageo {
+
+namespace {
+
+constexpr int kColsPerCta = 8;  // columns of the panel per CTA in gemv_t
+constexpr int kRowChunk = 4096;
+
+__global__ void __launch_bounds__(256) gemv_t_kernel(const double* __restrict__ P, int64_t ld, int nb,
+                                                     int64_t row0, int64_t rows, const double* __restrict__ w,
+                                                     double* __restrict__ part) {
+  // P: panel (column-major, ld), local row index lr corresponds to global row (row0 + lr - nb)
+  // when lr >= nb; here rows are local rows nb .. nb + rows - 1 of the panel, w indexed by
+  // the same global row.
+  __shared__ double red[8][kColsPerCta];
+  const int c0 = blockIdx.x * kColsPerCta;
+  const int64_t r_lo = (int64_t)blockIdx.y * kRowChunk;
+  const int64_t r_hi = (r_lo + kRowChunk) < rows ? (r_lo + kRowChunk) : rows;
+  double acc[kColsPerCta];
+#pragma unroll
+  for (int q = 0; q < kColsPerCta; ++q) acc[q] = 0.0;
+  for (int64_t r = r_lo + threadIdx.x; r < r_hi; r += blockDim.x) {
+    const double wr = w[row0 + r];
+#pragma unroll
+    for (int q = 0; q < kColsPerCta; ++q) acc[q] += P[(int64_t)(c0 + q) * ld + nb + r] * wr;
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int q = 0; q < kColsPerCta; ++q) {
+    double v = acc[q];
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if (lane == 0) red[warp][q] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < kColsPerCta) {
+    double v = 0.0;
+    for (int wq = 0; wq < 8; ++wq) v += red[wq][threadIdx.x];
+    part[(int64_t)blockIdx.y * nb + c0 + threadIdx.x] = v;
+  }
+}
+
+// One CTA of nb threads (nb <= 1024): thread c owns column c of the diagonal tile.
+__global__ void tile_solve_kernel(const double* __restrict__ P, int64_t ld, int nb, int64_t zrow,
+                                  const double* __restrict__ part, int nparts, double* __restrict__ wj) {
+  extern __shared__ double sh[];
+  double* rhs = sh;            // nb
+  double* blk = sh + nb;       // 64 x 65 diagonal block (column-major)
+  const int c = threadIdx.x;
+  double v = P[(int64_t)c * ld + zrow];  // y_c (z row of the panel)
+  for (int s = 0; s < nparts; ++s) v -= part[(int64_t)s * nb + c];
+  rhs[c] = v;
+  __syncthreads();
+  for (int b = nb / 64 - 1; b >= 0; --b) {
+    const int b0 = b * 64;
+    // load the 64 x 64 diagonal block L[b0.., b0..]
+    for (int idx = c; idx < 64 * 64; idx += blockDim.x) {
+      const int r = idx % 64, cc = idx / 64;
+      blk[cc * 65 + r] = P[(int64_t)(b0 + cc) * ld + b0 + r];
+    }
+    __syncthreads();
+    // backward substitution: w_k = (rhs_k - sum_{r > k} L_rk w_r) / L_kk, right-looking
+    for (int k = 63; k >= 0; --k) {
+      if (c == 0) rhs[b0 + k] /= blk[k * 65 + k];
+      __syncthreads();
+      const double wk = rhs[b0 + k];
+      if (c < k) rhs[b0 + c] -= blk[c * 65 + k] * wk;  // L_{k, c} = row k of column c
+      __syncthreads();
+    }
+    // rhs_c -= sum_{r in block b} L_rc w_r for the columns c < b0 (rows of block b, column c)
+    if (c < b0) {
+      double acc = 0.0;
+      const double* col = P + (int64_t)c * ld + b0;
+      for (int r = 0; r < 64; ++r) acc += col[r] * rhs[b0 + r];
+      rhs[c] -= acc;
+    }
+    __syncthreads();
+  }
+  wj[c] = rhs[c];
+}
+
+}  // namespace
+
+int trsv_chunks(int64_t rows) { return rows > 0 ? (int)((rows + kRowChunk - 1) / kRowChunk) : 0; }
+
+void launch_backsolve_panel(const double* P, int64_t ld, int nb, int64_t row_after, int64_t rows,
+                            const double* w, double* wj, double* part, cudaStream_t s) {
+  const int nparts = trsv_chunks(rows);
+  if (nparts > 0) {
+    dim3 grid(nb / kColsPerCta, nparts);
+    gemv_t_kernel<<<grid, 256, 0, s>>>(P, ld, nb, row_after, rows, w, part);
+  }
+  const int64_t zrow = ld - ZR;  // local row of the z row
+  tile_solve_kernel<<<1, nb, (nb + 64 * 65) * sizeof(double), s>>>(P, ld, nb, zrow, part, nparts, wj);
+}
+
+}  // namespace exageo

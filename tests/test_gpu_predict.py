@@ -1,0 +1,88 @@
+"""GPU exageo_predict (NEXT-2; Eq. (5), Alg. 3): kriging through the factor, against the
+oracle's Alg. 3 (explicit dposv by substitution + dense Sigma12 product), plus the
+properties Eq. (5) fixes: interpolation at observed sites, zero prior mean far away,
+linearity in Z2; distributed schedule (virtual ranks) equal to the single GPU; a small
+BASELINE configs[4] analogue (10% hold-out, MLE on the rest, MSE vs truth)."""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+import synth_inputs as si
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_1708_02835_b200 as ex  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    c = ex.Context(device=0)
+    yield c
+    c.close()
+
+
+@pytest.mark.parametrize("n,m,theta", [(400, 38, (1.0, 0.1, 0.5)), (1000, 200, (1.0, 0.1, 1.0)),
+                                       (1600, 1, (1.5, 0.05, 1.5)), (2100, 64, (0.8, 0.2, 0.7))])
+def test_predict_matches_oracle(ctx, n, m, theta):
+    x, y = ex.gen_locations(n, 5)
+    z = oracle.simulate(x, y, (1.0, 0.1, 0.5), si.normals(n, 6))
+    rng = np.random.default_rng(n)
+    xn, yn = rng.random(m), rng.random(m)
+    got = ctx.predict(x, y, z, xn, yn, theta)
+    ref = oracle.predict(x, y, z, xn, yn, theta)
+    assert np.abs(got - ref).max() <= 1e-9 * max(1.0, np.abs(ref).max())
+
+
+def test_predict_properties(ctx):
+    n = 900
+    theta = (1.0, 0.1, 1.0)
+    x, y = ex.gen_locations(n, 7)
+    z = si.normals(n, 8)
+    idx = np.array([0, 17, 450, 899])
+    got = ctx.predict(x, y, z, x[idx], y[idx], theta)
+    np.testing.assert_allclose(got, z[idx], rtol=1e-8, atol=1e-8)  # interpolation
+    far = ctx.predict(x, y, z, [1e4, -1e4], [1e4, 3.0], theta)
+    assert np.all(far == 0.0)  # prior mean
+    xn, yn = np.array([0.31, 0.77]), np.array([0.52, 0.05])
+    a = ctx.predict(x, y, z, xn, yn, theta)
+    b = ctx.predict(x, y, 2.5 * z, xn, yn, theta)
+    np.testing.assert_allclose(b, 2.5 * a, rtol=1e-12)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_predict_virtual_ranks(ctx, world):
+    n, m = 1300, 50
+    theta = (1.0, 0.1, 0.8)
+    x, y = ex.gen_locations(n, 9)
+    z = si.normals(n, 10)
+    rng = np.random.default_rng(1)
+    xn, yn = rng.random(m), rng.random(m)
+    c1 = ex.Context(device=0, nb=128)
+    a = c1.predict(x, y, z, xn, yn, theta)
+    c1.close()
+    cv = ex.Context(device=0, nb=128, virtual_ranks=world)
+    b = cv.predict(x, y, z, xn, yn, theta)
+    cv.close()
+    assert np.array_equal(a, b)
+
+
+def test_holdout_mle_and_kriging(ctx):
+    # BASELINE configs[4] analogue at n = 1600: 10% hold-out, MLE on the rest, kriging
+    n, theta_true = 1600, (1.0, 0.1, 0.5)
+    x, y = ex.gen_locations(n, 11)
+    z = ctx.simulate(x, y, si.normals(n, 11), theta_true)
+    hold = si.holdout_mask(n, n // 10, 11)
+    lo, hi = (0.01, 0.01, 0.1), (5.0, 2.0, 2.0)
+    start = tuple(math.sqrt(a * b) for a, b in zip(lo, hi))
+    th, ll, ne, _ = ctx.mle(x[~hold], y[~hold], z[~hold], lo, hi, start, xtol_rel=1e-7)
+    pred = ctx.predict(x[~hold], y[~hold], z[~hold], x[hold], y[hold], th)
+    mse = float(np.mean((pred - z[hold]) ** 2))
+    ref = oracle.predict(x[~hold], y[~hold], z[~hold], x[hold], y[hold], th)
+    assert np.abs(pred - ref).max() <= 1e-9
+    assert mse < 0.5 * float(np.var(z))  # kriging beats the prior mean by a wide margin
