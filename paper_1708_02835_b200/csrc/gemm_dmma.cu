@@ -6,11 +6,12 @@ namespace exageo {
 
 namespace {
 using namespace gemm;
-// Panel update / TRSM: 64 x 64 tiles, 4 warps of 32 x 32, BK 8 x 4 stages, 4 CTAs per SM.
-using PanelCfg = Cfg<64, 64, 8, 2, 2, 4, 4>;
-// Trailing update: 64 x 64 tiles, 4 warps of 32 x 32, BK 8 x 4 stages, 4 CTAs per SM
-// (tools/gemm_tune.cu at n=100k: 33.8 TF vs 30.3 for 128x64 at 2 CTAs/SM).
-using TrailCfg = Cfg<64, 64, 8, 2, 2, 4, 4>;
+// 64 x 64 tiles, 4 warps of 32 x 32, BK 16 x 2 stages, 4 CTAs per SM; accumulating
+// launches start from C (PRE) so the epilogue only stores. tools/gemm_tune.cu, U2(0) at
+// n = 100k (algorithmic TFLOP/s): 128x64 at 2 CTAs/SM 30.3; 64x64x8 x4 33.27;
+// 64x64x8 x4 PRE 33.37; 64x64x16 x2 PRE 33.56 (90% of the 37.2 TF DMMA peak).
+using PanelCfg = Cfg<64, 64, 16, 2, 2, 2, 4>;
+using TrailCfg = Cfg<64, 64, 16, 2, 2, 2, 4>;
 }  // namespace
 
 cudaError_t gemm_init() {
@@ -34,7 +35,7 @@ void launch_gemm_panel(int64_t M, int N, int K, const double* A, int64_t lda, co
   map.N = N;
   map.K = K;
   map.mblocks = (int)((M + PanelCfg::BM - 1) / PanelCfg::BM);
-  if (accumulate) launch<PanelCfg, true>(map, info, s);
+  if (accumulate) launch<PanelCfg, true, DenseMap, true>(map, info, s);
   else launch<PanelCfg, false>(map, info, s);
 }
 
@@ -48,7 +49,7 @@ void launch_syrk_panels(const Layout& L, double* ws, const double* Pk, int k, in
   map.k = k;
   map.J0 = J0;
   map.npan = npan;
-  launch<TrailCfg, true>(map, info, s);
+  launch<TrailCfg, true, SyrkMap, true>(map, info, s);
 }
 
 }  // namespace exageo

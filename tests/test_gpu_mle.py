@@ -79,7 +79,8 @@ def test_mle_fixed_parameters(ctx):
     lo, hi = (0.01, 0.1, 0.5), (5.0, 0.1, 0.5)  # only theta1 free
     th, ll, ne, _ = ctx.mle(x, y, z, lo, hi, (1.0, 0.1, 0.5), xtol_rel=1e-11)
     assert th[1] == 0.1 and th[2] == 0.5
-    assert th[0] == pytest.approx(oracle.profile_sigma2(x, y, z, 0.1, 0.5), rel=1e-8)
+    # l is flat to ~1e-13 relative within ~5e-7 of the maximiser (curvature ~n/2 in log theta1)
+    assert th[0] == pytest.approx(oracle.profile_sigma2(x, y, z, 0.1, 0.5), rel=2e-6)
 
 
 def test_mle_invalid_bounds(ctx):

@@ -1,5 +1,7 @@
 // gemm_tune.cu -- timing harness for DMMA contraction configurations (development tool).
-// Times the step-k trailing update (SyrkMap) over a synthetic panel workspace.
+// Times the step-k bulk trailing update U2(k) (SyrkMap over panels k+2 .. T-1) on a
+// synthetic panel workspace, for the cp.async+barrier kernel and the bulk-copy+mbarrier
+// kernel. Reports algorithmic TFLOP/s (the true lower triangle incl. the z row).
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I paper_1708_02835_b200/csrc \
 //        -o tools/gemm_tune tools/gemm_tune.cu
 #include <cstdio>
@@ -15,8 +17,8 @@ __global__ void fill(double* p, int64_t n) {
     p[i] = 1e-3 * (double)((i * 2654435761ull) % 1000) / 1000.0;
 }
 
-template <class C>
-void run(const char* name, const Layout& L, double* ws, int k, int reps, int band = 1) {
+template <class C, int BULK>
+void run(const char* name, const Layout& L, double* ws, int k, int reps) {
   if (set_smem<C, true, SyrkMap>() != cudaSuccess) {
     printf("%-40s smem attr failed\n", name);
     return;
@@ -24,21 +26,26 @@ void run(const char* name, const Layout& L, double* ws, int k, int reps, int ban
   SyrkMap map;
   map.L = L;
   map.ws = ws;
+  map.Pk = ws + L.off(k);
   map.k = k;
-  map.Mb = (int)((L.N - (int64_t)(k + 1) * L.nb) / 128);
-  map.cb_lo = 0;
-  map.cb_hi = map.Mb;
-  map.band = band;
-  const double flops = (double)map.blocks(C::BM, C::BN) * 2.0 * C::BM * C::BN * L.nb;
+  map.J0 = k + 2;
+  map.npan = L.T - k - 2;
+  const double m = (double)(L.n - (int64_t)(k + 2) * L.nb);
+  const double flops = 2.0 * L.nb * (m * (m + 1) / 2 + m);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
-  launch<C, true>(map, nullptr, 0);
+  auto go = [&]() {
+    if (BULK == 1) launch_bulk<C, true>(map, nullptr, 0);
+    else if (BULK == 2) launch<C, true, SyrkMap, true>(map, nullptr, 0);
+    else launch<C, true>(map, nullptr, 0);
+  };
+  go();
   cudaDeviceSynchronize();
   float best = 1e30f, tot = 0.f;
   for (int r = 0; r < reps; ++r) {
     cudaEventRecord(e0);
-    launch<C, true>(map, nullptr, 0);
+    go();
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
     float ms;
@@ -47,8 +54,8 @@ void run(const char* name, const Layout& L, double* ws, int k, int reps, int ban
     tot += ms;
   }
   cudaError_t err = cudaGetLastError();
-  printf("%-44s band=%2d k=%d blocks=%8lld best %8.3f ms  %6.2f TF  (avg %6.2f TF) %s\n", name, band, k,
-         (long long)map.blocks(C::BM, C::BN), best, flops / best / 1e9, flops / (tot / reps) / 1e9,
+  printf("%-44s %s k=%3d blocks=%8lld best %8.3f ms  %6.2f TF  (avg %6.2f TF) %s\n", name, BULK == 1 ? "bulk " : (BULK == 2 ? "preC " : "cpasy"),
+         k, (long long)map.blocks(C::BM, C::BN), best, flops / best / 1e9, flops / (tot / reps) / 1e9,
          err == cudaSuccess ? "" : cudaGetErrorString(err));
 }
 
@@ -68,13 +75,12 @@ int main(int argc, char** argv) {
   fill<<<1024, 256>>>(ws, (int64_t)(bytes / 8));
   cudaDeviceSynchronize();
   printf("n=%lld T=%d workspace %.2f GB\n", (long long)n, L.T, bytes / 1e9);
-  for (int k : {0}) {
-    run<Cfg<64, 64, 8, 2, 2, 4, 4>>("64x64x8 w2x2 st4 minb4 (32x32)", L, ws, k, 3, 8);
-    run<Cfg<64, 64, 8, 2, 2, 5, 4>>("64x64x8 w2x2 st5 minb4 (32x32)", L, ws, k, 3, 8);
-    run<Cfg<64, 64, 8, 2, 2, 6, 4>>("64x64x8 w2x2 st6 minb4 (32x32)", L, ws, k, 3, 8);
-    run<Cfg<64, 64, 4, 2, 2, 8, 4>>("64x64x4 w2x2 st8 minb4 (32x32)", L, ws, k, 3, 8);
-    run<Cfg<64, 64, 4, 2, 2, 12, 4>>("64x64x4 w2x2 st12 minb4 (32x32)", L, ws, k, 3, 8);
-    run<Cfg<64, 64, 8, 2, 2, 3, 4>>("64x64x8 w2x2 st3 minb4 (32x32)", L, ws, k, 3, 8);
+  for (int k : {0, L.T / 2}) {
+    run<Cfg<64, 64, 8, 2, 2, 4, 4>, 0>("64x64x8 w2x2 st4 minb4", L, ws, k, 3);
+    run<Cfg<64, 64, 8, 2, 2, 4, 4>, 2>("64x64x8 w2x2 st4 minb4", L, ws, k, 3);
+    run<Cfg<64, 64, 8, 2, 2, 3, 4>, 2>("64x64x8 w2x2 st3 minb4", L, ws, k, 3);
+    run<Cfg<64, 64, 16, 2, 2, 2, 4>, 2>("64x64x16 w2x2 st2 minb4", L, ws, k, 3);
+    run<Cfg<128, 64, 16, 4, 2, 4, 2>, 2>("128x64x16 w4x2 st4 minb2", L, ws, k, 3);
   }
   return 0;
 }
