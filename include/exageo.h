@@ -67,6 +67,12 @@ typedef struct {
   int virtual_ranks;    /* > 1: run that many ranks inside this process on one device,
                            panel broadcasts as device copies (tests the distributed
                            schedule on one GPU); excludes world > 1                      */
+  int ind_tiles;        /* > 0: Independent Blocks (IND) approximation: tiles
+                           outside the diagonal super tiles of ind_tiles x ind_tiles tiles
+                           are annihilated (Sigma becomes block diagonal over consecutive
+                           groups of ind_tiles * nb locations) and the factorization skips
+                           them; loglik, mle and predict (Sigma22 only) use the masked
+                           matrix. 0: exact.                                             */
 } exageo_opts;
 
 /* Per-evaluation details of exageo_loglik*. */

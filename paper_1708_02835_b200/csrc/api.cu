@@ -16,6 +16,7 @@
 // stores its panels, receives panel k before its step-k update. Lookahead depth 1 on
 // two prioritised streams per rank: the owner of panel k+1 updates it first (U1) and
 // factors it (F(k+1)) while every rank applies the bulk update U2(k).
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -68,8 +69,9 @@ int auto_nb(int64_t n) {
   return 128;
 }
 
-Layout make_layout(int64_t n, int nb, int rank = 0, int world = 1) {
+Layout make_layout(int64_t n, int nb, int rank = 0, int world = 1, int ind = 0) {
   Layout L;
+  L.ind = ind;
   L.n = n;
   L.nb = nb;
   L.T = (int)((n + nb - 1) / nb);
@@ -196,10 +198,10 @@ exageo_status do_generate(exageo_ctx* c, const exageo_theta* t, int64_t n, const
   if (!theta_ok(t)) return fail(c, EXAGEO_EINVAL, "theta must be finite and > 0");
   if (n < 1 || !x || !y) return fail(c, EXAGEO_EINVAL, "n < 1 or NULL location array");
   const int nb = c->nb_opt > 0 ? c->nb_opt : auto_nb(n);
-  c->G = make_layout(n, nb);
+  c->G = make_layout(n, nb, 0, 1, c->ind);
   for (size_t i = 0; i < c->rs.size(); ++i) {
     const int rank = c->virt ? (int)i : c->rank;
-    c->rs[i].L = make_layout(n, nb, rank, c->world);
+    c->rs[i].L = make_layout(n, nb, rank, c->world, c->ind);
   }
   exageo_status st = ensure_buffers(c);
   if (st != EXAGEO_OK) return st;
@@ -246,12 +248,13 @@ const double* panel_src(const RankState& R, int k) {
 
 // algorithmic flops of updating panels J0, J0 + world, ... (npan) by one panel:
 // 2 nb per (row, column) pair of the true lower triangle, plus the z row
-double update_flops(const Layout& L, int J0, int npan) {
+double update_flops(const Layout& L, int k, int J0, int npan) {
   double f = 0.0;
+  const int64_t rend = std::min<int64_t>((int64_t)L.sb_end(k) * L.nb, L.n);
   for (int i = 0; i < npan; ++i) {
     const int64_t c0 = (int64_t)(J0 + i * L.world) * L.nb;
     const int64_t c1 = (c0 + L.nb) < L.n ? (c0 + L.nb) : L.n;
-    for (int64_t cc = c0; cc < c1; ++cc) f += 2.0 * L.nb * (double)(L.n - cc + 1);
+    for (int64_t cc = c0; cc < c1; ++cc) f += 2.0 * L.nb * (double)(rend - cc + 1);
   }
   return f;
 }
@@ -331,16 +334,20 @@ exageo_status do_factor(exageo_ctx* c) {
       if (owns_next) {
         CUDA_TRY(c, cudaStreamWaitEvent(R.s_la, avail, 0));
         if (k > 0) CUDA_TRY(c, cudaStreamWaitEvent(R.s_la, R.ev_U2[(k - 1) & 1], 0));
-        launch_syrk_panels(L, R.ws, Pk, k, k + 1, 1, R.info, R.s_la);  // U1(k)
+        if (k + 1 < L.sb_end(k)) {  // (IND: panel k+1 opens a new super tile: no update)
+          launch_syrk_panels(L, R.ws, Pk, k, k + 1, 1, R.info, R.s_la);  // U1(k)
+          c->kernels += 1;
+        }
         CUDA_TRY(c, cudaEventRecord(R.ev_U1[k & 1], R.s_la));
         factor_panel(c, R, k + 1, R.s_la);  // F(k+1)
         CUDA_TRY(c, cudaEventRecord(R.ev_F, R.s_la));
-        c->kernels += 1;
       } else {
         CUDA_TRY(c, cudaEventRecord(R.ev_U1[k & 1], R.s_la));  // nothing read on s_la this step
       }
+      // panels updated by panel k: up to the end of k's diagonal super tile (T when exact)
+      const int Jend = L.sb_end(k);
       const int J0 = L.first_owned_from(owns_next ? k + 2 : k + 1);
-      const int npan = J0 < L.T ? (L.T - 1 - J0) / L.world + 1 : 0;
+      const int npan = J0 < Jend ? (Jend - 1 - J0) / L.world + 1 : 0;
       if (npan > 0) {
         if ((int)R.u2b.size() <= R.n_u2) {
           cudaEvent_t b, e;
@@ -353,7 +360,7 @@ exageo_status do_factor(exageo_ctx* c) {
         launch_syrk_panels(L, R.ws, Pk, k, J0, npan, R.info, R.s_main);  // U2(k)
         CUDA_TRY(c, cudaEventRecord(R.u2e[R.n_u2], R.s_main));
         ++R.n_u2;
-        R.u2_flops += update_flops(L, J0, npan);
+        R.u2_flops += update_flops(L, k, J0, npan);
         c->kernels += 1;
       }
       CUDA_TRY(c, cudaEventRecord(R.ev_U2[k & 1], R.s_main));
@@ -561,6 +568,7 @@ exageo_status exageo_create(exageo_ctx** out, const exageo_opts* opts) {
   if (opts) o = *opts;
   if (o.nb != 0 && (o.nb < 128 || o.nb % 128 != 0))
     return fail(nullptr, EXAGEO_EINVAL, "nb must be 0 (auto) or a positive multiple of 128");
+  if (o.ind_tiles < 0) return fail(nullptr, EXAGEO_EINVAL, "ind_tiles must be >= 0");
   if (o.world < 0 || o.virtual_ranks < 0 || (o.world > 1 && o.virtual_ranks > 1) ||
       (o.world > 1 && (o.rank < 0 || o.rank >= o.world || !o.nccl_id)))
     return fail(nullptr, EXAGEO_EINVAL, "bad distribution options (world/rank/nccl_id/virtual_ranks)");
@@ -574,6 +582,7 @@ exageo_status exageo_create(exageo_ctx** out, const exageo_opts* opts) {
   exageo_ctx* c = new exageo_ctx();
   c->device = o.device;
   c->nb_opt = o.nb;
+  c->ind = o.ind_tiles > 0 ? o.ind_tiles : 0;
   c->virt = o.virtual_ranks > 1;
   c->world = c->virt ? o.virtual_ranks : (o.world > 1 ? o.world : 1);
   c->rank = (!c->virt && o.world > 1) ? o.rank : 0;

@@ -49,6 +49,7 @@ void launch_syrk_panels(const Layout& L, double* ws, const double* Pk, int k, in
   map.k = k;
   map.J0 = J0;
   map.npan = npan;
+  map.row_end = (int64_t)L.sb_end(k) * L.nb;  // N unless IND
   launch<TrailCfg, true, SyrkMap, true>(map, info, s);
 }
 

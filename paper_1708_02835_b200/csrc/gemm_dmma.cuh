@@ -93,9 +93,11 @@ struct SyrkMap {
   int k;
   int J0;            // first panel of this launch (owned)
   int npan;          // number of panels (J0, J0 + world, ...)
+  int64_t row_end;   // rows updated: [J nb, row_end) and the z block (N for the exact problem;
+                     // the end of the diagonal super tile for IND: zero tiles are skipped)
 
   __host__ __device__ int cpt() const { return L.nb / 128; }
-  __host__ __device__ int64_t Mr0() const { return (L.N - (int64_t)J0 * L.nb) / 128; }
+  __host__ __device__ int64_t Mr0() const { return (row_end - (int64_t)J0 * L.nb) / 128; }
   // 128-blocks of panel i: cpt (Mr_i + 1) - cpt (cpt - 1) / 2, Mr_i = Mr0 - i world cpt
   __host__ __device__ int64_t panel_blocks(int64_t i) const {
     const int64_t c = cpt(), Mr = Mr0() - i * L.world * c;
@@ -139,8 +141,9 @@ struct SyrkMap {
       cb = qq % w;
     }
     const int64_t Jb = (int64_t)J * L.nb;
+    const int64_t Mri = Mr0() - i * L.world * w;    // row block index of the z block
     const int64_t gc = Jb + cb * 128 + half * BN;   // global column of the tile
-    const int64_t gr = Jb + rb * 128 + rhalf * BM;  // global row of the tile (N.. = z block)
+    const int64_t gr = (rb == Mri ? L.N : Jb + rb * 128) + rhalf * BM;  // global row (N.. = z block)
     const int64_t kb = (int64_t)k * L.nb;
     const int64_t ldk = L.ld(k);
     t.A = Pk + (gr - kb);

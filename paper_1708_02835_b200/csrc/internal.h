@@ -32,6 +32,20 @@ struct Layout {
   int64_t N = 0;   // padded size T*nb
   int rank = 0;    // this rank
   int world = 1;   // number of ranks (panel j lives on rank j % world)
+  int ind = 0;     // IND approximation: diagonal super tiles of `ind` tiles; 0 = exact
+
+  // one past the last panel of the diagonal super tile holding panel k (T when exact)
+  __host__ __device__ int sb_end(int k) const {
+    if (ind <= 0) return T;
+    const int e = (k / ind + 1) * ind;
+    return e < T ? e : T;
+  }
+  // IND: is global element (r, c) (r, c < N) inside a diagonal super tile?
+  __host__ __device__ bool in_super_tile(int64_t r, int64_t c) const {
+    if (ind <= 0) return true;
+    const int64_t w = (int64_t)ind * nb;
+    return r / w == c / w;
+  }
 
   __host__ __device__ int64_t ld(int j) const { return N - (int64_t)j * nb + ZR; }
   __host__ __device__ bool owns(int j) const { return j % world == rank; }

@@ -145,6 +145,7 @@ __global__ void __launch_bounds__(256) gen_panels_kernel(Layout L, double* __res
       if (lr < R) {
         const int64_t r = (int64_t)j * L.nb + lr;  // global row
         if (r >= L.n || !cin) val = (r == c) ? 1.0 : 0.0;
+        else if (!L.in_super_tile(r, c)) val = 0.0;  // IND: annihilated off-diagonal tile
         else if (r == c) val = mc.theta1;
         else val = matern_eval(dist2d(x[r], y[r], xc, yc), mc);
       } else {

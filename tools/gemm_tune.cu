@@ -30,6 +30,7 @@ void run(const char* name, const Layout& L, double* ws, int k, int reps) {
   map.k = k;
   map.J0 = k + 2;
   map.npan = L.T - k - 2;
+  map.row_end = L.N;
   const double m = (double)(L.n - (int64_t)(k + 2) * L.nb);
   const double flops = 2.0 * L.nb * (m * (m + 1) / 2 + m);
   cudaEvent_t e0, e1;

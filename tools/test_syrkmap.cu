@@ -13,7 +13,7 @@ using namespace exageo;
 using namespace exageo::gemm;
 
 template <int BM, int BN>
-int check(int T, int nb, int world, int rank, int k, int J0, int npan) {
+int check(int T, int nb, int world, int rank, int k, int J0, int npan, int64_t row_end = 0) {
   Layout L;
   L.nb = nb;
   L.T = T;
@@ -29,6 +29,7 @@ int check(int T, int nb, int world, int rank, int k, int J0, int npan) {
   m.k = k;
   m.J0 = J0;
   m.npan = npan;
+  m.row_end = row_end > 0 ? row_end : L.N;
   const int64_t nblk = m.blocks(BM, BN);
   std::set<std::tuple<int64_t, int64_t>> seen;
   const int64_t kb = (int64_t)k * nb;
@@ -58,8 +59,8 @@ int check(int T, int nb, int world, int rank, int k, int J0, int npan) {
       printf("bad ld/K\n");
       return 1;
     }
-    // tile must intersect the lower triangle of panel J or be in the z block
-    if (gr + BM - 1 < gc || gr > L.N + ZR - BM) {
+    // tile must intersect the lower triangle of panel J below row_end, or be in the z block
+    if (gr + BM - 1 < gc || gr > L.N + ZR - BM || (gr >= m.row_end && gr < L.N)) {
       printf("out of range gr=%lld gc=%lld\n", (long long)gr, (long long)gc);
       return 1;
     }
@@ -72,12 +73,13 @@ int check(int T, int nb, int world, int rank, int k, int J0, int npan) {
   int64_t expect = 0;  // sub-tiles of the lower 128-blocks that reach the lower triangle
   for (int i = 0; i < npan; ++i) {
     const int J = J0 + i * world;
-    const int64_t Mr = (L.N - (int64_t)J * nb) / 128;
+    const int64_t Mr = (m.row_end - (int64_t)J * nb) / 128;
     for (int cb = 0; cb < nb / 128; ++cb)
       for (int64_t rb = cb; rb <= Mr; ++rb)
         for (int rh = 0; rh < 128 / BM; ++rh)
           for (int ch = 0; ch < 128 / BN; ++ch) {
-            const int64_t gr = (int64_t)J * nb + rb * 128 + rh * BM, gc = (int64_t)J * nb + cb * 128 + ch * BN;
+            const int64_t gr = (rb == Mr ? L.N : (int64_t)J * nb + rb * 128) + rh * BM,
+                          gc = (int64_t)J * nb + cb * 128 + ch * BN;
             if (gr + BM > gc) ++expect;
           }
   }
@@ -152,6 +154,21 @@ int main() {
           }
       }
   bad += check<64, 64>(196, 512, 1, 0, 0, 2, 194);
+  // IND: super tiles of 3 panels -> rows limited to the super tile of k
+  for (int world : {1, 2, 4})
+    for (int rank = 0; rank < world; ++rank)
+      for (int k = 0; k + 1 < 20; ++k) {
+        Layout L;
+        L.T = 20;
+        L.rank = rank;
+        L.world = world;
+        L.ind = 3;
+        const int e = L.sb_end(k);
+        const int J0 = L.first_owned_from(L.owns(k + 1) ? k + 2 : k + 1);
+        const int npan = J0 < e ? (e - 1 - J0) / world + 1 : 0;
+        if (npan > 0) bad += check<64, 64>(20, 256, world, rank, k, J0, npan, (int64_t)e * 256);
+        ++n;
+      }
   bad += check<64, 64>(586, 512, 8, 3, 5, 11, 72);
   printf("%s: %d failures in %d enumerations\n", bad ? "FAIL" : "OK", bad, n + 2);
   return bad ? 1 : 0;
