@@ -73,6 +73,10 @@ typedef struct {
                            groups of ind_tiles * nb locations) and the factorization skips
                            them; loglik, mle and predict (Sigma22 only) use the masked
                            matrix. 0: exact.                                             */
+  int distance;         /* 0: Euclidean r = ||s - s'||. 1: great-circle distance by the
+                           haversine formula: x = longitude, y = latitude in
+                           degrees, r = 2 R asin(sqrt(hav(dlat) + cos lat1 cos lat2 hav(dlon))) */
+  double radius;        /* sphere radius R for distance = 1 (units of theta2); 0 = 6371     */
 } exageo_opts;
 
 /* Per-evaluation details of exageo_loglik*. */

@@ -81,6 +81,10 @@ def lib():
         L.oracle_predict.argtypes = [ctypes.c_int64, _f64p, _f64p, _f64p, ctypes.c_int64, _f64p, _f64p,
                                      ctypes.c_double, ctypes.c_double, ctypes.c_double, _f64p, _i64p]
         L.oracle_num_threads.restype = ctypes.c_int
+        L.oracle_set_distance.restype = None
+        L.oracle_set_distance.argtypes = [ctypes.c_int, ctypes.c_double]
+        L.oracle_distance.restype = ctypes.c_double
+        L.oracle_distance.argtypes = [ctypes.c_double] * 4
         _lib = L
     return _lib
 
@@ -206,6 +210,16 @@ def predict(x, y, z, xnew, ynew, theta) -> np.ndarray:
 
 def num_threads() -> int:
     return int(lib().oracle_num_threads())
+
+
+def set_distance(metric: str = "euclidean", radius: float = 6371.0) -> None:
+    """Distance used by every oracle routine: 'euclidean' or 'great_circle'
+    (haversine, P:1119-1130; x = longitude, y = latitude in degrees)."""
+    lib().oracle_set_distance({"euclidean": 0, "great_circle": 1}[metric], float(radius))
+
+
+def distance(x1: float, y1: float, x2: float, y2: float) -> float:
+    return float(lib().oracle_distance(x1, y1, x2, y2))
 
 
 def mle(x, y, z, lo, hi, start, xtol: float = 1e-10, max_evals: int = 4000):

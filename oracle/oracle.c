@@ -180,11 +180,35 @@ double oracle_matern(double r, double t1, double t2, double t3) {
   return (double)oracle_matern_l((long double)r, (long double)t1, (long double)t2, (long double)t3);
 }
 
-/* Euclidean distance r = sqrt(dx*dx + dy*dy) (DESIGN R15). */
+/* Distance metric of all oracle routines: 0 = Euclidean, 1 = great-circle. */
+static int orc_metric = 0;
+static double orc_radius = 6371.0;
+
+void oracle_set_distance(int metric, double radius) {
+  orc_metric = metric;
+  orc_radius = radius;
+}
+
+/* Euclidean distance r = sqrt(dx*dx + dy*dy) (DESIGN R15), or the great-circle
+ * distance by the haversine formula, x = longitude and y = latitude in
+ * degrees, computed in long double:
+ *   hav(d/R) = hav(phi2 - phi1) + cos(phi1) cos(phi2) hav(lambda2 - lambda1),
+ *   hav(a) = sin^2(a/2),  d = 2 R asin(sqrt(hav(d/R))). */
 static double orc_dist(double x1, double y1, double x2, double y2) {
+  if (orc_metric == 1) {
+    const long double deg = 3.14159265358979323846264338327950288L / 180.0L;
+    long double p1 = (long double)y1 * deg, p2 = (long double)y2 * deg;
+    long double l1 = (long double)x1 * deg, l2 = (long double)x2 * deg;
+    long double s1 = sinl(0.5L * (p2 - p1)), s2 = sinl(0.5L * (l2 - l1));
+    long double h = s1 * s1 + cosl(p1) * cosl(p2) * s2 * s2;
+    if (h > 1.0L) h = 1.0L;
+    return (double)(2.0L * (long double)orc_radius * asinl(sqrtl(h)));
+  }
   double dx = x1 - x2, dy = y1 - y2;
   return sqrt(dx * dx + dy * dy);
 }
+
+double oracle_distance(double x1, double y1, double x2, double y2) { return orc_dist(x1, y1, x2, y2); }
 
 /* Dense covariance block C[i + j*ldc] = C(||s1_i - s2_j||; theta), i < m, j < n
  * (Alg. 1 l.3-4, Alg. 3 l.3-6: genDistanceMatrix + genCovMatrix, P:639-642,

@@ -34,7 +34,8 @@ class Theta(ctypes.Structure):
 class Opts(ctypes.Structure):
     _fields_ = [("device", ctypes.c_int), ("nb", ctypes.c_int), ("stream", ctypes.c_void_p),
                 ("world", ctypes.c_int), ("rank", ctypes.c_int), ("nccl_id", ctypes.c_void_p),
-                ("virtual_ranks", ctypes.c_int), ("ind_tiles", ctypes.c_int)]
+                ("virtual_ranks", ctypes.c_int), ("ind_tiles", ctypes.c_int), ("distance", ctypes.c_int),
+                ("radius", ctypes.c_double)]
 
 
 class LoglikInfo(ctypes.Structure):
@@ -188,7 +189,8 @@ class Context:
     IND approximation with diagonal super tiles of ind_tiles tiles."""
 
     def __init__(self, device: int = 0, nb: int = 0, stream=None, world: int = 1, rank: int = 0,
-                 nccl_id: bytes | None = None, virtual_ranks: int = 0, ind_tiles: int = 0):
+                 nccl_id: bytes | None = None, virtual_ranks: int = 0, ind_tiles: int = 0,
+                 distance: str = "euclidean", radius: float = 6371.0):
         self._lib = load_library()
         self._ctx = ctypes.c_void_p()
         sp = None
@@ -196,7 +198,9 @@ class Context:
             sp = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
         self._id_buf = ctypes.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
         idp = ctypes.cast(self._id_buf, ctypes.c_void_p) if self._id_buf is not None else None
-        o = Opts(int(device), int(nb), sp, int(world), int(rank), idp, int(virtual_ranks), int(ind_tiles))
+        metric = {"euclidean": 0, "great_circle": 1, "gcd": 1}[distance]
+        o = Opts(int(device), int(nb), sp, int(world), int(rank), idp, int(virtual_ranks), int(ind_tiles), metric,
+                 float(radius))
         st = self._lib.exageo_create(ctypes.byref(self._ctx), ctypes.byref(o))
         if st != OK:
             raise ExageoError(st, self._lib.exageo_last_error(None).decode())

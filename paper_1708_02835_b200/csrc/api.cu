@@ -82,8 +82,10 @@ Layout make_layout(int64_t n, int nb, int rank = 0, int world = 1, int ind = 0) 
 }
 
 // Per-theta constants of Eq. (2), long double on the host.
-MaternConsts make_consts(const exageo_theta& t) {
+MaternConsts make_consts(const exageo_theta& t, const exageo_ctx* ctx) {
   MaternConsts c{};
+  c.metric = ctx->metric;
+  c.radius = ctx->radius;
   const long double nu = t.nu;
   c.theta1 = t.sigma2;
   c.inv_theta2 = 1.0 / t.beta;
@@ -205,7 +207,7 @@ exageo_status do_generate(exageo_ctx* c, const exageo_theta* t, int64_t n, const
   }
   exageo_status st = ensure_buffers(c);
   if (st != EXAGEO_OK) return st;
-  const MaternConsts mc = make_consts(*t);
+  const MaternConsts mc = make_consts(*t, c);
   for (auto& R : c->rs) {
     CUDA_TRY(c, cudaMemsetAsync(R.info, 0, sizeof(int), c->stream));
     launch_gen_panels(R.L, R.ws, mc, x, y, z, c->stream);
@@ -569,6 +571,8 @@ exageo_status exageo_create(exageo_ctx** out, const exageo_opts* opts) {
   if (o.nb != 0 && (o.nb < 128 || o.nb % 128 != 0))
     return fail(nullptr, EXAGEO_EINVAL, "nb must be 0 (auto) or a positive multiple of 128");
   if (o.ind_tiles < 0) return fail(nullptr, EXAGEO_EINVAL, "ind_tiles must be >= 0");
+  if (o.distance < 0 || o.distance > 1 || !(o.radius >= 0) || !std::isfinite(o.radius))
+    return fail(nullptr, EXAGEO_EINVAL, "distance must be 0 (Euclidean) or 1 (great-circle), radius >= 0");
   if (o.world < 0 || o.virtual_ranks < 0 || (o.world > 1 && o.virtual_ranks > 1) ||
       (o.world > 1 && (o.rank < 0 || o.rank >= o.world || !o.nccl_id)))
     return fail(nullptr, EXAGEO_EINVAL, "bad distribution options (world/rank/nccl_id/virtual_ranks)");
@@ -583,6 +587,8 @@ exageo_status exageo_create(exageo_ctx** out, const exageo_opts* opts) {
   c->device = o.device;
   c->nb_opt = o.nb;
   c->ind = o.ind_tiles > 0 ? o.ind_tiles : 0;
+  c->metric = o.distance;
+  c->radius = o.radius > 0 ? o.radius : 6371.0;
   c->virt = o.virtual_ranks > 1;
   c->world = c->virt ? o.virtual_ranks : (o.world > 1 ? o.world : 1);
   c->rank = (!c->virt && o.world > 1) ? o.rank : 0;
@@ -689,7 +695,7 @@ exageo_status exageo_matern_cov(exageo_ctx* c, const exageo_theta* t, int64_t m,
   cudaMemcpyAsync(dy1, y1, sizeof(double) * m, cudaMemcpyHostToDevice, c->stream);
   cudaMemcpyAsync(dx2, x2, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream);
   cudaMemcpyAsync(dy2, y2, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream);
-  launch_matern_dense(make_consts(*t), m, dx1, dy1, n, dx2, dy2, dC, m, c->stream);
+  launch_matern_dense(make_consts(*t, c), m, dx1, dy1, n, dx2, dy2, dC, m, c->stream);
   c->kernels += 1;
   cudaError_t e = cudaMemcpy2DAsync(C, sizeof(double) * ldc, dC, sizeof(double) * m, sizeof(double) * m, n,
                                     cudaMemcpyDeviceToHost, c->stream);
@@ -824,7 +830,7 @@ exageo_status exageo_predict(exageo_ctx* c, const exageo_theta* t, int64_t n, co
                                   c->stream));
   }
   // Alg. 3 l.8 / Eq. (5): z1 = Sigma12 w with Sigma12 generated on the fly
-  launch_krige(make_consts(*t), m, dxn, dyn, n, dx, dy, w, pkr, dzn, c->stream);
+  launch_krige(make_consts(*t, c), m, dxn, dyn, n, dx, dy, w, pkr, dzn, c->stream);
   c->kernels += 2;
   st = check_launch(c);
   if (st != EXAGEO_OK) return st;

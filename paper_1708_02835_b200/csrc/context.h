@@ -47,6 +47,8 @@ struct exageo_ctx {
   bool own_stream = false;
   int nb_opt = 0;
   int ind = 0;         // IND approximation: diagonal super tiles of `ind` tiles (0 = exact)
+  int metric = 0;      // 0 Euclidean, 1 great-circle (lon/lat degrees)
+  double radius = 6371.0;
   int world = 1;       // ranks of the distribution (NCCL processes or virtual ranks)
   int rank = 0;        // this process's rank (NCCL mode), 0 otherwise
   bool virt = false;   // virtual ranks: all `world` ranks in this process on one device

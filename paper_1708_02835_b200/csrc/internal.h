@@ -82,6 +82,8 @@ struct MaternConsts {
   double gam1, gam2;    // Temme gamma_1(mu), gamma_2(mu)
   double gampl, gammi;  // 1/Gamma(1+mu), 1/Gamma(1-mu)
   double pimu_sin;      // pi mu / sin(pi mu)  (1 at mu = 0)
+  int metric;           // 0: Euclidean r = ||s - s'||; 1: great-circle (haversine)
+  double radius;        // sphere radius for the great-circle distance (length units of theta2)
 };
 
 // Set kernel attributes (dynamic shared memory) on the current device.

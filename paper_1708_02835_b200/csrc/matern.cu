@@ -118,7 +118,18 @@ __device__ __forceinline__ double matern_eval(double r, const MaternConsts& c) {
   return c.pref * ex * knu;
 }
 
-__device__ __forceinline__ double dist2d(double x1, double y1, double x2, double y2) {
+// Distance between s1 = (x1, y1) and s2 = (x2, y2): Euclidean (R15), or the great-circle
+// distance by the haversine formula with x = longitude, y = latitude in
+// degrees: d = 2 R asin(sqrt(hav(dphi) + cos(phi1) cos(phi2) hav(dlambda))), hav(a) = sin^2(a/2).
+__device__ __forceinline__ double dist2d(double x1, double y1, double x2, double y2, const MaternConsts& c) {
+  if (c.metric == 1) {
+    constexpr double kDeg = 0.017453292519943295769;  // pi / 180
+    const double p1 = y1 * kDeg, p2 = y2 * kDeg;
+    const double sp = sin(0.5 * (p2 - p1)), sl = sin(0.5 * (x2 - x1) * kDeg);
+    double h = sp * sp + cos(p1) * cos(p2) * sl * sl;
+    h = h < 1.0 ? h : 1.0;
+    return 2.0 * c.radius * asin(sqrt(h));
+  }
   const double dx = x1 - x2, dy = y1 - y2;
   return sqrt(dx * dx + dy * dy);
 }
@@ -147,7 +158,7 @@ __global__ void __launch_bounds__(256) gen_panels_kernel(Layout L, double* __res
         if (r >= L.n || !cin) val = (r == c) ? 1.0 : 0.0;
         else if (!L.in_super_tile(r, c)) val = 0.0;  // IND: annihilated off-diagonal tile
         else if (r == c) val = mc.theta1;
-        else val = matern_eval(dist2d(x[r], y[r], xc, yc), mc);
+        else val = matern_eval(dist2d(x[r], y[r], xc, yc, mc), mc);
       } else {
         val = (lr == R && cin && z != nullptr) ? z[c] : 0.0;  // z row block
       }
@@ -165,7 +176,7 @@ __global__ void __launch_bounds__(256) matern_dense_kernel(MaternConsts mc, int6
   const int64_t j = blockIdx.y;
   const double xj = x2[j], yj = y2[j];
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
-    C[i + j * ldc] = matern_eval(dist2d(x1[i], y1[i], xj, yj), mc);
+    C[i + j * ldc] = matern_eval(dist2d(x1[i], y1[i], xj, yj, mc), mc);
 }
 
 constexpr int kKrigeChunk = 8192;
@@ -182,7 +193,7 @@ __global__ void __launch_bounds__(256) krige_partial_kernel(MaternConsts mc, int
   const int64_t j1 = (j0 + kKrigeChunk) < n ? (j0 + kKrigeChunk) : n;
   const double xi = xn[i], yi = yn[i];
   double acc = 0.0;
-  for (int64_t j = j0 + threadIdx.x; j < j1; j += blockDim.x) acc += matern_eval(dist2d(xi, yi, x[j], y[j]), mc) * w[j];
+  for (int64_t j = j0 + threadIdx.x; j < j1; j += blockDim.x) acc += matern_eval(dist2d(xi, yi, x[j], y[j], mc), mc) * w[j];
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
   __syncthreads();
