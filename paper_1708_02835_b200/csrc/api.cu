@@ -265,7 +265,7 @@ double update_flops(const Layout& L, int k, int J0, int npan) {
 // device copies between virtual ranks. Buffer j % 2 of a receiver was last read by
 // U1(j-2) / U2(j-2); those events gate the overwrite.
 exageo_status broadcast_panel(exageo_ctx* c, int j) {
-  if (c->world == 1) return EXAGEO_OK;
+  if (c->world == 1 && !c->comm) return EXAGEO_OK;
   const int o = j % c->world;
   const size_t bytes = (size_t)c->G.ld(j) * c->G.nb * sizeof(double);
   if (!c->virt) {
@@ -389,7 +389,7 @@ exageo_status first_pivot(exageo_ctx* c, int64_t* pivot) {
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));
     if (info > 0 && (int64_t)info - 1 < best) best = (int64_t)info - 1;
   }
-  if (!c->virt && c->world > 1) {
+  if (c->comm) {
     CUDA_TRY(c, cudaMemcpyAsync(c->pivbuf, &best, sizeof(int64_t), cudaMemcpyHostToDevice, c->stream));
     NCCL_TRY(c, nccl::AllReduce(c->pivbuf, c->pivbuf, 1, ncclInt64, ncclMin, c->comm, c->stream));
     CUDA_TRY(c, cudaMemcpyAsync(&best, c->pivbuf, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
@@ -406,7 +406,7 @@ exageo_status do_finish(exageo_ctx* c, double* out3, int64_t* pivot) {
     c->kernels += 2;
   }
   int nparts = (int)c->rs.size();
-  if (!c->virt && c->world > 1) {
+  if (c->comm) {
     NCCL_TRY(c, nccl::AllReduce(c->parts, c->parts, 2, ncclDouble, ncclSum, c->comm, c->stream));
     nparts = 1;
   }
@@ -617,7 +617,7 @@ exageo_status exageo_create(exageo_ctx** out, const exageo_opts* opts) {
   if ((e = cudaMalloc(&c->parts, sizeof(double) * 2 * c->world)) != cudaSuccess) return bail(e, "cudaMalloc");
   if ((e = cudaMalloc(&c->out3, sizeof(double) * 4)) != cudaSuccess) return bail(e, "cudaMalloc");
   if ((e = cudaMalloc(&c->pivbuf, sizeof(int64_t))) != cudaSuccess) return bail(e, "cudaMalloc");
-  if (!c->virt && c->world > 1) {
+  if (!c->virt && o.nccl_id) {  // world > 1, or a single-rank NCCL communicator (world 1)
     ncclUniqueId id;
     memcpy(&id, o.nccl_id, sizeof(id));
     std::string lerr;
@@ -763,7 +763,7 @@ exageo_status exageo_simulate(exageo_ctx* c, const exageo_theta* t, int64_t n, c
     slices += R.L.owned();
     c->kernels += 1;
   }
-  if (!c->virt && c->world > 1) {
+  if (c->comm) {
     launch_trmv_sum(n, G.N, R0.part, slices, c->zsum, c->stream);
     NCCL_TRY(c, nccl::AllReduce(c->zsum, dz, n, ncclDouble, ncclSum, c->comm, c->stream));
   } else {
@@ -825,7 +825,7 @@ exageo_status exageo_predict(exageo_ctx* c, const exageo_theta* t, int64_t n, co
                              c->stream);
       c->kernels += rows > 0 ? 2 : 1;
     }
-    if (!c->virt && c->world > 1)
+    if (c->comm)
       NCCL_TRY(c, nccl::Broadcast(w + (int64_t)j * G.nb, w + (int64_t)j * G.nb, G.nb, ncclDouble, o, c->comm,
                                   c->stream));
   }

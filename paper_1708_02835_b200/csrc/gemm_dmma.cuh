@@ -163,10 +163,11 @@ struct SyrkMap {
   }
 };
 
-template <int BM_, int BN_, int BK_, int WARPS_M_, int WARPS_N_, int STAGES_, int MINB_>
+template <int BM_, int BN_, int BK_, int WARPS_M_, int WARPS_N_, int STAGES_, int MINB_, bool XPF_ = false>
 struct Cfg {
   static constexpr int BM = BM_, BN = BN_, BK = BK_, WARPS_M = WARPS_M_, WARPS_N = WARPS_N_, STAGES = STAGES_,
                        MINB = MINB_;
+  static constexpr bool XPF = XPF_;  // cross-stage fragment pipelining (see gemm_nt_dmma)
   static constexpr int NT = WARPS_M * WARPS_N * 32;
   static constexpr int LDA_S = BM + 4, LDB_S = BN + 4;  // = 4 (mod 16) doubles
   static constexpr int SMEM = STAGES * BK * (LDA_S + LDB_S) * (int)sizeof(double);
@@ -241,6 +242,52 @@ __global__ void __launch_bounds__(C::NT, C::MINB) gemm_nt_dmma(Map map, const in
         }
       }
 
+  if constexpr (C::XPF) {
+    // Cross-stage fragment pipelining: the fragments of k-step g+1 are loaded before the
+    // DMMAs of step g; the barrier for stage kt+1 sits before the last k-step of stage kt,
+    // so the first LDS of a stage never waits behind a barrier.
+    constexpr int KS = BK / 4;
+    static_assert(KS % 2 == 0, "XPF needs an even number of k4 steps per stage");
+    double af[2][MI], bf[2][NI];
+    auto frag = [&](int buf, int kt, int kk) {
+      const double* a_s = sA + (kt % STAGES) * BK * LDA_S + wm * WM + fr + (kk * 4 + fk) * LDA_S;
+      const double* b_s = sB + (kt % STAGES) * BK * LDB_S + wn * WN + fr + (kk * 4 + fk) * LDB_S;
+#pragma unroll
+      for (int i = 0; i < MI; ++i) af[buf][i] = LOADC ? -a_s[i * 8] : a_s[i * 8];
+#pragma unroll
+      for (int j = 0; j < NI; ++j) bf[buf][j] = b_s[j * 8];
+    };
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    {
+      const int nk = STAGES - 1;
+      if (nk < KT) load_stage(nk % STAGES, nk);
+      cp_async_commit();
+    }
+    frag(0, 0, 0);
+    for (int kt = 0; kt < KT; ++kt) {
+#pragma unroll
+      for (int kk = 0; kk < KS; ++kk) {
+        const int cur = kk & 1;
+        if (kk == KS - 1) {
+          if (kt + 1 < KT) {
+            cp_async_wait<STAGES - 2>();
+            __syncthreads();  // every warp holds its step-(kt, last) fragments: slot kt is free
+            const int nk = kt + STAGES;
+            if (nk < KT) load_stage(nk % STAGES, nk);
+            cp_async_commit();
+            frag(cur ^ 1, kt + 1, 0);
+          }
+        } else {
+          frag(cur ^ 1, kt, kk + 1);
+        }
+#pragma unroll
+        for (int i = 0; i < MI; ++i)
+#pragma unroll
+          for (int j = 0; j < NI; ++j) dmma(acc[i][j], af[cur][i], bf[cur][j]);
+      }
+    }
+  } else
   for (int kt = 0; kt < KT; ++kt) {
     if (ACC && !LOADC && kt == KT / 2) {
       // pull this tile's C into L2 ahead of the read-modify-write epilogue (128-byte lines)

@@ -77,11 +77,11 @@ int main(int argc, char** argv) {
   cudaDeviceSynchronize();
   printf("n=%lld T=%d workspace %.2f GB\n", (long long)n, L.T, bytes / 1e9);
   for (int k : {0, L.T / 2}) {
-    run<Cfg<64, 64, 8, 2, 2, 4, 4>, 0>("64x64x8 w2x2 st4 minb4", L, ws, k, 3);
-    run<Cfg<64, 64, 8, 2, 2, 4, 4>, 2>("64x64x8 w2x2 st4 minb4", L, ws, k, 3);
-    run<Cfg<64, 64, 8, 2, 2, 3, 4>, 2>("64x64x8 w2x2 st3 minb4", L, ws, k, 3);
-    run<Cfg<64, 64, 16, 2, 2, 2, 4>, 2>("64x64x16 w2x2 st2 minb4", L, ws, k, 3);
-    run<Cfg<128, 64, 16, 4, 2, 4, 2>, 2>("128x64x16 w4x2 st4 minb2", L, ws, k, 3);
+    run<Cfg<64, 64, 16, 2, 2, 2, 4>, 2>("64x64x16 st2 preC", L, ws, k, 3);
+    run<Cfg<64, 64, 16, 2, 2, 2, 4, true>, 2>("64x64x16 st2 preC xpf", L, ws, k, 3);
+    run<Cfg<64, 64, 16, 2, 2, 3, 4, true>, 2>("64x64x16 st3 preC xpf", L, ws, k, 3);
+    run<Cfg<64, 64, 8, 2, 2, 4, 4, true>, 2>("64x64x8 st4 preC xpf", L, ws, k, 3);
+    run<Cfg<64, 64, 8, 2, 2, 3, 4, true>, 2>("64x64x8 st3 preC xpf", L, ws, k, 3);
   }
   return 0;
 }
