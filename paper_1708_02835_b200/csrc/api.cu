@@ -63,9 +63,11 @@ bool theta_ok(const exageo_theta* t) {
          t->beta > 0 && t->nu > 0;
 }
 
+// Tile size by n (tools/nb_sweep.py on B200): small n is bound by the panel critical
+// path (smaller tiles = shorter POTRF chains), large n by the trailing-update efficiency.
 int auto_nb(int64_t n) {
-  if (n >= 10000) return 512;
-  if (n >= 2000) return 256;
+  if (n >= 30000) return 512;
+  if (n >= 12000) return 256;
   return 128;
 }
 

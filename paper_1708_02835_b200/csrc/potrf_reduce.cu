@@ -24,27 +24,33 @@ namespace {
 
 constexpr int LDS_P = PB + 1;
 
-// 256 threads: thread t owns row r = t / 4 and the 16 slots c = (t % 4) + 4 s of it, in
-// registers. Slot c holds a_rc (the Schur complement, unscaled) while c > j and, from step
-// c on, w_rc of W = L^{-1} (unscaled). Step j: the owners of row j publish W's row j to
-// shared memory (column j of A was published at step j-1), one barrier, then every row
-// r > j applies, with d_j = a_jj and f = a_rj / d_j,
+// 64 TPR threads: thread t owns row r = t / TPR and the NS = 64 / TPR slots
+// c = (t % TPR) + TPR s of it, in registers. Slot c holds a_rc (the Schur complement,
+// unscaled) while c > j and, from step c on, w_rc of W = L^{-1} (unscaled). Step j: the
+// owners of row j publish W's row j to shared memory (column j of A was published at step
+// j-1), one barrier, then every row r > j applies, with d_j = a_jj and f = a_rj / d_j,
 //   c >  j: a_rc -= f a_cj        (right-looking Cholesky; L_jj = sqrt d_j, L_rj = a_rj / L_jj)
 //   c <= j: w_rc -= f w_jc        (right-looking L W = I;  W_jc = w_jc / L_jj, w_jj = 1)
 // and the owner of column j+1 publishes a_r,j+1. Scaling is deferred to the write-out.
-__global__ void __launch_bounds__(256) potrf_block_kernel(double* __restrict__ a, int64_t lda, double* __restrict__ W,
-                                                          double* __restrict__ slot, int* __restrict__ info,
-                                                          int64_t pivot_base) {
+// colA and rowW share one array (rowW at offset PB * LDS_P) so the per-slot source is an
+// index select, not a pointer select.
+template <int TPR>
+__global__ void __launch_bounds__(64 * TPR) potrf_block_kernel(double* __restrict__ a, int64_t lda,
+                                                               double* __restrict__ W, double* __restrict__ slot,
+                                                               int* __restrict__ info, int64_t pivot_base) {
+  constexpr int NS = PB / TPR;
+  constexpr int RPW = 32 / TPR;  // rows per warp
+  constexpr int WOFF = PB * LDS_P;
   if (*(volatile int*)info != 0) return;
   extern __shared__ double smem_p[];
-  double* colA = smem_p;               // colA[j * LDS_P + r] = a_rj at step j (unscaled)
-  double* rowW = smem_p + PB * LDS_P;  // rowW[j * LDS_P + c] = w_jc at step j (unscaled)
+  double* colA = smem_p;         // colA[j * LDS_P + r] = a_rj at step j (unscaled)
+  double* rowW = smem_p + WOFF;  // rowW[j * LDS_P + c] = w_jc at step j (unscaled)
   const int tid = threadIdx.x;
-  const int r = tid >> 2, q = tid & 3;
-  double v[16];
+  const int r = tid / TPR, q = tid % TPR;
+  double v[NS];
 #pragma unroll
-  for (int s = 0; s < 16; ++s) {
-    const int c = q + 4 * s;
+  for (int s = 0; s < NS; ++s) {
+    const int c = q + TPR * s;
     v[s] = (c <= r) ? a[(int64_t)c * lda + r] : 0.0;
   }
   if (q == 0) colA[r] = v[0];  // column 0
@@ -52,8 +58,8 @@ __global__ void __launch_bounds__(256) potrf_block_kernel(double* __restrict__ a
   for (int j = 0; j < PB; ++j) {
     if (r == j) {
 #pragma unroll
-      for (int s = 0; s < 16; ++s) {
-        const int c = q + 4 * s;
+      for (int s = 0; s < NS; ++s) {
+        const int c = q + TPR * s;
         rowW[j * LDS_P + c] = (c < j) ? v[s] : (c == j ? 1.0 : 0.0);
       }
     }
@@ -63,19 +69,21 @@ __global__ void __launch_bounds__(256) potrf_block_kernel(double* __restrict__ a
       bad = j;
       break;
     }
-    if (r > j) {
-      const double f = colA[j * LDS_P + r] * (1.0 / d);
+    if ((tid >> 5) * RPW + RPW - 1 > j) {  // warp-uniform: this warp holds rows > j
+      // Branch-free over the slots (the lanes of a row own different columns, so any
+      // per-slot branch would diverge): select the source row/column, predicate the update.
+      const bool row_active = r > j;
+      const double f = colA[j * LDS_P + r] * __drcp_rn(d);
 #pragma unroll
-      for (int s = 0; s < 16; ++s) {
-        const int c = q + 4 * s;
-        if (c < j) {
-          v[s] -= f * rowW[j * LDS_P + c];
-        } else if (c == j) {
-          v[s] = -f;  // w_rj = 0 - f * w_jj
-        } else if (c <= r) {
-          v[s] -= f * colA[j * LDS_P + c];
-          if (c == j + 1) colA[(j + 1) * LDS_P + r] = v[s];
-        }
+      for (int s = 0; s < NS; ++s) {
+        const int c = q + TPR * s;
+        const bool isw = c <= j;  // W part (c == j: reset a_rj to w_rj = 0 - f w_jj, w_jj = 1)
+        const double src = smem_p[j * LDS_P + c + (isw ? WOFF : 0)];
+        const double base = (c == j) ? 0.0 : v[s];
+        const double nv = base - f * src;
+        const bool act = row_active && (isw || c <= r);
+        v[s] = act ? nv : v[s];
+        if (act && c == j + 1) colA[(j + 1) * LDS_P + r] = nv;
       }
     }
   }
@@ -84,16 +92,23 @@ __global__ void __launch_bounds__(256) potrf_block_kernel(double* __restrict__ a
     return;
   }
   __syncthreads();
-  if (tid == 0) {
-    double ld = 0.0;
-    for (int i = 0; i < PB; ++i) ld += log(sqrt(colA[i * LDS_P + i]));
-    *slot = ld;
+  // L_jj = sqrt(d_j) and 1 / L_jj once per column; sum log L_jj = sum log(d_j) / 2 by a
+  // fixed two-level tree (warps 0-1, then lane 0 of warp 0)
+  __shared__ double lj[PB], ilj[PB], lred[2];
+  if (tid < PB) {
+    const double dj = colA[tid * LDS_P + tid];
+    lj[tid] = sqrt(dj);
+    ilj[tid] = 1.0 / lj[tid];
+    double lg = 0.5 * log(dj);
+    for (int o = 16; o > 0; o >>= 1) lg += __shfl_down_sync(0xffffffffu, lg, o);
+    if ((tid & 31) == 0) lred[tid >> 5] = lg;
   }
+  __syncthreads();
+  if (tid == 0) *slot = lred[0] + lred[1];
   for (int idx = tid; idx < PB * PB; idx += blockDim.x) {
     const int rr = idx % PB, c = idx / PB;
-    const double lc = sqrt(colA[c * LDS_P + c]);
-    a[(int64_t)c * lda + rr] = (rr > c) ? colA[c * LDS_P + rr] / lc : (rr == c ? lc : 0.0);
-    W[c * PB + rr] = (rr >= c) ? rowW[rr * LDS_P + c] / sqrt(colA[rr * LDS_P + rr]) : 0.0;
+    a[(int64_t)c * lda + rr] = (rr > c) ? colA[c * LDS_P + rr] * ilj[c] : (rr == c ? lj[c] : 0.0);
+    W[c * PB + rr] = (rr >= c) ? rowW[rr * LDS_P + c] * ilj[rr] : 0.0;
   }
 }
 
@@ -235,14 +250,19 @@ __global__ void trmv_sum_kernel(int64_t n, int64_t N, const double* __restrict__
 }  // namespace
 
 constexpr int kPotrfSmem = 2 * PB * LDS_P * (int)sizeof(double);
+#ifndef EXAGEO_POTRF_TPR
+#define EXAGEO_POTRF_TPR 16
+#endif
+constexpr int kPotrfTpr = EXAGEO_POTRF_TPR;  // threads per row of the 64 x 64 block
 
 cudaError_t potrf_init() {
-  return cudaFuncSetAttribute(potrf_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kPotrfSmem);
+  return cudaFuncSetAttribute(potrf_block_kernel<kPotrfTpr>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              kPotrfSmem);
 }
 
 void launch_potrf_block(double* a, int64_t lda, double* W, double* slot, int* info, int64_t pivot_base,
                         cudaStream_t s) {
-  potrf_block_kernel<<<1, 256, kPotrfSmem, s>>>(a, lda, W, slot, info, pivot_base);
+  potrf_block_kernel<kPotrfTpr><<<1, 64 * kPotrfTpr, kPotrfSmem, s>>>(a, lda, W, slot, info, pivot_base);
 }
 
 void launch_local_partials(const Layout& L, const double* ws, const double* slots, int nslots, double* scratch,

@@ -1,0 +1,78 @@
+// potrf_bench.cu -- latency of the 64x64 diagonal-block POTRF (+inverse) kernel and of the
+// panel GEMMs at a few sizes (development tool). Links potrf_reduce.cu / gemm_dmma.cu.
+#include <cstdio>
+#include <vector>
+
+#include "internal.h"
+
+using namespace exageo;
+
+__global__ void make_spd(double* a, int64_t lda, int n) {
+  for (int idx = threadIdx.x + blockIdx.x * blockDim.x; idx < n * n; idx += blockDim.x * gridDim.x) {
+    const int r = idx % n, c = idx / n;
+    a[(int64_t)c * lda + r] = (r == c) ? (double)n : 1.0 / (1.0 + r + c);
+  }
+}
+
+int main() {
+  potrf_init();
+  gemm_init();
+  const int64_t lda = 4096;
+  double *a, *W, *slot;
+  int* info;
+  cudaMalloc(&a, sizeof(double) * lda * 64);
+  cudaMalloc(&W, sizeof(double) * 64 * 64);
+  cudaMalloc(&slot, sizeof(double));
+  cudaMalloc(&info, sizeof(int));
+  cudaMemset(info, 0, sizeof(int));
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  for (int rep = 0; rep < 3; ++rep) {
+    make_spd<<<64, 256>>>(a, lda, 64);
+    cudaEventRecord(e0);
+    for (int i = 0; i < 20; ++i) {
+      make_spd<<<64, 256>>>(a, lda, 64);
+      launch_potrf_block(a, lda, W, slot, info, 0, 0);
+    }
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    printf("potrf_block+make_spd: %.2f us per call\n", 1000.f * ms / 20);
+    cudaEventRecord(e0);
+    for (int i = 0; i < 20; ++i) make_spd<<<64, 256>>>(a, lda, 64);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    cudaEventElapsedTime(&ms, e0, e1);
+    printf("make_spd alone: %.2f us per call\n", 1000.f * ms / 20);
+  }
+  int h;
+  cudaMemcpy(&h, info, sizeof(int), cudaMemcpyDeviceToHost);
+  printf("info=%d err=%s\n", h, cudaGetErrorString(cudaGetLastError()));
+  // panel GEMMs
+  for (int64_t M : {1024, 16384, 100000}) {
+    double *A, *B, *C;
+    cudaMalloc(&A, sizeof(double) * M * 512);
+    cudaMalloc(&C, sizeof(double) * M * 64);
+    cudaMalloc(&B, sizeof(double) * 64 * 512);
+    cudaMemset(A, 0, sizeof(double) * M * 512);
+    cudaMemset(B, 0, sizeof(double) * 64 * 512);
+    cudaMemset(C, 0, sizeof(double) * M * 64);
+    for (int K : {64, 256, 448}) {
+      launch_gemm_panel(M, 64, K, A, M, B, 64, C, M, true, info, 0);
+      cudaEventRecord(e0);
+      for (int i = 0; i < 10; ++i) launch_gemm_panel(M, 64, K, A, M, B, 64, C, M, true, info, 0);
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      float ms;
+      cudaEventElapsedTime(&ms, e0, e1);
+      const double us = 1000.0 * ms / 10;
+      printf("gemm_panel M=%lld K=%d: %.2f us  (%.2f TF)\n", (long long)M, K, us, 2.0 * M * 64 * K / us / 1e6);
+    }
+    cudaFree(A);
+    cudaFree(B);
+    cudaFree(C);
+  }
+  return 0;
+}
