@@ -170,6 +170,55 @@ def reduce_max(value: float, dist, device: str = "cpu") -> float:
     return float(t.item())
 
 
+# ----------------------------------------------------------------------------- side measurements
+def run_extras(ex, si, torch, device: int) -> dict:
+    """BASELINE configs[0], [1], [2] as side measurements (1 GPU, untimed by the driver):
+    n = 400 latency, the n = 1600 MLE (nu in {0.5, 1.0}) and the n = 10k-80k sweep."""
+    import math
+
+    out = {}
+    dev = f"cuda:{device}"
+    with ex.Context(device=device) as c:
+        # configs[0]: single evaluation at n = 400 (20 x 20 jittered grid)
+        x, y = ex.gen_locations(400, SEED)
+        z = c.simulate(x, y, si.normals(400, SEED), THETA)
+        X, Y, Z = (torch.from_numpy(a).to(dev) for a in (x, y, z))
+        for _ in range(20):
+            c.loglik_dev(X, Y, Z, THETA)
+        dt, walls = [], []
+        for _ in range(100):
+            t0 = time.perf_counter()
+            r = c.loglik_dev(X, Y, Z, THETA)
+            walls.append(time.perf_counter() - t0)
+            dt.append(r.info["ms_total"])
+        out["config1_n400"] = {"loglik": r.loglik, "device_us_median": 1e3 * statistics.median(dt),
+                               "wall_us_median": 1e6 * statistics.median(walls), "kernels": r.info["kernels"]}
+        # configs[1]: full MLE of (sigma2, beta, nu) at n = 1600
+        lo, hi = (0.01, 0.01, 0.1), (5.0, 2.0, 2.0)
+        start = tuple(math.sqrt(a * b) for a, b in zip(lo, hi))
+        x, y = ex.gen_locations(1600, SEED)
+        for nu in (0.5, 1.0):
+            z = c.simulate(x, y, si.normals(1600, SEED), (1.0, 0.1, nu))
+            t0 = time.perf_counter()
+            th, ll, ne, _ = c.mle(x, y, z, lo, hi, start, xtol_rel=1e-6, max_evals=2000)
+            sec = time.perf_counter() - t0
+            out[f"config2_mle_n1600_nu{nu}"] = {"theta_hat": th, "loglik": ll, "evals": ne, "seconds": sec,
+                                               "ms_per_eval": 1e3 * sec / max(ne, 1)}
+        # configs[2]: single-GPU sweep n = 10k - 80k (n = 100k is the headline line)
+        sweep = []
+        for n in (10_000, 20_000, 40_000, 60_000, 80_000):
+            x, y = ex.gen_locations(n, SEED)
+            zz = si.normals(n, SEED)
+            X, Y, Z = (torch.from_numpy(a).to(dev) for a in (x, y, zz))
+            c.loglik_dev(X, Y, Z, THETA)
+            r = c.loglik_dev(X, Y, Z, THETA)
+            i = r.info
+            sweep.append({"n": n, "nb": i["nb"], "evals_per_s": 1e3 / i["ms_total"], "ms": i["ms_total"],
+                          "cholesky_tflops": n**3 / 3 / (i["ms_chol"] * 1e-3) / 1e12})
+        out["config3_sweep"] = sweep
+    return out
+
+
 # ----------------------------------------------------------------------------- GPU arm
 def run_gpu(args):
     import numpy as np
@@ -263,6 +312,10 @@ def run_gpu(args):
         except Exception:
             traffic = None
 
+    extras = None
+    if world == 1 and not args.no_extras:
+        extras = run_extras(ex, si, torch, local)
+
     result = None
     if rank == 0:
         cpu = None
@@ -298,6 +351,7 @@ def run_gpu(args):
                     "d2h_bytes_per_step": 3 * 8 + 4, "steps": e2e_steps},
             "gpu_launches": launches,
             "clocks": clk,
+            "other_configs": extras,
         }
         print(json.dumps(result), flush=True)
     ctx.close()
@@ -316,6 +370,7 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=3000)
     ap.add_argument("--ref-sample", type=int, default=2000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip BASELINE configs 1-3 side measurements")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
