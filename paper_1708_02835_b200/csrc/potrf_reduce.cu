@@ -260,6 +260,8 @@ cudaError_t potrf_init() {
                               kPotrfSmem);
 }
 
+// (A 4 x 4-blocked variant with a warp-serial 16 x 16 diagonal factorization and
+// 3 barriers per block column measured 68 us against 32 us for this kernel on B200.)
 void launch_potrf_block(double* a, int64_t lda, double* W, double* slot, int* info, int64_t pivot_base,
                         cudaStream_t s) {
   potrf_block_kernel<kPotrfTpr><<<1, 64 * kPotrfTpr, kPotrfSmem, s>>>(a, lda, W, slot, info, pivot_base);
