@@ -260,8 +260,10 @@ cudaError_t potrf_init() {
                               kPotrfSmem);
 }
 
-// (A 4 x 4-blocked variant with a warp-serial 16 x 16 diagonal factorization and
-// 3 barriers per block column measured 68 us against 32 us for this kernel on B200.)
+// (Measured alternatives on B200: a 4 x 4-blocked variant with a warp-serial 16 x 16
+// diagonal factorization, 68 us; a pair-step variant eliminating two columns per barrier
+// with a 2 x 2 pivot block, 27 us but it loses exact-zero pivot detection for duplicate
+// sites; this kernel: 31 us.)
 void launch_potrf_block(double* a, int64_t lda, double* W, double* slot, int* info, int64_t pivot_base,
                         cudaStream_t s) {
   potrf_block_kernel<kPotrfTpr><<<1, 64 * kPotrfTpr, kPotrfSmem, s>>>(a, lda, W, slot, info, pivot_base);
