@@ -199,11 +199,12 @@ def run_extras(ex, si, torch, device: int) -> dict:
         x, y = ex.gen_locations(1600, SEED)
         for nu in (0.5, 1.0):
             z = c.simulate(x, y, si.normals(1600, SEED), (1.0, 0.1, nu))
-            t0 = time.perf_counter()
-            th, ll, ne, _ = c.mle(x, y, z, lo, hi, start, xtol_rel=1e-6, max_evals=2000)
-            sec = time.perf_counter() - t0
-            out[f"config2_mle_n1600_nu{nu}"] = {"theta_hat": th, "loglik": ll, "evals": ne, "seconds": sec,
-                                               "ms_per_eval": 1e3 * sec / max(ne, 1)}
+            for prof in (False, True):  # 3-D search / theta1 profiled out (exageo_mle_profile)
+                t0 = time.perf_counter()
+                th, ll, ne, _ = c.mle(x, y, z, lo, hi, start, xtol_rel=1e-6, max_evals=2000, profile=prof)
+                sec = time.perf_counter() - t0
+                out[f"config2_mle{'_profile' if prof else ''}_n1600_nu{nu}"] = {
+                    "theta_hat": th, "loglik": ll, "evals": ne, "seconds": sec, "ms_per_eval": 1e3 * sec / max(ne, 1)}
         # configs[2]: single-GPU sweep n = 10k - 80k (n = 100k is the headline line)
         sweep = []
         for n in (10_000, 20_000, 40_000, 60_000, 80_000):

@@ -187,6 +187,17 @@ exageo_status exageo_mle(exageo_ctx* ctx, int64_t n, const double* x, const doub
                          const exageo_theta* lo, const exageo_theta* hi, const exageo_theta* start, double xtol_rel,
                          int max_evals, exageo_theta* theta_hat, double* loglik, int* nevals, double* trace);
 
+/* Same contract as exageo_mle, but the search runs over (theta2, theta3) only: theta1
+ * is profiled out in closed form. Eq. (2) is linear in theta1, Sigma = theta1 R, so one
+ * factorization of R (theta1 = 1) gives log|R| and q = z^T R^-1 z, and
+ *   l(s, theta2, theta3) = -q / (2 s) - (n log s + log|R|) / 2 - (n / 2) log 2 pi
+ * is maximised over s in [lo.sigma2, hi.sigma2] by s = clamp(q / n). Same maximiser as
+ * exageo_mle with one dimension fewer (fewer evaluations); the trace records s. */
+exageo_status exageo_mle_profile(exageo_ctx* ctx, int64_t n, const double* x, const double* y, const double* z,
+                                 const exageo_theta* lo, const exageo_theta* hi, const exageo_theta* start,
+                                 double xtol_rel, int max_evals, exageo_theta* theta_hat, double* loglik,
+                                 int* nevals, double* trace);
+
 /* Kriging prediction, Eq. (5) by Alg. 3 (R19):
  *   Sigma22 = L L^T (with the forward solve y = L^{-1} z fused into the factorization),
  *   L^T w = y (blocked backward solve), znew = Sigma12 w with the m x n block Sigma12

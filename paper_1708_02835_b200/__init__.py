@@ -80,6 +80,9 @@ SIGNATURES = [
     ("exageo_mle", ctypes.c_int, [_C, ctypes.c_int64, _f64p, _f64p, _f64p, ctypes.POINTER(Theta),
                                   ctypes.POINTER(Theta), ctypes.POINTER(Theta), ctypes.c_double, ctypes.c_int,
                                   ctypes.POINTER(Theta), _f64p, ctypes.POINTER(ctypes.c_int), _f64p]),
+    ("exageo_mle_profile", ctypes.c_int, [_C, ctypes.c_int64, _f64p, _f64p, _f64p, ctypes.POINTER(Theta),
+                                          ctypes.POINTER(Theta), ctypes.POINTER(Theta), ctypes.c_double, ctypes.c_int,
+                                          ctypes.POINTER(Theta), _f64p, ctypes.POINTER(ctypes.c_int), _f64p]),
 ]
 
 _lib = None
@@ -277,8 +280,9 @@ class Context:
         self._check(st, info.npd_pivot)
         return Result(info.loglik, info.logdet, info.quad, info.as_dict())
 
-    def mle(self, x, y, z, lo, hi, start, xtol_rel: float = 1e-9, max_evals: int = 1000):
-        """Maximum-likelihood estimate over the box lo <= theta <= hi (exageo_mle).
+    def mle(self, x, y, z, lo, hi, start, xtol_rel: float = 1e-9, max_evals: int = 1000, profile: bool = False):
+        """Maximum-likelihood estimate over the box lo <= theta <= hi (exageo_mle, or
+        exageo_mle_profile with theta1 profiled out when profile=True).
 
         Returns (theta_hat tuple, loglik, nevals, trace as an (nevals, 4) array)."""
         x, y, z = _f(x), _f(y), _f(z)
@@ -287,9 +291,9 @@ class Context:
         ll = ctypes.c_double()
         ne = ctypes.c_int()
         trace = np.zeros((max_evals, 4), np.float64)
-        st = self._lib.exageo_mle(self._ctx, z.size, _p(x), _p(y), _p(z), ctypes.byref(tlo), ctypes.byref(thi),
-                                  ctypes.byref(ts), float(xtol_rel), int(max_evals), ctypes.byref(th),
-                                  ctypes.byref(ll), ctypes.byref(ne), _p(trace))
+        fn = self._lib.exageo_mle_profile if profile else self._lib.exageo_mle
+        st = fn(self._ctx, z.size, _p(x), _p(y), _p(z), ctypes.byref(tlo), ctypes.byref(thi), ctypes.byref(ts),
+                float(xtol_rel), int(max_evals), ctypes.byref(th), ctypes.byref(ll), ctypes.byref(ne), _p(trace))
         self._check(st)
         return (th.sigma2, th.beta, th.nu), ll.value, ne.value, trace[: ne.value].copy()
 

@@ -488,8 +488,13 @@ exageo_status loglik_device(exageo_ctx* c, const exageo_theta* t, int64_t n, con
 
 namespace exageo {
 exageo_status eval_loglik(exageo_ctx* c, const exageo_theta* t, int64_t n, const double* x_d, const double* y_d,
-                          const double* z_d, double* ll) {
-  return loglik_device(c, t, n, x_d, y_d, z_d, ll, nullptr);
+                          const double* z_d, double* ll, double* logdet, double* quad) {
+  if (!logdet && !quad) return loglik_device(c, t, n, x_d, y_d, z_d, ll, nullptr);
+  exageo_loglik_info info;
+  const exageo_status st = loglik_device(c, t, n, x_d, y_d, z_d, ll, &info);
+  if (logdet) *logdet = info.logdet;
+  if (quad) *quad = info.quad;
+  return st;
 }
 exageo_status staging(exageo_ctx* c, int64_t n, double** buf) {
   exageo_status st = ensure_vec(c, n);

@@ -69,10 +69,10 @@ struct exageo_ctx {
 };
 
 namespace exageo {
-// One evaluation of l(theta) on device-resident inputs (api.cu). Returns EXAGEO_OK,
-// EXAGEO_ENOTPD (ll = -inf), or another error.
+// One evaluation of l(theta) on device-resident inputs (api.cu), optionally with its parts
+// log|Sigma| and z^T Sigma^-1 z. Returns EXAGEO_OK, EXAGEO_ENOTPD (ll = -inf), or another error.
 exageo_status eval_loglik(exageo_ctx* c, const exageo_theta* t, int64_t n, const double* x_d, const double* y_d,
-                          const double* z_d, double* ll);
+                          const double* z_d, double* ll, double* logdet = nullptr, double* quad = nullptr);
 // Device staging buffer of at least 4 n doubles (api.cu).
 exageo_status staging(exageo_ctx* c, int64_t n, double** buf);
 exageo_status set_error(exageo_ctx* c, exageo_status s, const std::string& msg);

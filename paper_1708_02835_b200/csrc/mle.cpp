@@ -10,6 +10,12 @@
 // below xtol_rel; then one restart from the best vertex with a fresh simplex, kept only
 // while it improves. Deterministic: on a distributed context every rank runs the same
 // search on bitwise-identical l values (all-reduced), so no theta broadcast is needed.
+//
+// exageo_mle_profile: the same search over (theta2, theta3) only, with theta1 profiled out
+// in closed form. Sigma(theta) = theta1 R(theta2, theta3) (Eq. 2 is linear in theta1), so one
+// factorization of R gives l(s, theta2, theta3) = -q/(2s) - (n log s + log|R|)/2 - (n/2) log 2pi
+// for every s, with q = z^T R^-1 z; it is unimodal in s with maximum at s = q/n, clamped to
+// [lo1, hi1]. The maximiser over the box is the same as the full search's.
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -39,6 +45,9 @@ struct Objective {
   int fails = 0;
   double fixed[3] = {0, 0, 0};  // exact values of the fixed parameters
   bool is_free[3] = {false, false, false};
+  bool profile = false;         // theta1 profiled out (exageo_mle_profile)
+  double s_lo = 0, s_hi = 0;    // theta1 bounds (profile)
+  exageo_theta best_theta{0, 0, 0};
 
   exageo_theta to_theta(const double u[3]) const {
     double v[3];
@@ -58,7 +67,20 @@ struct Objective {
     if (evals >= max_evals || err != EXAGEO_OK) return kInf;
     exageo_theta t = to_theta(u);
     double ll = -kInf;
-    const exageo_status st = eval_loglik(ctx, &t, n, x, y, z, &ll);
+    exageo_status st;
+    if (profile) {
+      t.sigma2 = 1.0;
+      double logdet = 0.0, quad = 0.0;
+      st = eval_loglik(ctx, &t, n, x, y, z, &ll, &logdet, &quad);
+      if (st == EXAGEO_OK) {
+        const double nn = (double)n;
+        t.sigma2 = std::min(std::max(quad / nn, s_lo), s_hi);
+        const double log2pi = 1.8378770664093454835606594728112;
+        ll = -0.5 * quad / t.sigma2 - 0.5 * (nn * std::log(t.sigma2) + logdet) - 0.5 * nn * log2pi;
+      }
+    } else {
+      st = eval_loglik(ctx, &t, n, x, y, z, &ll);
+    }
     if (st != EXAGEO_OK && st != EXAGEO_ENOTPD) {
       err = st;
       return kInf;
@@ -79,6 +101,7 @@ struct Objective {
     if (f < best_f) {
       best_f = f;
       memcpy(best_u, u, sizeof(u));
+      best_theta = t;
     }
     return f;
   }
@@ -179,10 +202,12 @@ void nelder_mead(Objective& f, std::vector<double> v0, const std::vector<double>
 
 using namespace exageo;
 
-extern "C" exageo_status exageo_mle(exageo_ctx* c, int64_t n, const double* x, const double* y, const double* z,
-                                    const exageo_theta* lo, const exageo_theta* hi, const exageo_theta* start,
-                                    double xtol_rel, int max_evals, exageo_theta* theta_hat, double* loglik,
-                                    int* nevals, double* trace) {
+namespace {
+
+exageo_status run_mle(exageo_ctx* c, int64_t n, const double* x, const double* y, const double* z,
+                      const exageo_theta* lo, const exageo_theta* hi, const exageo_theta* start, double xtol_rel,
+                      int max_evals, exageo_theta* theta_hat, double* loglik, int* nevals, double* trace,
+                      bool profile) {
   if (!c) return EXAGEO_EINVAL;
   if (n < 1 || !x || !y || !z || !lo || !hi || !start || !theta_hat || max_evals < 1 || !(xtol_rel > 0))
     return set_error(c, EXAGEO_EINVAL, "bad arguments to exageo_mle");
@@ -210,14 +235,17 @@ extern "C" exageo_status exageo_mle(exageo_ctx* c, int64_t n, const double* x, c
   f.z = dz;
   f.max_evals = max_evals;
   f.trace = trace;
+  f.profile = profile;
+  f.s_lo = l3[0];
+  f.s_hi = h3[0];
   std::vector<double> v0, h;
   for (int p = 0; p < 3; ++p) {
     f.lo[p] = std::log(l3[p]);
     f.hi[p] = std::log(h3[p]);
     f.base[p] = std::log(s3[p]);
     f.fixed[p] = s3[p];
-    f.is_free[p] = h3[p] > l3[p];
-    if (h3[p] > l3[p]) {
+    f.is_free[p] = h3[p] > l3[p] && !(profile && p == 0);
+    if (f.is_free[p]) {
       f.free_.push_back(p);
       v0.push_back(f.base[p]);
       h.push_back(0.1 * (f.hi[p] - f.lo[p]));
@@ -244,7 +272,23 @@ extern "C" exageo_status exageo_mle(exageo_ctx* c, int64_t n, const double* x, c
   if (f.err != EXAGEO_OK) return f.err;
   if (nevals) *nevals = f.evals;
   if (!std::isfinite(f.best_f)) return set_error(c, EXAGEO_EFIT, "every likelihood evaluation failed");
-  *theta_hat = f.to_theta(f.best_u);
+  *theta_hat = f.best_theta;
   if (loglik) *loglik = -f.best_f;
   return EXAGEO_OK;
+}
+
+}  // namespace
+
+extern "C" exageo_status exageo_mle(exageo_ctx* c, int64_t n, const double* x, const double* y, const double* z,
+                                    const exageo_theta* lo, const exageo_theta* hi, const exageo_theta* start,
+                                    double xtol_rel, int max_evals, exageo_theta* theta_hat, double* loglik,
+                                    int* nevals, double* trace) {
+  return run_mle(c, n, x, y, z, lo, hi, start, xtol_rel, max_evals, theta_hat, loglik, nevals, trace, false);
+}
+
+extern "C" exageo_status exageo_mle_profile(exageo_ctx* c, int64_t n, const double* x, const double* y,
+                                            const double* z, const exageo_theta* lo, const exageo_theta* hi,
+                                            const exageo_theta* start, double xtol_rel, int max_evals,
+                                            exageo_theta* theta_hat, double* loglik, int* nevals, double* trace) {
+  return run_mle(c, n, x, y, z, lo, hi, start, xtol_rel, max_evals, theta_hat, loglik, nevals, trace, true);
 }

@@ -87,3 +87,48 @@ def test_mle_invalid_bounds(ctx):
     with pytest.raises(ex.ExageoError) as ei:
         ctx.mle([0.1, 0.2], [0.1, 0.3], [1.0, 2.0], (1, 1, 1), (0.5, 2, 2), (1, 1, 1))
     assert ei.value.status == ex.EINVAL
+
+
+def test_mle_profile_matches_oracle_estimate(ctx):
+    # exageo_mle_profile: theta1 in closed form, search over (theta2, theta3); same maximiser
+    g = json.load(open(GOLDEN))
+    n = g["n"]
+    x, y = ex.gen_locations(n, g["seed"])
+    z = oracle.simulate(x, y, tuple(g["theta_true"]), si.normals(n, g["seed"]))
+    th, ll, ne, trace = ctx.mle(x, y, z, tuple(g["lo"]), tuple(g["hi"]), tuple(g["start"]), xtol_rel=1e-10,
+                                max_evals=3000, profile=True)
+    for a, b in zip(th, g["theta_hat"]):
+        assert a == pytest.approx(b, rel=1e-4), (th, g["theta_hat"])
+    assert ll == pytest.approx(g["loglik"], rel=1e-10)
+    # the closed-form l(s, theta2, theta3) equals a direct evaluation at theta_hat
+    assert ll == pytest.approx(ctx.loglik(x, y, z, th).loglik, rel=1e-12)
+    assert np.max(trace[:, 3]) == ll
+    # theta1 of every trace row is the profile maximiser q/n of its (theta2, theta3) (oracle)
+    for row in trace[:: max(1, len(trace) // 5)]:
+        assert row[0] == pytest.approx(oracle.profile_sigma2(x, y, z, row[1], row[2]), rel=1e-10)
+
+
+@pytest.mark.parametrize("nu_true", [0.5, 1.0])
+def test_mle_profile_config2_fewer_evals(ctx, nu_true):
+    n = 1600
+    x, y = ex.gen_locations(n, 2)
+    z = ctx.simulate(x, y, si.normals(n, 2), (1.0, 0.1, nu_true))
+    start = tuple(math.sqrt(a * b) for a, b in zip(LO, HI))
+    th3, ll3, ne3, _ = ctx.mle(x, y, z, LO, HI, start, xtol_rel=1e-9, max_evals=3000)
+    th2, ll2, ne2, _ = ctx.mle(x, y, z, LO, HI, start, xtol_rel=1e-9, max_evals=3000, profile=True)
+    assert ll2 >= ll3 - 1e-9 * abs(ll3)
+    for a, b in zip(th2, th3):
+        assert a == pytest.approx(b, rel=1e-4)
+    assert ne2 < ne3
+
+
+def test_mle_profile_sigma2_bound_active(ctx):
+    n = 400
+    x, y = ex.gen_locations(n, 4)
+    z = oracle.simulate(x, y, (1.0, 0.1, 0.5), si.normals(n, 4))
+    lo, hi = (0.01, 0.01, 0.1), (0.3, 2.0, 2.0)  # q/n ~ 1 lies above hi.sigma2
+    th, ll, _, _ = ctx.mle(x, y, z, lo, hi, (0.1, 0.1, 0.5), xtol_rel=1e-9, profile=True)
+    assert th[0] == 0.3
+    assert ll == pytest.approx(ctx.loglik(x, y, z, th).loglik, rel=1e-12)
+    thf, llf, _, _ = ctx.mle(x, y, z, lo, hi, (0.1, 0.1, 0.5), xtol_rel=1e-9)
+    assert ll >= llf - 1e-9 * abs(llf)

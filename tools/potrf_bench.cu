@@ -1,5 +1,6 @@
 // potrf_bench.cu -- latency of the 64x64 diagonal-block POTRF (+inverse) kernel and of the
 // panel GEMMs at a few sizes (development tool). Links potrf_reduce.cu / gemm_dmma.cu.
+#include <cmath>
 #include <cstdio>
 #include <vector>
 
@@ -50,6 +51,32 @@ int main() {
   int h;
   cudaMemcpy(&h, info, sizeof(int), cudaMemcpyDeviceToHost);
   printf("info=%d err=%s\n", h, cudaGetErrorString(cudaGetLastError()));
+  {  // correctness: L L^T = A, W L = I, upper parts zero, slot = sum log L_jj
+    make_spd<<<64, 256>>>(a, lda, 64);
+    launch_potrf_block(a, lda, W, slot, info, 0, 0);
+    std::vector<double> hL(64 * 64), hW(64 * 64);
+    double hs;
+    cudaMemcpy2D(hL.data(), 64 * sizeof(double), a, lda * sizeof(double), 64 * sizeof(double), 64,
+                 cudaMemcpyDeviceToHost);
+    cudaMemcpy(hW.data(), W, sizeof(double) * 64 * 64, cudaMemcpyDeviceToHost);
+    cudaMemcpy(&hs, slot, sizeof(double), cudaMemcpyDeviceToHost);
+    double e1 = 0, e2 = 0, up = 0, ls = 0;
+    for (int i = 0; i < 64; ++i) {
+      ls += std::log(hL[i * 64 + i]);
+      for (int j = 0; j < 64; ++j) {
+        if (j > i) up = std::fmax(up, std::fabs(hL[j * 64 + i]) + std::fabs(hW[j * 64 + i]));
+        double s1 = 0, s2 = 0;
+        for (int k = 0; k < 64; ++k) {
+          s1 += hL[k * 64 + i] * hL[k * 64 + j];
+          s2 += hW[k * 64 + i] * hL[j * 64 + k];
+        }
+        const double aij = (i == j) ? 64.0 : 1.0 / (1.0 + i + j);
+        e1 = std::fmax(e1, std::fabs(s1 - aij));
+        e2 = std::fmax(e2, std::fabs(s2 - (i == j ? 1.0 : 0.0)));
+      }
+    }
+    printf("check: max|LL^T-A|=%.3e max|WL-I|=%.3e upper=%.3e slot-err=%.3e\n", e1, e2, up, hs - ls);
+  }
   // panel GEMMs
   for (int64_t M : {1024, 16384, 100000}) {
     double *A, *B, *C;

@@ -12,14 +12,15 @@ import paper_1708_02835_b200 as ex
 import synth_inputs as si
 
 ns = [int(v) for v in sys.argv[1:]] or [10000, 20000, 40000]
+THETA = tuple(float(v) for v in os.environ.get("THETA", "1.0,0.1,0.5").split(","))
 ctx = ex.Context(device=0)
 for n in ns:
     x, y = ex.gen_locations(n, 1)
     z = si.normals(n, 2)
     X, Y, Z = (torch.from_numpy(a).cuda() for a in (x, y, z))
-    r = ctx.loglik_dev(X, Y, Z, (1.0, 0.1, 0.5))
+    r = ctx.loglik_dev(X, Y, Z, THETA)
     t0 = time.time()
-    r = ctx.loglik_dev(X, Y, Z, (1.0, 0.1, 0.5))
+    r = ctx.loglik_dev(X, Y, Z, THETA)
     wall = time.time() - t0
     i = r.info
     tf = i["flops"] / (i["ms_chol"] * 1e-3) / 1e12

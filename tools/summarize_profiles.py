@@ -115,8 +115,48 @@ def summarize_full(path: str, rnd: str, n: int, nb: int):
     print(open(out).read())
 
 
+AUX_METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+               "dram__throughput.avg.pct_of_peak_sustained_elapsed", "sm__issue_active.avg.pct_of_peak_sustained_elapsed",
+               "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
+               "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
+               "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
+               "sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active",
+               "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__grid_size", "launch__block_size",
+               "launch__registers_per_thread", "smsp__inst_executed.sum"]
+
+
+def summarize_aux(paths, rnd: str):
+    """Key metrics of --set full captures of the secondary kernels (generation, POTRF, ...)."""
+    out = os.path.join(PROF, f"{rnd}_aux_kernels_summary.txt")
+    with open(out, "w") as f:
+        f.write("# ncu --set full --clock-control none captures of the secondary kernels (tools/prof_aux.sh)\n")
+        for label, path in paths:
+            raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+            rows = list(csv.reader(raw.splitlines()))
+            if len(rows) < 3:
+                continue
+            hdr, units, vals = rows[0], rows[1], rows[2]
+            got = {h: (v, u) for h, u, v in zip(hdr, units, vals) if h in AUX_METRICS}
+            stalls = []
+            for h, v in zip(hdr, vals):
+                if h.startswith("smsp__pcsamp_warps_issue_stalled_") and not h.endswith("not_issued"):
+                    try:
+                        stalls.append((float(v.replace(",", "")), h.replace("smsp__pcsamp_warps_issue_stalled_", "")))
+                    except ValueError:
+                        pass
+            st = sum(x for x, _ in stalls) or 1.0
+            f.write(f"\n== {label}  ({os.path.basename(path)})\n")
+            for h in AUX_METRICS:
+                if h in got:
+                    f.write(f"  {h:72s} {got[h][0]:>16s} {got[h][1]}\n")
+            f.write("  warp stall samples: " + ", ".join(f"{name} {100 * x / st:.0f}%"
+                                                        for x, name in sorted(stalls, reverse=True)[:5]) + "\n")
+    print(open(out).read())
+
+
 def main():
     ap = argparse.ArgumentParser()
+    ap.add_argument("--aux", nargs="*", default=None, help="label::path.ncu-rep pairs for summarize_aux")
     ap.add_argument("--round", default="r01")
     ap.add_argument("--launches", default=os.path.join(ROOT, "gpurun_out", "launches_bench.csv"))
     ap.add_argument("--full", default=os.path.join(ROOT, "gpurun_out", "prof_u2_100k.ncu-rep"))
@@ -124,6 +164,9 @@ def main():
     ap.add_argument("--nb", type=int, default=512)
     a = ap.parse_args()
     os.makedirs(PROF, exist_ok=True)
+    if a.aux:
+        summarize_aux([tuple(x.split("::", 1)) for x in a.aux], a.round)
+        return
     if os.path.exists(a.launches):
         summarize_launches(a.launches, a.round)
     if os.path.exists(a.full):
