@@ -23,41 +23,51 @@ namespace {
 
 constexpr double kPi = 3.141592653589793238462643383279502884;
 
+// 1 / d: MUFU approximation + two Newton steps (within ~1 ulp, branch-free). The series
+// and continued-fraction loops below divide 3-4 times per term; the IEEE-rounded
+// division is a long branchy sequence and dominated the generator's instruction count.
+__device__ __forceinline__ double rcp_nr(double d) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
+  y = fma(y, fma(-d, y, 1.0), y);
+  return fma(y, fma(-d, y, 1.0), y);
+}
+
 // Temme series for K_mu(x), K_mu+1(x), 0 < x <= 2 (unscaled).
 __device__ __forceinline__ void bessel_k_temme(double x, const MaternConsts& c, double& kmu, double& kmu1) {
   const double mu = c.mu;
   const double x2 = 0.5 * x;
   const double d = -log(x2);          // ln(2/x)
   const double e = mu * d;            // sigma = mu ln(2/x)
-  const double sinh_e_over_e = (fabs(e) < 1e-4) ? (1.0 + e * e * (1.0 / 6.0 + e * e * (1.0 / 120.0))) : sinh(e) / e;
+  const double sinh_e_over_e = (fabs(e) < 1e-4) ? (1.0 + e * e * (1.0 / 6.0 + e * e * (1.0 / 120.0))) : sinh(e) * rcp_nr(e);
   double f = c.pimu_sin * (c.gam1 * cosh(e) + c.gam2 * sinh_e_over_e * d);  // f_0
   const double ee = exp(e);           // (2/x)^mu
-  double p = 0.5 * ee / c.gampl;      // p_0 = (x/2)^-mu Gamma(1+mu) / 2
-  double q = 0.5 / (ee * c.gammi);    // q_0 = (x/2)^mu  Gamma(1-mu) / 2
+  double p = 0.5 * ee * rcp_nr(c.gampl);  // p_0 = (x/2)^-mu Gamma(1+mu) / 2
+  double q = 0.5 * rcp_nr(ee * c.gammi);  // q_0 = (x/2)^mu  Gamma(1-mu) / 2
   double ck = 1.0;
   const double dd = x2 * x2;
   double sum = f, sum1 = p;
   const double mu2 = mu * mu;
   for (int i = 1; i < 200; ++i) {
     const double di = (double)i;
-    f = (di * f + p + q) / (di * di - mu2);
-    ck *= dd / di;
-    p /= (di - mu);
-    q /= (di + mu);
+    f = (di * f + p + q) * rcp_nr(di * di - mu2);
+    ck *= dd * rcp_nr(di);
+    p *= rcp_nr(di - mu);
+    q *= rcp_nr(di + mu);
     const double del = ck * f;
     sum += del;
     sum1 += ck * (p - di * f);
     if (fabs(del) < 1e-17 * fabs(sum)) break;
   }
   kmu = sum;
-  kmu1 = sum1 * (2.0 / x);
+  kmu1 = sum1 * (2.0 * rcp_nr(x));
 }
 
 // Steed's algorithm (CF2, Temme 1975) for e^x K_mu(x), e^x K_mu+1(x), x > 2.
 __device__ __forceinline__ void bessel_k_cf2_scaled(double x, double mu, double& kmu, double& kmu1) {
   const double a1 = 0.25 - mu * mu;
   double b = 2.0 * (1.0 + x);
-  double d = 1.0 / b;
+  double d = rcp_nr(b);
   double h = d, delh = d;
   double q1 = 0.0, q2 = 1.0;
   double q = a1, c = a1, a = -a1;
@@ -65,13 +75,13 @@ __device__ __forceinline__ void bessel_k_cf2_scaled(double x, double mu, double&
   for (int i = 1; i < 500; ++i) {
     const double di = (double)i;
     a -= 2.0 * di;
-    c = -a * c / (di + 1.0);
-    const double qn = (q1 - b * q2) / a;
+    c = -a * c * rcp_nr(di + 1.0);
+    const double qn = (q1 - b * q2) * rcp_nr(a);
     q1 = q2;
     q2 = qn;
     q += c * qn;
     b += 2.0;
-    d = 1.0 / (b + a * d);
+    d = rcp_nr(b + a * d);
     delh = (b * d - 1.0) * delh;
     h += delh;
     const double dels = q * delh;
@@ -79,8 +89,9 @@ __device__ __forceinline__ void bessel_k_cf2_scaled(double x, double mu, double&
     if (fabs(dels) < 1e-17 * fabs(s)) break;
   }
   h = a1 * h;
-  kmu = sqrt(kPi / (2.0 * x)) / s;
-  kmu1 = kmu * (mu + x + 0.5 - h) / x;
+  const double rx = rcp_nr(x);
+  kmu = sqrt(0.5 * kPi * rx) * rcp_nr(s);
+  kmu1 = kmu * (mu + x + 0.5 - h) * rx;
 }
 
 }  // namespace
@@ -104,8 +115,9 @@ __device__ __forceinline__ double matern_eval(double r, const MaternConsts& c) {
     knu = k0;
   } else {
     double a = c.mu + 1.0;
+    const double two_rx = 2.0 * rcp_nr(x);
     for (int i = 1; i < c.nl; ++i) {
-      const double kn = k0 + (2.0 * a / x) * k1;
+      const double kn = k0 + (a * two_rx) * k1;
       k0 = k1;
       k1 = kn;
       a += 1.0;
@@ -134,37 +146,65 @@ __device__ __forceinline__ double dist2d(double x1, double y1, double x2, double
   return sqrt(dx * dx + dy * dy);
 }
 
-// One CTA per (owned panel j = rank + world * blockIdx.y, column cc = blockIdx.x) -> walks the rows
-// of that column with coalesced double2 stores.
+// Entry (global row r, global column c) of the generated panel (slow path): identity
+// padding outside n, IND-annihilated tiles, the diagonal theta1 (R9), else Eq. (2).
+__device__ __noinline__ double gen_entry(const Layout& L, const MaternConsts& mc, const double* __restrict__ x,
+                                            const double* __restrict__ y, int64_t r, int64_t c, double xc,
+                                            double yc) {
+  if (r >= L.n || c >= L.n) return (r == c) ? 1.0 : 0.0;
+  if (!L.in_super_tile(r, c)) return 0.0;  // IND: annihilated off-diagonal tile
+  if (r == c) return mc.theta1;
+  return matern_eval(dist2d(x[r], y[r], xc, yc, mc), mc);
+}
+
+constexpr int kGenCols = 8;  // columns per CTA: one (x, y) row load and index test serve 8 entries
+
+// One CTA per (owned panel j = rank + world * blockIdx.y, columns kGenCols * blockIdx.x ..)
+// -> walks the rows of those columns, two rows per thread and step, coalesced double2
+// stores down each column. Rows below the diagonal tile inside n (the bulk) take the
+// check-free path.
 __global__ void __launch_bounds__(256) gen_panels_kernel(Layout L, double* __restrict__ ws, MaternConsts mc,
                                                          const double* __restrict__ x, const double* __restrict__ y,
                                                          const double* __restrict__ z) {
   const int j = L.owned_panel(blockIdx.y);
-  const int cc = blockIdx.x;
-  const int64_t c = (int64_t)j * L.nb + cc;  // global column
+  const int cc0 = blockIdx.x * kGenCols;
+  const int64_t jb = (int64_t)j * L.nb;
   const int64_t ld = L.ld(j);
-  const int64_t R = L.N - (int64_t)j * L.nb;  // square rows of this panel
-  double* col = ws + L.off(j) + (int64_t)cc * ld;
-  const bool cin = c < L.n;
-  const double xc = cin ? x[c] : 0.0, yc = cin ? y[c] : 0.0;
+  const int64_t R = L.N - jb;  // square rows of this panel
+  double* col0 = ws + L.off(j) + (int64_t)cc0 * ld;
+  __shared__ double xc[kGenCols], yc[kGenCols];
+  if (threadIdx.x < kGenCols) {
+    const int64_t c = jb + cc0 + threadIdx.x;
+    xc[threadIdx.x] = c < L.n ? x[c] : 0.0;
+    yc[threadIdx.x] = c < L.n ? y[c] : 0.0;
+  }
+  __syncthreads();
+  const bool cols_in = jb + cc0 + kGenCols <= L.n;
   for (int64_t rr = 2 * (int64_t)threadIdx.x; rr < ld; rr += 2 * blockDim.x) {
-    double v[2];
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      const int64_t lr = rr + e;
-      double val;
-      if (lr < R) {
-        const int64_t r = (int64_t)j * L.nb + lr;  // global row
-        if (r >= L.n || !cin) val = (r == c) ? 1.0 : 0.0;
-        else if (!L.in_super_tile(r, c)) val = 0.0;  // IND: annihilated off-diagonal tile
-        else if (r == c) val = mc.theta1;
-        else val = matern_eval(dist2d(x[r], y[r], xc, yc, mc), mc);
-      } else {
-        val = (lr == R && cin && z != nullptr) ? z[c] : 0.0;  // z row block
+    const int64_t r0 = jb + rr;
+    if (cols_in && rr >= L.nb && r0 + 1 < L.n && L.in_super_tile(r0, jb)) {
+      const double x0 = x[r0], y0 = y[r0], x1 = x[r0 + 1], y1 = y[r0 + 1];
+#pragma unroll 1
+      for (int k = 0; k < kGenCols; ++k) {  // rolled: one inlined copy of the evaluator
+        const double v0 = matern_eval(dist2d(x0, y0, xc[k], yc[k], mc), mc);
+        const double v1 = matern_eval(dist2d(x1, y1, xc[k], yc[k], mc), mc);
+        *reinterpret_cast<double2*>(col0 + k * ld + rr) = make_double2(v0, v1);
       }
-      v[e] = val;
+    } else {
+#pragma unroll 1
+      for (int k = 0; k < kGenCols; ++k) {
+        const int64_t c = jb + cc0 + k;
+        const double xck = c < L.n ? x[c] : 0.0, yck = c < L.n ? y[c] : 0.0;
+        double v[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int64_t lr = rr + e;
+          if (lr < R) v[e] = gen_entry(L, mc, x, y, jb + lr, c, xck, yck);
+          else v[e] = (lr == R && c < L.n && z != nullptr) ? z[c] : 0.0;  // z row block
+        }
+        *reinterpret_cast<double2*>(col0 + k * ld + rr) = make_double2(v[0], v[1]);
+      }
     }
-    *reinterpret_cast<double2*>(col + rr) = make_double2(v[0], v[1]);
   }
 }
 
@@ -225,7 +265,7 @@ void launch_krige(const MaternConsts& mc, int64_t m, const double* xn, const dou
 void launch_gen_panels(const Layout& L, double* ws, const MaternConsts& mc, const double* x, const double* y,
                        const double* z, cudaStream_t s) {
   if (L.owned() == 0) return;
-  dim3 grid(L.nb, L.owned());
+  dim3 grid(L.nb / kGenCols, L.owned());
   gen_panels_kernel<<<grid, 256, 0, s>>>(L, ws, mc, x, y, z);
 }
 
