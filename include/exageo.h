@@ -77,6 +77,10 @@ typedef struct {
                            haversine formula: x = longitude, y = latitude in
                            degrees, r = 2 R asin(sqrt(hav(dlat) + cos lat1 cos lat2 hav(dlon))) */
   double radius;        /* sphere radius R for distance = 1 (units of theta2); 0 = 6371     */
+  int graphs;           /* CUDA-graph replay of whole evaluations (capture once per problem
+                           shape and buffer set, then replay with theta patched into the
+                           generator nodes): 0 = automatic (n <= 32768, no NCCL communicator,
+                           a non-default stream), 1 = always when possible, -1 = never      */
 } exageo_opts;
 
 /* Per-evaluation details of exageo_loglik*. */

@@ -120,6 +120,12 @@ exageo_status check_launch(exageo_ctx* c) {
   return EXAGEO_OK;
 }
 
+// Record a timing event: inside a stream capture it must become an event-record node of the
+// graph (cudaEventRecordExternal); a plain record there would only mark a dependency.
+cudaError_t record_timing(exageo_ctx* c, cudaEvent_t ev, cudaStream_t s) {
+  return c->capturing ? cudaEventRecordWithFlags(ev, s, cudaEventRecordExternal) : cudaEventRecord(ev, s);
+}
+
 exageo_status ensure_vec(exageo_ctx* c, int64_t n) {
   if (c->vec_cap >= n) return EXAGEO_OK;
   cudaFree(c->vec);
@@ -197,8 +203,8 @@ exageo_status ensure_buffers(exageo_ctx* c) {
 }
 
 // ---------------------------------------------------------------------------- generation
-exageo_status do_generate(exageo_ctx* c, const exageo_theta* t, int64_t n, const double* x, const double* y,
-                          const double* z) {
+// Validate, set the layouts for n and make sure every buffer exists (no launches).
+exageo_status prepare_generate(exageo_ctx* c, const exageo_theta* t, int64_t n, const double* x, const double* y) {
   if (!theta_ok(t)) return fail(c, EXAGEO_EINVAL, "theta must be finite and > 0");
   if (n < 1 || !x || !y) return fail(c, EXAGEO_EINVAL, "n < 1 or NULL location array");
   const int nb = c->nb_opt > 0 ? c->nb_opt : auto_nb(n);
@@ -207,9 +213,11 @@ exageo_status do_generate(exageo_ctx* c, const exageo_theta* t, int64_t n, const
     const int rank = c->virt ? (int)i : c->rank;
     c->rs[i].L = make_layout(n, nb, rank, c->world, c->ind);
   }
-  exageo_status st = ensure_buffers(c);
-  if (st != EXAGEO_OK) return st;
-  const MaternConsts mc = make_consts(*t, c);
+  return ensure_buffers(c);
+}
+
+exageo_status launch_generate(exageo_ctx* c, const MaternConsts& mc, const double* x, const double* y,
+                              const double* z) {
   for (auto& R : c->rs) {
     CUDA_TRY(c, cudaMemsetAsync(R.info, 0, sizeof(int), c->stream));
     launch_gen_panels(R.L, R.ws, mc, x, y, z, c->stream);
@@ -217,6 +225,13 @@ exageo_status do_generate(exageo_ctx* c, const exageo_theta* t, int64_t n, const
   }
   c->have_matrix = true;
   return check_launch(c);
+}
+
+exageo_status do_generate(exageo_ctx* c, const exageo_theta* t, int64_t n, const double* x, const double* y,
+                          const double* z) {
+  exageo_status st = prepare_generate(c, t, n, x, y);
+  if (st != EXAGEO_OK) return st;
+  return launch_generate(c, make_consts(*t, c), x, y, z);
 }
 
 // ---------------------------------------------------------------------------- factorization
@@ -360,9 +375,9 @@ exageo_status do_factor(exageo_ctx* c) {
           R.u2b.push_back(b);
           R.u2e.push_back(e);
         }
-        CUDA_TRY(c, cudaEventRecord(R.u2b[R.n_u2], R.s_main));
+        CUDA_TRY(c, record_timing(c, R.u2b[R.n_u2], R.s_main));
         launch_syrk_panels(L, R.ws, Pk, k, J0, npan, R.info, R.s_main);  // U2(k)
-        CUDA_TRY(c, cudaEventRecord(R.u2e[R.n_u2], R.s_main));
+        CUDA_TRY(c, record_timing(c, R.u2e[R.n_u2], R.s_main));
         ++R.n_u2;
         R.u2_flops += update_flops(L, k, J0, npan);
         c->kernels += 1;
@@ -401,7 +416,8 @@ exageo_status first_pivot(exageo_ctx* c, int64_t* pivot) {
   return EXAGEO_OK;
 }
 
-exageo_status do_finish(exageo_ctx* c, double* out3, int64_t* pivot) {
+// Launch the log-det / dot reductions and the combination into c->out3 (no host sync).
+exageo_status launch_finish(exageo_ctx* c) {
   for (size_t i = 0; i < c->rs.size(); ++i) {
     RankState& R = c->rs[i];
     launch_local_partials(R.L, R.ws, R.slots, R.L.owned() * (R.L.nb / PB), R.scratch, c->parts + 2 * i, c->stream);
@@ -414,7 +430,11 @@ exageo_status do_finish(exageo_ctx* c, double* out3, int64_t* pivot) {
   }
   launch_combine(c->parts, nparts, c->G.n, c->out3, c->stream);
   c->kernels += 1;
-  exageo_status st = check_launch(c);
+  return check_launch(c);
+}
+
+exageo_status do_finish(exageo_ctx* c, double* out3, int64_t* pivot) {
+  exageo_status st = launch_finish(c);
   if (st != EXAGEO_OK) return st;
   double h[3];
   CUDA_TRY(c, cudaMemcpyAsync(h, c->out3, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
@@ -433,23 +453,168 @@ exageo_status do_finish(exageo_ctx* c, double* out3, int64_t* pivot) {
   return EXAGEO_OK;
 }
 
+// ---------------------------------------------------------------------------- CUDA graphs
+// One evaluation (K1 .. K6 and the result copies) is captured once per problem shape and
+// buffer set and replayed; only theta changes between replays, and it lives in the K1
+// nodes' MaternConsts argument, rewritten with cudaGraphExecKernelNodeSetParams. This
+// removes the per-launch host overhead and the launch gaps of the ~8 launches per panel
+// that dominate small n (the MLE loop evaluates the same shape hundreds of times).
+bool graph_eligible(const exageo_ctx* c, int64_t n) {
+  if (c->graphs < 0 || c->comm) return false;  // NCCL collectives stay outside graphs
+  if (c->stream == nullptr || c->stream == cudaStreamLegacy || c->stream == cudaStreamPerThread) return false;
+  return c->graphs > 0 || n <= 32768;
+}
+
+void destroy_graph(exageo_ctx* c) {
+  if (c->gexec) cudaGraphExecDestroy(c->gexec);
+  if (c->graph) cudaGraphDestroy(c->graph);
+  c->gexec = nullptr;
+  c->graph = nullptr;
+  c->gen_nodes.clear();
+  c->gkey.clear();
+}
+
+std::vector<const void*> graph_key(const exageo_ctx* c, const double* x, const double* y, const double* z) {
+  std::vector<const void*> k = {(const void*)(intptr_t)c->G.n, (const void*)(intptr_t)c->G.nb, x, y, z,
+                                c->parts, c->out3, c->h_res};
+  for (const auto& R : c->rs) {
+    for (const void* p : {(const void*)R.ws, (const void*)R.slots, (const void*)R.recv[0], (const void*)R.recv[1],
+                          (const void*)R.W, (const void*)R.scratch, (const void*)R.info})
+      k.push_back(p);
+  }
+  return k;
+}
+
+// The captured body: timing events are event-record nodes (record_timing).
+exageo_status graph_body(exageo_ctx* c, const MaternConsts& mc, const double* x, const double* y,
+                         const double* z) {
+  CUDA_TRY(c, record_timing(c, c->ev[0], c->stream));
+  exageo_status st = launch_generate(c, mc, x, y, z);
+  if (st != EXAGEO_OK) return st;
+  CUDA_TRY(c, record_timing(c, c->ev[1], c->stream));
+  if ((st = do_factor(c)) != EXAGEO_OK) return st;
+  CUDA_TRY(c, record_timing(c, c->ev[2], c->stream));
+  if ((st = launch_finish(c)) != EXAGEO_OK) return st;
+  double* hd = (double*)c->h_res;
+  int* hi = (int*)(hd + 4);
+  CUDA_TRY(c, cudaMemcpyAsync(hd, c->out3, 3 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  for (size_t i = 0; i < c->rs.size(); ++i)
+    CUDA_TRY(c, cudaMemcpyAsync(hi + i, c->rs[i].info, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, record_timing(c, c->ev[3], c->stream));
+  return EXAGEO_OK;
+}
+
+exageo_status run_graph(exageo_ctx* c, const exageo_theta* t, int64_t n, const double* x, const double* y,
+                        const double* z, double* r3, int64_t* pivot) {
+  exageo_status st = prepare_generate(c, t, n, x, y);
+  if (st != EXAGEO_OK) return st;
+  if (!c->h_res) CUDA_TRY(c, cudaMallocHost(&c->h_res, sizeof(double) * 4 + sizeof(int) * c->rs.size()));
+  for (auto& R : c->rs)  // timing events of every U2 launch exist before the capture
+    while ((int)R.u2b.size() < R.L.T) {
+      cudaEvent_t b, e;
+      CUDA_TRY(c, cudaEventCreate(&b));
+      CUDA_TRY(c, cudaEventCreate(&e));
+      R.u2b.push_back(b);
+      R.u2e.push_back(e);
+    }
+  const MaternConsts mc = make_consts(*t, c);
+  std::vector<const void*> key = graph_key(c, x, y, z);
+  if (!c->gexec || key != c->gkey) {
+    destroy_graph(c);
+    const int64_t k0 = c->kernels;
+    CUDA_TRY(c, cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    c->capturing = true;
+    st = graph_body(c, mc, x, y, z);
+    c->capturing = false;
+    cudaGraph_t g = nullptr;
+    const cudaError_t e = cudaStreamEndCapture(c->stream, &g);
+    if (st != EXAGEO_OK || e != cudaSuccess) {
+      if (g) cudaGraphDestroy(g);
+      cudaGetLastError();
+      return st != EXAGEO_OK ? st : fail(c, EXAGEO_ECUDA, std::string("graph capture: ") + cudaGetErrorString(e));
+    }
+    c->graph = g;
+    CUDA_TRY(c, cudaGraphInstantiateWithFlags(&c->gexec, g, cudaGraphInstantiateFlagUseNodePriority));
+    size_t nn = 0;
+    CUDA_TRY(c, cudaGraphGetNodes(g, nullptr, &nn));
+    std::vector<cudaGraphNode_t> nodes(nn);
+    CUDA_TRY(c, cudaGraphGetNodes(g, nodes.data(), &nn));
+    for (cudaGraphNode_t nd : nodes) {
+      cudaGraphNodeType ty;
+      CUDA_TRY(c, cudaGraphNodeGetType(nd, &ty));
+      if (ty != cudaGraphNodeTypeKernel) continue;
+      cudaKernelNodeParams kp;
+      CUDA_TRY(c, cudaGraphKernelNodeGetParams(nd, &kp));
+      if (kp.func == gen_panels_kernel_fn()) c->gen_nodes.push_back(nd);
+    }
+    if (c->gen_nodes.size() != c->rs.size()) {
+      destroy_graph(c);
+      return fail(c, EXAGEO_ECUDA, "graph capture: generator nodes not found");
+    }
+    c->gkey = key;
+    c->graph_kernels = c->kernels - k0;
+    c->kernels = k0;
+    for (auto& R : c->rs) {
+      R.g_n_u2 = R.n_u2;
+      R.g_u2_flops = R.u2_flops;
+    }
+  } else {
+    for (auto& R : c->rs) {
+      R.n_u2 = R.g_n_u2;
+      R.u2_flops = R.g_u2_flops;
+    }
+    for (cudaGraphNode_t nd : c->gen_nodes) {  // new theta into every K1 node
+      cudaKernelNodeParams kp;
+      CUDA_TRY(c, cudaGraphKernelNodeGetParams(nd, &kp));
+      void* args[6];
+      for (int i = 0; i < 6; ++i) args[i] = kp.kernelParams[i];
+      args[2] = (void*)&mc;  // gen_panels_kernel(Layout, double*, MaternConsts, x, y, z)
+      kp.kernelParams = args;
+      CUDA_TRY(c, cudaGraphExecKernelNodeSetParams(c->gexec, nd, &kp));
+    }
+  }
+  CUDA_TRY(c, cudaGraphLaunch(c->gexec, c->stream));
+  c->kernels += c->graph_kernels;
+  c->have_matrix = true;
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  const double* hd = (const double*)c->h_res;
+  const int* hi = (const int*)(hd + 4);
+  int64_t best = -1;
+  for (size_t i = 0; i < c->rs.size(); ++i)
+    if (hi[i] > 0 && (best < 0 || hi[i] - 1 < best)) best = hi[i] - 1;
+  *pivot = best;
+  if (best >= 0) {
+    r3[0] = -std::numeric_limits<double>::infinity();
+    r3[1] = r3[2] = std::numeric_limits<double>::quiet_NaN();
+    return fail(c, EXAGEO_ENOTPD, "covariance not positive definite at pivot " + std::to_string(best));
+  }
+  memcpy(r3, hd, 3 * sizeof(double));
+  return EXAGEO_OK;
+}
+
 exageo_status loglik_device(exageo_ctx* c, const exageo_theta* t, int64_t n, const double* x, const double* y,
                             const double* z, double* loglik, exageo_loglik_info* info) {
   if (!z) return fail(c, EXAGEO_EINVAL, "NULL z");
   const int64_t k0 = c->kernels;
-  CUDA_TRY(c, cudaEventRecord(c->ev[0], c->stream));
-  exageo_status st = do_generate(c, t, n, x, y, z);
-  if (st != EXAGEO_OK) return st;
-  CUDA_TRY(c, cudaEventRecord(c->ev[1], c->stream));
-  st = do_factor(c);
-  if (st != EXAGEO_OK) return st;
-  CUDA_TRY(c, cudaEventRecord(c->ev[2], c->stream));
   double r3[3];
   int64_t piv = -1;
-  st = do_finish(c, r3, &piv);
-  if (st != EXAGEO_OK && st != EXAGEO_ENOTPD) return st;
-  CUDA_TRY(c, cudaEventRecord(c->ev[3], c->stream));
-  CUDA_TRY(c, cudaEventSynchronize(c->ev[3]));
+  exageo_status st;
+  if (graph_eligible(c, n)) {
+    st = run_graph(c, t, n, x, y, z, r3, &piv);
+    if (st != EXAGEO_OK && st != EXAGEO_ENOTPD) return st;
+  } else {
+    CUDA_TRY(c, cudaEventRecord(c->ev[0], c->stream));
+    st = do_generate(c, t, n, x, y, z);
+    if (st != EXAGEO_OK) return st;
+    CUDA_TRY(c, cudaEventRecord(c->ev[1], c->stream));
+    st = do_factor(c);
+    if (st != EXAGEO_OK) return st;
+    CUDA_TRY(c, cudaEventRecord(c->ev[2], c->stream));
+    st = do_finish(c, r3, &piv);
+    if (st != EXAGEO_OK && st != EXAGEO_ENOTPD) return st;
+    CUDA_TRY(c, cudaEventRecord(c->ev[3], c->stream));
+    CUDA_TRY(c, cudaEventSynchronize(c->ev[3]));
+  }
   if (loglik) *loglik = r3[0];
   if (info) {
     memset(info, 0, sizeof(*info));
@@ -594,6 +759,7 @@ exageo_status exageo_create(exageo_ctx** out, const exageo_opts* opts) {
   c->device = o.device;
   c->nb_opt = o.nb;
   c->ind = o.ind_tiles > 0 ? o.ind_tiles : 0;
+  c->graphs = o.graphs > 0 ? 1 : (o.graphs < 0 ? -1 : 0);
   c->metric = o.distance;
   c->radius = o.radius > 0 ? o.radius : 6371.0;
   c->virt = o.virtual_ranks > 1;
@@ -650,6 +816,8 @@ void exageo_destroy(exageo_ctx* c) {
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
   if (c->comm) nccl::CommDestroy(c->comm);
+  destroy_graph(c);
+  if (c->h_res) cudaFreeHost(c->h_res);
   for (auto& R : c->rs) destroy_rank(R);
   cudaFree(c->parts);
   cudaFree(c->out3);

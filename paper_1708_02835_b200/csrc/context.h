@@ -37,6 +37,8 @@ struct RankState {
   std::vector<cudaEvent_t> u2b, u2e;             // timing of the bulk trailing update
   int n_u2 = 0;
   double u2_flops = 0.0;
+  int g_n_u2 = 0;                                // n_u2 / u2_flops of the captured graph
+  double g_u2_flops = 0.0;
 };
 
 }  // namespace exageo
@@ -66,6 +68,15 @@ struct exageo_ctx {
   cudaEvent_t ev_fork = nullptr;
   int64_t kernels = 0;
   std::string err;
+  // CUDA-graph replay of a whole evaluation (exageo_opts.graphs; api.cu loglik_graph)
+  int graphs = 0;                          // 0 automatic, 1 always, -1 never
+  bool capturing = false;                  // inside cudaStreamBeginCapture on `stream`
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  std::vector<cudaGraphNode_t> gen_nodes;  // K1 nodes: theta is updated per replay
+  std::vector<const void*> gkey;           // sizes + every device pointer the graph bakes in
+  int64_t graph_kernels = 0;
+  void* h_res = nullptr;                   // pinned: {loglik, logdet, quad, -} + one info word per rank
 };
 
 namespace exageo {

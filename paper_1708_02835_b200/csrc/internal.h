@@ -94,6 +94,7 @@ cudaError_t potrf_init();
 // K1: generate this rank's panels of Sigma(theta) (identity padding, z in the z row block).
 void launch_gen_panels(const Layout& L, double* ws, const MaternConsts& mc, const double* x, const double* y,
                        const double* z, cudaStream_t s);
+const void* gen_panels_kernel_fn();  // the K1 kernel (CUDA-graph node identification)
 void launch_matern_dense(const MaternConsts& mc, int64_t m, const double* x1, const double* y1, int64_t n,
                          const double* x2, const double* y2, double* C, int64_t ldc, cudaStream_t s);
 

@@ -262,6 +262,8 @@ void launch_krige(const MaternConsts& mc, int64_t m, const double* xn, const dou
   krige_sum_kernel<<<(unsigned)((m + 255) / 256), 256, 0, s>>>(m, part, nch, znew);
 }
 
+const void* gen_panels_kernel_fn() { return (const void*)gen_panels_kernel; }
+
 void launch_gen_panels(const Layout& L, double* ws, const MaternConsts& mc, const double* x, const double* y,
                        const double* z, cudaStream_t s) {
   if (L.owned() == 0) return;
