@@ -214,8 +214,12 @@ def run_extras(ex, si, torch, device: int) -> dict:
             c.loglik_dev(X, Y, Z, THETA)
             r = c.loglik_dev(X, Y, Z, THETA)
             i = r.info
+            tf = n**3 / 3 / (i["ms_chol"] * 1e-3) / 1e12
             sweep.append({"n": n, "nb": i["nb"], "evals_per_s": 1e3 / i["ms_total"], "ms": i["ms_total"],
-                          "cholesky_tflops": n**3 / 3 / (i["ms_chol"] * 1e-3) / 1e12})
+                          "phase_ms": {"gen": i["ms_gen"], "chol_and_solve": i["ms_chol"], "reduce": i["ms_reduce"]},
+                          "cholesky_tflops": tf, "cholesky_frac_fp64_peak": tf / FP64_PEAK_TFLOPS,
+                          "gen_gb_per_s": 8.0 * n * (n + 1) / 2 / (i["ms_gen"] * 1e-3) / 1e9,
+                          "graphs": n <= 32768})
         out["config3_sweep"] = sweep
     return out
 
