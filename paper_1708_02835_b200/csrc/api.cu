@@ -218,9 +218,10 @@ exageo_status prepare_generate(exageo_ctx* c, const exageo_theta* t, int64_t n, 
 
 exageo_status launch_generate(exageo_ctx* c, const MaternConsts& mc, const double* x, const double* y,
                               const double* z) {
+  c->kernels += launch_matern_table(mc, c->mtab, c->stream);
   for (auto& R : c->rs) {
     CUDA_TRY(c, cudaMemsetAsync(R.info, 0, sizeof(int), c->stream));
-    launch_gen_panels(R.L, R.ws, mc, x, y, z, c->stream);
+    launch_gen_panels(R.L, R.ws, mc, x, y, z, c->mtab, c->stream);
     c->kernels += 1;
   }
   c->have_matrix = true;
@@ -474,9 +475,10 @@ void destroy_graph(exageo_ctx* c) {
   c->gkey.clear();
 }
 
-std::vector<const void*> graph_key(const exageo_ctx* c, const double* x, const double* y, const double* z) {
+std::vector<const void*> graph_key(const exageo_ctx* c, const double* x, const double* y, const double* z,
+                                   int kind) {
   std::vector<const void*> k = {(const void*)(intptr_t)c->G.n, (const void*)(intptr_t)c->G.nb, x, y, z,
-                                c->parts, c->out3, c->h_res};
+                                c->parts, c->out3, c->h_res, c->mtab, (const void*)(intptr_t)(kind == 0)};
   for (const auto& R : c->rs) {
     for (const void* p : {(const void*)R.ws, (const void*)R.slots, (const void*)R.recv[0], (const void*)R.recv[1],
                           (const void*)R.W, (const void*)R.scratch, (const void*)R.info})
@@ -518,7 +520,7 @@ exageo_status run_graph(exageo_ctx* c, const exageo_theta* t, int64_t n, const d
       R.u2e.push_back(e);
     }
   const MaternConsts mc = make_consts(*t, c);
-  std::vector<const void*> key = graph_key(c, x, y, z);
+  std::vector<const void*> key = graph_key(c, x, y, z, mc.kind);
   if (!c->gexec || key != c->gkey) {
     destroy_graph(c);
     const int64_t k0 = c->kernels;
@@ -545,9 +547,9 @@ exageo_status run_graph(exageo_ctx* c, const exageo_theta* t, int64_t n, const d
       if (ty != cudaGraphNodeTypeKernel) continue;
       cudaKernelNodeParams kp;
       CUDA_TRY(c, cudaGraphKernelNodeGetParams(nd, &kp));
-      if (kp.func == gen_panels_kernel_fn()) c->gen_nodes.push_back(nd);
+      if (kp.func == gen_panels_kernel_fn() || kp.func == matern_table_kernel_fn()) c->gen_nodes.push_back(nd);
     }
-    if (c->gen_nodes.size() != c->rs.size()) {
+    if (c->gen_nodes.size() != c->rs.size() + (mc.kind == 0 ? 1 : 0)) {
       destroy_graph(c);
       return fail(c, EXAGEO_ECUDA, "graph capture: generator nodes not found");
     }
@@ -563,12 +565,15 @@ exageo_status run_graph(exageo_ctx* c, const exageo_theta* t, int64_t n, const d
       R.n_u2 = R.g_n_u2;
       R.u2_flops = R.g_u2_flops;
     }
-    for (cudaGraphNode_t nd : c->gen_nodes) {  // new theta into every K1 node
+    for (cudaGraphNode_t nd : c->gen_nodes) {  // new theta into every K1 / K1T node
       cudaKernelNodeParams kp;
       CUDA_TRY(c, cudaGraphKernelNodeGetParams(nd, &kp));
-      void* args[6];
-      for (int i = 0; i < 6; ++i) args[i] = kp.kernelParams[i];
-      args[2] = (void*)&mc;  // gen_panels_kernel(Layout, double*, MaternConsts, x, y, z)
+      void* args[7];
+      const bool gen = kp.func == gen_panels_kernel_fn();
+      const int nargs = gen ? 7 : 2, imc = gen ? 2 : 0;
+      // gen_panels_kernel(Layout, ws, MaternConsts, x, y, z, tab); matern_table_kernel(MaternConsts, tab)
+      for (int i = 0; i < nargs; ++i) args[i] = kp.kernelParams[i];
+      args[imc] = (void*)&mc;
       kp.kernelParams = args;
       CUDA_TRY(c, cudaGraphExecKernelNodeSetParams(c->gexec, nd, &kp));
     }
@@ -789,6 +794,7 @@ exageo_status exageo_create(exageo_ctx** out, const exageo_opts* opts) {
     if ((e = init_rank(R)) != cudaSuccess) return bail(e, "rank state");
   if ((e = cudaMalloc(&c->parts, sizeof(double) * 2 * c->world)) != cudaSuccess) return bail(e, "cudaMalloc");
   if ((e = cudaMalloc(&c->out3, sizeof(double) * 4)) != cudaSuccess) return bail(e, "cudaMalloc");
+  if ((e = cudaMalloc(&c->mtab, sizeof(double) * matern_table_doubles())) != cudaSuccess) return bail(e, "cudaMalloc");
   if ((e = cudaMalloc(&c->pivbuf, sizeof(int64_t))) != cudaSuccess) return bail(e, "cudaMalloc");
   if (!c->virt && o.nccl_id) {  // world > 1, or a single-rank NCCL communicator (world 1)
     ncclUniqueId id;
@@ -821,6 +827,7 @@ void exageo_destroy(exageo_ctx* c) {
   for (auto& R : c->rs) destroy_rank(R);
   cudaFree(c->parts);
   cudaFree(c->out3);
+  cudaFree(c->mtab);
   cudaFree(c->pivbuf);
   cudaFree(c->vec);
   cudaFree(c->zsum);
@@ -870,7 +877,7 @@ exageo_status exageo_matern_cov(exageo_ctx* c, const exageo_theta* t, int64_t m,
   cudaMemcpyAsync(dy1, y1, sizeof(double) * m, cudaMemcpyHostToDevice, c->stream);
   cudaMemcpyAsync(dx2, x2, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream);
   cudaMemcpyAsync(dy2, y2, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream);
-  launch_matern_dense(make_consts(*t, c), m, dx1, dy1, n, dx2, dy2, dC, m, c->stream);
+  launch_matern_dense(make_consts(*t, c), m, dx1, dy1, n, dx2, dy2, dC, m, c->mtab, c->stream);
   c->kernels += 1;
   cudaError_t e = cudaMemcpy2DAsync(C, sizeof(double) * ldc, dC, sizeof(double) * m, sizeof(double) * m, n,
                                     cudaMemcpyDeviceToHost, c->stream);
@@ -1005,7 +1012,7 @@ exageo_status exageo_predict(exageo_ctx* c, const exageo_theta* t, int64_t n, co
                                   c->stream));
   }
   // Alg. 3 l.8 / Eq. (5): z1 = Sigma12 w with Sigma12 generated on the fly
-  launch_krige(make_consts(*t, c), m, dxn, dyn, n, dx, dy, w, pkr, dzn, c->stream);
+  launch_krige(make_consts(*t, c), m, dxn, dyn, n, dx, dy, w, pkr, dzn, c->mtab, c->stream);
   c->kernels += 2;
   st = check_launch(c);
   if (st != EXAGEO_OK) return st;

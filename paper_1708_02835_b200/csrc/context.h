@@ -58,6 +58,7 @@ struct exageo_ctx {
   std::vector<exageo::RankState> rs;
   double* parts = nullptr;    // 2 * world doubles: per-rank {sum log L_ii, sum y^2}
   double* out3 = nullptr;     // {loglik, logdet, quad}
+  double* mtab = nullptr;     // per-theta Chebyshev table of the Matern function (K1T)
   int64_t* pivbuf = nullptr;  // NCCL mode: all-reduced first failing pivot
   double* vec = nullptr;      // 4 n staging for host-pointer entry points
   int64_t vec_cap = 0;

@@ -91,12 +91,19 @@ cudaError_t gemm_init();
 cudaError_t potrf_init();
 
 // ---- launchers (all asynchronous on `s`) ----
-// K1: generate this rank's panels of Sigma(theta) (identity padding, z in the z row block).
+// K1T: per-theta Chebyshev table of the Matern function for general nu (matern.cu);
+// returns 1 if a table kernel was launched (kind == 0), 0 for the closed forms.
+int matern_table_doubles();
+int launch_matern_table(const MaternConsts& mc, double* tab, cudaStream_t s);
+const void* matern_table_kernel_fn();  // CUDA-graph node identification
+// K1: generate this rank's panels of Sigma(theta) (identity padding, z in the z row block);
+// tab = the table built by launch_matern_table for this theta (used when kind == 0).
 void launch_gen_panels(const Layout& L, double* ws, const MaternConsts& mc, const double* x, const double* y,
-                       const double* z, cudaStream_t s);
+                       const double* z, const double* tab, cudaStream_t s);
 const void* gen_panels_kernel_fn();  // the K1 kernel (CUDA-graph node identification)
+// Dense Matern block and kriging sums (build the table themselves into tab when needed).
 void launch_matern_dense(const MaternConsts& mc, int64_t m, const double* x1, const double* y1, int64_t n,
-                         const double* x2, const double* y2, double* C, int64_t ldc, cudaStream_t s);
+                         const double* x2, const double* y2, double* C, int64_t ldc, double* tab, cudaStream_t s);
 
 // C (M x N, ldc) = C - A (M x K, lda) * B (N x K, ldb)^T      (accumulate = true)
 // C (M x N, ldc) =     A (M x K, lda) * B (N x K, ldb)^T      (accumulate = false; may alias A when N == K <= 64)
@@ -140,6 +147,7 @@ void launch_backsolve_panel(const double* P, int64_t ld, int nb, int64_t row_aft
 // covariance block Sigma12 generated on the fly and never stored. part: krige_chunks(n) * m.
 int krige_chunks(int64_t n);
 void launch_krige(const MaternConsts& mc, int64_t m, const double* xn, const double* yn, int64_t n,
-                  const double* x, const double* y, const double* w, double* part, double* znew, cudaStream_t s);
+                  const double* x, const double* y, const double* w, double* part, double* znew, double* tab,
+                  cudaStream_t s);
 
 }  // namespace exageo

@@ -96,10 +96,8 @@ __device__ __forceinline__ void bessel_k_cf2_scaled(double x, double mu, double&
 
 }  // namespace
 
-// Matern covariance at distance r (Eq. (2)); C(0) = theta1 (R9).
-__device__ __forceinline__ double matern_eval(double r, const MaternConsts& c) {
-  if (r == 0.0) return c.theta1;
-  const double x = r * c.inv_theta2;
+// theta1 / (2^(nu-1) Gamma(nu)) x^nu K_nu(x) for x > 0 (Eq. (2) at x = r / theta2).
+__device__ __forceinline__ double matern_x(double x, const MaternConsts& c) {
   switch (c.kind) {
     case 1: return c.theta1 * exp(-x);
     case 2: return c.theta1 * (1.0 + x) * exp(-x);
@@ -130,6 +128,78 @@ __device__ __forceinline__ double matern_eval(double r, const MaternConsts& c) {
   return c.pref * ex * knu;
 }
 
+// ---- per-theta Chebyshev table of matern_x for general nu (K1T) -------------------------
+// theta is fixed during one evaluation, so x -> C(x) is tabulated once per evaluation on
+// 152 intervals -- [2^-6, 4) in quarter octaves (their width is proportional to the
+// distance from the branch point x = 0 of x^nu K_nu, so the Chebyshev series converge at
+// the same geometric rate on every interval) and [4, 64) in steps of 1/2 -- each by a
+// degree-15 Chebyshev interpolant of the direct evaluator (coefficients decay below 1e-20
+// of the value), evaluated by Clenshaw's recurrence: ~35 FP64 instructions per entry instead
+// of the series/continued fraction's ~1500. Outside [2^-6, 64) the direct evaluator runs.
+constexpr int kTabDeg = 16;     // Chebyshev coefficients per interval
+constexpr int kTabStride = 18;  // {1 / half width, mid / half width, c_0 .. c_15}
+constexpr int kTabLog = 32;     // [2^-6, 4): 8 octaves x 4
+constexpr int kTabLin = 120;    // [4, 64): width 1/2
+constexpr int kTabN = kTabLog + kTabLin;
+constexpr double kTabX0 = 0.015625, kTabX1 = 4.0, kTabXMax = 64.0;
+
+__global__ void __launch_bounds__(kTabDeg) matern_table_kernel(MaternConsts mc, double* __restrict__ tab) {
+  const int i = blockIdx.x, j = threadIdx.x;
+  double a, b;
+  if (i < kTabLog) {
+    a = exp2(-6.0 + 0.25 * i);
+    b = exp2(-6.0 + 0.25 * (i + 1));
+  } else {
+    a = kTabX1 + 0.5 * (i - kTabLog);
+    b = a + 0.5;
+  }
+  const double mid = 0.5 * (a + b), half = 0.5 * (b - a);
+  __shared__ double fv[kTabDeg];
+  fv[j] = matern_x(mid + half * cospi((j + 0.5) / kTabDeg), mc);  // Chebyshev nodes
+  __syncthreads();
+  double ck = 0.0;  // c_k = (2/N) sum_j f_j cos(pi k (j + 1/2) / N), c_0 halved
+  for (int jj = 0; jj < kTabDeg; ++jj) ck += fv[jj] * cospi(j * (jj + 0.5) / kTabDeg);
+  ck *= (j == 0 ? 1.0 : 2.0) / kTabDeg;
+  double* p = tab + i * kTabStride;
+  p[2 + j] = ck;
+  if (j == 0) {
+    p[0] = 1.0 / half;
+    p[1] = mid / half;
+  }
+}
+
+__device__ __forceinline__ double matern_tab(double x, const double* __restrict__ tab) {
+  int i;
+  if (x < kTabX1) {  // quarter octave of x: exponent bits + three mantissa thresholds
+    const long long bits = __double_as_longlong(x);
+    const int e = (int)((bits >> 52) & 0x7ff) - 1023;
+    const double m = __longlong_as_double((bits & 0x000fffffffffffffLL) | 0x3ff0000000000000LL);
+    i = 4 * (e + 6) + (m >= 1.1892071150027210667) + (m >= 1.4142135623730950488) + (m >= 1.6817928305074290861);
+  } else {
+    i = kTabLog + (int)((x - kTabX1) * 2.0);
+  }
+  const double* p = tab + i * kTabStride;
+  const double t = fma(x, __ldg(p), -__ldg(p + 1));
+  const double t2 = 2.0 * t;
+  double b1 = 0.0, b2 = 0.0;
+#pragma unroll
+  for (int k = kTabDeg - 1; k >= 1; --k) {
+    const double b0 = fma(t2, b1, __ldg(p + 2 + k) - b2);
+    b2 = b1;
+    b1 = b0;
+  }
+  return fma(t, b1, __ldg(p + 2) - b2);
+}
+
+// Matern covariance at distance r (Eq. (2)); C(0) = theta1 (R9). tab: the per-theta table
+// (general nu) or nullptr.
+__device__ __forceinline__ double matern_eval(double r, const MaternConsts& c, const double* __restrict__ tab) {
+  if (r == 0.0) return c.theta1;
+  const double x = r * c.inv_theta2;
+  if (c.kind == 0 && tab != nullptr && x >= kTabX0 && x < kTabXMax) return matern_tab(x, tab);
+  return matern_x(x, c);
+}
+
 // Distance between s1 = (x1, y1) and s2 = (x2, y2): Euclidean (R15), or the great-circle
 // distance by the haversine formula with x = longitude, y = latitude in
 // degrees: d = 2 R asin(sqrt(hav(dphi) + cos(phi1) cos(phi2) hav(dlambda))), hav(a) = sin^2(a/2).
@@ -150,11 +220,11 @@ __device__ __forceinline__ double dist2d(double x1, double y1, double x2, double
 // padding outside n, IND-annihilated tiles, the diagonal theta1 (R9), else Eq. (2).
 __device__ __noinline__ double gen_entry(const Layout& L, const MaternConsts& mc, const double* __restrict__ x,
                                             const double* __restrict__ y, int64_t r, int64_t c, double xc,
-                                            double yc) {
+                                            double yc, const double* __restrict__ tab) {
   if (r >= L.n || c >= L.n) return (r == c) ? 1.0 : 0.0;
   if (!L.in_super_tile(r, c)) return 0.0;  // IND: annihilated off-diagonal tile
   if (r == c) return mc.theta1;
-  return matern_eval(dist2d(x[r], y[r], xc, yc, mc), mc);
+  return matern_eval(dist2d(x[r], y[r], xc, yc, mc), mc, tab);
 }
 
 constexpr int kGenCols = 8;  // columns per CTA: one (x, y) row load and index test serve 8 entries
@@ -165,7 +235,7 @@ constexpr int kGenCols = 8;  // columns per CTA: one (x, y) row load and index t
 // check-free path.
 __global__ void __launch_bounds__(256) gen_panels_kernel(Layout L, double* __restrict__ ws, MaternConsts mc,
                                                          const double* __restrict__ x, const double* __restrict__ y,
-                                                         const double* __restrict__ z) {
+                                                         const double* __restrict__ z, const double* __restrict__ tab) {
   const int j = L.owned_panel(blockIdx.y);
   const int cc0 = blockIdx.x * kGenCols;
   const int64_t jb = (int64_t)j * L.nb;
@@ -186,8 +256,8 @@ __global__ void __launch_bounds__(256) gen_panels_kernel(Layout L, double* __res
       const double x0 = x[r0], y0 = y[r0], x1 = x[r0 + 1], y1 = y[r0 + 1];
 #pragma unroll 1
       for (int k = 0; k < kGenCols; ++k) {  // rolled: one inlined copy of the evaluator
-        const double v0 = matern_eval(dist2d(x0, y0, xc[k], yc[k], mc), mc);
-        const double v1 = matern_eval(dist2d(x1, y1, xc[k], yc[k], mc), mc);
+        const double v0 = matern_eval(dist2d(x0, y0, xc[k], yc[k], mc), mc, tab);
+        const double v1 = matern_eval(dist2d(x1, y1, xc[k], yc[k], mc), mc, tab);
         *reinterpret_cast<double2*>(col0 + k * ld + rr) = make_double2(v0, v1);
       }
     } else {
@@ -199,7 +269,7 @@ __global__ void __launch_bounds__(256) gen_panels_kernel(Layout L, double* __res
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int64_t lr = rr + e;
-          if (lr < R) v[e] = gen_entry(L, mc, x, y, jb + lr, c, xck, yck);
+          if (lr < R) v[e] = gen_entry(L, mc, x, y, jb + lr, c, xck, yck, tab);
           else v[e] = (lr == R && c < L.n && z != nullptr) ? z[c] : 0.0;  // z row block
         }
         *reinterpret_cast<double2*>(col0 + k * ld + rr) = make_double2(v[0], v[1]);
@@ -212,11 +282,11 @@ __global__ void __launch_bounds__(256) matern_dense_kernel(MaternConsts mc, int6
                                                            const double* __restrict__ y1, int64_t n,
                                                            const double* __restrict__ x2,
                                                            const double* __restrict__ y2, double* __restrict__ C,
-                                                           int64_t ldc) {
+                                                           int64_t ldc, const double* __restrict__ tab) {
   const int64_t j = blockIdx.y;
   const double xj = x2[j], yj = y2[j];
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
-    C[i + j * ldc] = matern_eval(dist2d(x1[i], y1[i], xj, yj, mc), mc);
+    C[i + j * ldc] = matern_eval(dist2d(x1[i], y1[i], xj, yj, mc), mc, tab);
 }
 
 constexpr int kKrigeChunk = 8192;
@@ -226,14 +296,15 @@ __global__ void __launch_bounds__(256) krige_partial_kernel(MaternConsts mc, int
                                                             const double* __restrict__ yn, int64_t n,
                                                             const double* __restrict__ x,
                                                             const double* __restrict__ y,
-                                                            const double* __restrict__ w, double* __restrict__ part) {
+                                                            const double* __restrict__ w, double* __restrict__ part,
+                                                            const double* __restrict__ tab) {
   __shared__ double red[8];
   const int64_t i = blockIdx.x;
   const int64_t j0 = (int64_t)blockIdx.y * kKrigeChunk;
   const int64_t j1 = (j0 + kKrigeChunk) < n ? (j0 + kKrigeChunk) : n;
   const double xi = xn[i], yi = yn[i];
   double acc = 0.0;
-  for (int64_t j = j0 + threadIdx.x; j < j1; j += blockDim.x) acc += matern_eval(dist2d(xi, yi, x[j], y[j], mc), mc) * w[j];
+  for (int64_t j = j0 + threadIdx.x; j < j1; j += blockDim.x) acc += matern_eval(dist2d(xi, yi, x[j], y[j], mc), mc, tab) * w[j];
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
   __syncthreads();
@@ -254,31 +325,42 @@ __global__ void krige_sum_kernel(int64_t m, const double* __restrict__ part, int
 
 int krige_chunks(int64_t n) { return (int)((n + kKrigeChunk - 1) / kKrigeChunk); }
 
+int matern_table_doubles() { return kTabN * kTabStride; }
+const void* matern_table_kernel_fn() { return (const void*)matern_table_kernel; }
+
+int launch_matern_table(const MaternConsts& mc, double* tab, cudaStream_t s) {
+  if (mc.kind != 0 || tab == nullptr) return 0;
+  matern_table_kernel<<<kTabN, kTabDeg, 0, s>>>(mc, tab);
+  return 1;
+}
+
 void launch_krige(const MaternConsts& mc, int64_t m, const double* xn, const double* yn, int64_t n, const double* x,
-                  const double* y, const double* w, double* part, double* znew, cudaStream_t s) {
+                  const double* y, const double* w, double* part, double* znew, double* tab, cudaStream_t s) {
   const int nch = krige_chunks(n);  // <= 65535 chunks (n < 5.3e8)
   dim3 grid((unsigned)m, (unsigned)nch);
-  krige_partial_kernel<<<grid, 256, 0, s>>>(mc, m, xn, yn, n, x, y, w, part);
+  const double* t = launch_matern_table(mc, tab, s) ? tab : nullptr;
+  krige_partial_kernel<<<grid, 256, 0, s>>>(mc, m, xn, yn, n, x, y, w, part, t);
   krige_sum_kernel<<<(unsigned)((m + 255) / 256), 256, 0, s>>>(m, part, nch, znew);
 }
 
 const void* gen_panels_kernel_fn() { return (const void*)gen_panels_kernel; }
 
 void launch_gen_panels(const Layout& L, double* ws, const MaternConsts& mc, const double* x, const double* y,
-                       const double* z, cudaStream_t s) {
+                       const double* z, const double* tab, cudaStream_t s) {
   if (L.owned() == 0) return;
   dim3 grid(L.nb / kGenCols, L.owned());
-  gen_panels_kernel<<<grid, 256, 0, s>>>(L, ws, mc, x, y, z);
+  gen_panels_kernel<<<grid, 256, 0, s>>>(L, ws, mc, x, y, z, mc.kind == 0 ? tab : nullptr);
 }
 
 void launch_matern_dense(const MaternConsts& mc, int64_t m, const double* x1, const double* y1, int64_t n,
-                         const double* x2, const double* y2, double* C, int64_t ldc, cudaStream_t s) {
+                         const double* x2, const double* y2, double* C, int64_t ldc, double* tab, cudaStream_t s) {
+  const double* t = launch_matern_table(mc, tab, s) ? tab : nullptr;
   for (int64_t j0 = 0; j0 < n; j0 += 65535) {
     const int64_t nj = (n - j0) < 65535 ? (n - j0) : 65535;
     int gx = (int)((m + 255) / 256);
     if (gx > 64) gx = 64;
     dim3 grid(gx, (unsigned)nj);
-    matern_dense_kernel<<<grid, 256, 0, s>>>(mc, m, x1, y1, nj, x2 + j0, y2 + j0, C + j0 * ldc, ldc);
+    matern_dense_kernel<<<grid, 256, 0, s>>>(mc, m, x1, y1, nj, x2 + j0, y2 + j0, C + j0 * ldc, ldc, t);
   }
 }
 
