@@ -90,3 +90,28 @@ def test_graph_mle_identical_to_stream_mle():
         b = s.mle(x, y, z, lo, hi, start, xtol_rel=1e-6, profile=True)
     assert a[0] == b[0] and a[1] == b[1] and a[2] == b[2]
     assert np.array_equal(a[3], b[3])
+
+
+def test_graph_ind_and_great_circle():
+    # the IND mask and the haversine distance are baked into the captured kernels' arguments
+    n = 1500
+    x, y = ex.gen_locations(n, 11)
+    z = si.normals(n, 12)
+    X, Y, Z = _dev(x, y, z)
+    for kw in ({"ind_tiles": 3, "nb": 128}, {"distance": "great_circle", "radius": 1.0}):
+        with ex.Context(device=0, graphs=1, **kw) as g, ex.Context(device=0, graphs=-1, **kw) as s:
+            for th in THETAS[:3]:
+                a, b = g.loglik_dev(X, Y, Z, th), s.loglik_dev(X, Y, Z, th)
+                assert (a.loglik, a.logdet, a.quad) == (b.loglik, b.logdet, b.quad), (kw, th)
+
+
+def test_graph_closed_form_to_general_nu_recapture():
+    # nu = 1/2 needs no table kernel, general nu does: switching recaptures, results stay exact
+    n = 800
+    x, y = ex.gen_locations(n, 13)
+    z = si.normals(n, 14)
+    X, Y, Z = _dev(x, y, z)
+    seq = [(1.0, 0.1, 0.5), (1.0, 0.1, 0.9), (1.0, 0.1, 1.5), (1.0, 0.1, 0.9), (1.0, 0.1, 0.5), (1.0, 0.1, 0.61)]
+    with ex.Context(device=0, graphs=1) as g, ex.Context(device=0, graphs=-1) as s:
+        for th in seq:
+            assert g.loglik_dev(X, Y, Z, th).loglik == s.loglik_dev(X, Y, Z, th).loglik, th

@@ -83,7 +83,7 @@ def test_matern_cov_distance_sweep(ctx):
 # the quarter-octave intervals, 0.1 the linear intervals
 @pytest.mark.parametrize("n,nb,nu,beta", [(700, 128, 0.5, 0.1), (1000, 256, 1.3, 0.1), (131, 128, 2.5, 0.1),
                                           (900, 128, 0.37, 0.01), (600, 128, 1.73, 2.0), (800, 256, 1.0, 0.1),
-                                          (500, 128, 0.83, 0.5)])
+                                          (500, 128, 0.83, 0.5), (400, 128, 0.1, 0.3), (400, 128, 4.9, 0.05)])
 def test_generated_panels_match_oracle(n, nb, nu, beta):
     c = ex.Context(device=0, nb=nb)
     x, y = ex.gen_locations(n, 3)

@@ -77,11 +77,13 @@ int main(int argc, char** argv) {
   cudaDeviceSynchronize();
   printf("n=%lld T=%d workspace %.2f GB\n", (long long)n, L.T, bytes / 1e9);
   for (int k : {0, L.T / 2}) {
-    run<Cfg<64, 64, 16, 2, 2, 2, 4>, 2>("64x64x16 st2 preC", L, ws, k, 3);
-    run<Cfg<64, 64, 16, 2, 2, 2, 4, true>, 2>("64x64x16 st2 preC xpf", L, ws, k, 3);
-    run<Cfg<64, 64, 16, 2, 2, 3, 4, true>, 2>("64x64x16 st3 preC xpf", L, ws, k, 3);
-    run<Cfg<64, 64, 8, 2, 2, 4, 4, true>, 2>("64x64x8 st4 preC xpf", L, ws, k, 3);
-    run<Cfg<64, 64, 8, 2, 2, 3, 4, true>, 2>("64x64x8 st3 preC xpf", L, ws, k, 3);
+    run<Cfg<64, 64, 16, 2, 2, 2, 4>, 2>("64x64x16 st2 preC (product)", L, ws, k, 3);
+    run<Cfg<64, 64, 16, 2, 2, 2, 5>, 2>("64x64x16 st2 preC 5 CTA/SM", L, ws, k, 3);
+    run<Cfg<64, 64, 16, 2, 2, 3, 4>, 2>("64x64x16 st3 preC", L, ws, k, 3);
+    run<Cfg<64, 64, 32, 2, 2, 2, 3>, 2>("64x64x32 st2 preC 3 CTA/SM", L, ws, k, 3);
+    run<Cfg<64, 128, 16, 2, 2, 2, 2>, 2>("64x128x16 st2 preC warp 32x64", L, ws, k, 3);
+    run<Cfg<128, 64, 16, 2, 2, 2, 2>, 2>("128x64x16 st2 preC warp 64x32", L, ws, k, 3);
+    run<Cfg<64, 128, 16, 2, 2, 3, 2>, 2>("64x128x16 st3 preC warp 32x64", L, ws, k, 3);
   }
   return 0;
 }
