@@ -199,12 +199,18 @@ def run_extras(ex, si, torch, device: int) -> dict:
         x, y = ex.gen_locations(1600, SEED)
         for nu in (0.5, 1.0):
             z = c.simulate(x, y, si.normals(1600, SEED), (1.0, 0.1, nu))
-            for prof in (False, True):  # 3-D search / theta1 profiled out (exageo_mle_profile)
-                t0 = time.perf_counter()
-                th, ll, ne, _ = c.mle(x, y, z, lo, hi, start, xtol_rel=1e-6, max_evals=2000, profile=prof)
-                sec = time.perf_counter() - t0
-                out[f"config2_mle{'_profile' if prof else ''}_n1600_nu{nu}"] = {
-                    "theta_hat": th, "loglik": ll, "evals": ne, "seconds": sec, "ms_per_eval": 1e3 * sec / max(ne, 1)}
+            # 3-D search (the paper's) / theta1 profiled out (R20); Nelder-Mead / quadratic-model
+            # trust region (BOBYQA class)
+            for prof in (False, True):
+                for meth in ("nelder-mead", "trust-region"):
+                    t0 = time.perf_counter()
+                    th, ll, ne, _ = c.mle(x, y, z, lo, hi, start, xtol_rel=1e-6, max_evals=2000, profile=prof,
+                                          method=meth)
+                    sec = time.perf_counter() - t0
+                    tag = ("_profile" if prof else "") + ("_tr" if meth == "trust-region" else "")
+                    out[f"config2_mle{tag}_n1600_nu{nu}"] = {
+                        "theta_hat": th, "loglik": ll, "evals": ne, "seconds": sec,
+                        "ms_per_eval": 1e3 * sec / max(ne, 1)}
         # configs[2]: single-GPU sweep n = 10k - 80k (n = 100k is the headline line)
         sweep = []
         for n in (10_000, 20_000, 40_000, 60_000, 80_000):

@@ -202,6 +202,26 @@ exageo_status exageo_mle_profile(exageo_ctx* ctx, int64_t n, const double* x, co
                                  double xtol_rel, int max_evals, exageo_theta* theta_hat, double* loglik,
                                  int* nevals, double* trace);
 
+/* Options of exageo_mle_ex. */
+typedef struct {
+  double xtol_rel; /* stop when the search scale in log(theta) (simplex diameter / trust-region
+                      radius) falls below this                                                 */
+  int max_evals;   /* evaluation budget                                                        */
+  int profile;     /* 1: theta1 profiled out in closed form (as exageo_mle_profile)            */
+  int method;      /* 0: Nelder-Mead (as exageo_mle); 1: quadratic-model trust region (the
+                      BOBYQA/UOBYQA class): fully determined quadratic interpolation
+                      models on (d+1)(d+2)/2 points, exact box-constrained trust-region steps,
+                      Lagrange-function point replacement; falls back to Nelder-Mead if the
+                      initial interpolation set cannot be evaluated                           */
+} exageo_mle_opts;
+
+/* exageo_mle / exageo_mle_profile with the search method selectable (exageo_mle_opts);
+ * same arguments, outputs and errors (EXAGEO_EINVAL also for a bad method). */
+exageo_status exageo_mle_ex(exageo_ctx* ctx, int64_t n, const double* x, const double* y, const double* z,
+                            const exageo_theta* lo, const exageo_theta* hi, const exageo_theta* start,
+                            const exageo_mle_opts* opts, exageo_theta* theta_hat, double* loglik, int* nevals,
+                            double* trace);
+
 /* Kriging prediction, Eq. (5) by Alg. 3 (R19):
  *   Sigma22 = L L^T (with the forward solve y = L^{-1} z fused into the factorization),
  *   L^T w = y (blocked backward solve), znew = Sigma12 w with the m x n block Sigma12

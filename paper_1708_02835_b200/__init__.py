@@ -38,6 +38,11 @@ class Opts(ctypes.Structure):
                 ("radius", ctypes.c_double), ("graphs", ctypes.c_int)]
 
 
+class MleOpts(ctypes.Structure):
+    _fields_ = [("xtol_rel", ctypes.c_double), ("max_evals", ctypes.c_int), ("profile", ctypes.c_int),
+                ("method", ctypes.c_int)]
+
+
 class LoglikInfo(ctypes.Structure):
     _fields_ = [("loglik", ctypes.c_double), ("logdet", ctypes.c_double), ("quad", ctypes.c_double),
                 ("npd_pivot", ctypes.c_int64), ("n", ctypes.c_int64), ("nb", ctypes.c_int64),
@@ -83,6 +88,9 @@ SIGNATURES = [
     ("exageo_mle_profile", ctypes.c_int, [_C, ctypes.c_int64, _f64p, _f64p, _f64p, ctypes.POINTER(Theta),
                                           ctypes.POINTER(Theta), ctypes.POINTER(Theta), ctypes.c_double, ctypes.c_int,
                                           ctypes.POINTER(Theta), _f64p, ctypes.POINTER(ctypes.c_int), _f64p]),
+    ("exageo_mle_ex", ctypes.c_int, [_C, ctypes.c_int64, _f64p, _f64p, _f64p, ctypes.POINTER(Theta),
+                                     ctypes.POINTER(Theta), ctypes.POINTER(Theta), ctypes.POINTER(MleOpts),
+                                     ctypes.POINTER(Theta), _f64p, ctypes.POINTER(ctypes.c_int), _f64p]),
 ]
 
 _lib = None
@@ -282,9 +290,11 @@ class Context:
         self._check(st, info.npd_pivot)
         return Result(info.loglik, info.logdet, info.quad, info.as_dict())
 
-    def mle(self, x, y, z, lo, hi, start, xtol_rel: float = 1e-9, max_evals: int = 1000, profile: bool = False):
-        """Maximum-likelihood estimate over the box lo <= theta <= hi (exageo_mle, or
-        exageo_mle_profile with theta1 profiled out when profile=True).
+    def mle(self, x, y, z, lo, hi, start, xtol_rel: float = 1e-9, max_evals: int = 1000, profile: bool = False,
+            method: str = "nelder-mead"):
+        """Maximum-likelihood estimate over the box lo <= theta <= hi (exageo_mle_ex):
+        profile=True profiles theta1 out in closed form (exageo_mle_profile); method
+        "nelder-mead" (exageo_mle) or "trust-region" (quadratic-model trust region).
 
         Returns (theta_hat tuple, loglik, nevals, trace as an (nevals, 4) array)."""
         x, y, z = _f(x), _f(y), _f(z)
@@ -293,9 +303,11 @@ class Context:
         ll = ctypes.c_double()
         ne = ctypes.c_int()
         trace = np.zeros((max_evals, 4), np.float64)
-        fn = self._lib.exageo_mle_profile if profile else self._lib.exageo_mle
-        st = fn(self._ctx, z.size, _p(x), _p(y), _p(z), ctypes.byref(tlo), ctypes.byref(thi), ctypes.byref(ts),
-                float(xtol_rel), int(max_evals), ctypes.byref(th), ctypes.byref(ll), ctypes.byref(ne), _p(trace))
+        o = MleOpts(float(xtol_rel), int(max_evals), int(bool(profile)),
+                    {"nelder-mead": 0, "trust-region": 1}[method])
+        st = self._lib.exageo_mle_ex(self._ctx, z.size, _p(x), _p(y), _p(z), ctypes.byref(tlo), ctypes.byref(thi),
+                                     ctypes.byref(ts), ctypes.byref(o), ctypes.byref(th), ctypes.byref(ll),
+                                     ctypes.byref(ne), _p(trace))
         self._check(st)
         return (th.sigma2, th.beta, th.nu), ll.value, ne.value, trace[: ne.value].copy()
 

@@ -24,6 +24,7 @@
 #include <vector>
 
 #include "context.h"
+#include "trust_region.h"
 
 namespace exageo {
 namespace {
@@ -207,7 +208,7 @@ namespace {
 exageo_status run_mle(exageo_ctx* c, int64_t n, const double* x, const double* y, const double* z,
                       const exageo_theta* lo, const exageo_theta* hi, const exageo_theta* start, double xtol_rel,
                       int max_evals, exageo_theta* theta_hat, double* loglik, int* nevals, double* trace,
-                      bool profile) {
+                      bool profile, int method) {
   if (!c) return EXAGEO_EINVAL;
   if (n < 1 || !x || !y || !z || !lo || !hi || !start || !theta_hat || max_evals < 1 || !(xtol_rel > 0))
     return set_error(c, EXAGEO_EINVAL, "bad arguments to exageo_mle");
@@ -254,6 +255,19 @@ exageo_status run_mle(exageo_ctx* c, int64_t n, const double* x, const double* y
   if (f.free_.empty()) {
     std::vector<double> none;
     f(none);
+  } else if (method == 1) {
+    // quadratic-model trust region (trust_region.h) on the free log-parameters
+    std::vector<double> lo_f, hi_f;
+    double span = 1.0;
+    for (int p : f.free_) {
+      lo_f.push_back(f.lo[p]);
+      hi_f.push_back(f.hi[p]);
+      span = std::min(span, f.hi[p] - f.lo[p]);
+    }
+    const double delta0 = std::max(0.1 * span, 10.0 * xtol_rel);
+    const bool ok = dfo::minimize([&](std::vector<double>& v) { return f(v); }, v0, lo_f, hi_f, delta0, xtol_rel,
+                                  [&]() { return f.evals >= f.max_evals || f.err != EXAGEO_OK; });
+    if (!ok && f.err == EXAGEO_OK && f.evals < f.max_evals) nelder_mead(f, v0, h, xtol_rel);  // fallback
   } else {
     nelder_mead(f, v0, h, xtol_rel);
     // restarts from the best vertex with a small fresh simplex while they improve
@@ -283,12 +297,22 @@ extern "C" exageo_status exageo_mle(exageo_ctx* c, int64_t n, const double* x, c
                                     const exageo_theta* lo, const exageo_theta* hi, const exageo_theta* start,
                                     double xtol_rel, int max_evals, exageo_theta* theta_hat, double* loglik,
                                     int* nevals, double* trace) {
-  return run_mle(c, n, x, y, z, lo, hi, start, xtol_rel, max_evals, theta_hat, loglik, nevals, trace, false);
+  return run_mle(c, n, x, y, z, lo, hi, start, xtol_rel, max_evals, theta_hat, loglik, nevals, trace, false, 0);
 }
 
 extern "C" exageo_status exageo_mle_profile(exageo_ctx* c, int64_t n, const double* x, const double* y,
                                             const double* z, const exageo_theta* lo, const exageo_theta* hi,
                                             const exageo_theta* start, double xtol_rel, int max_evals,
                                             exageo_theta* theta_hat, double* loglik, int* nevals, double* trace) {
-  return run_mle(c, n, x, y, z, lo, hi, start, xtol_rel, max_evals, theta_hat, loglik, nevals, trace, true);
+  return run_mle(c, n, x, y, z, lo, hi, start, xtol_rel, max_evals, theta_hat, loglik, nevals, trace, true, 0);
+}
+
+extern "C" exageo_status exageo_mle_ex(exageo_ctx* c, int64_t n, const double* x, const double* y, const double* z,
+                                       const exageo_theta* lo, const exageo_theta* hi, const exageo_theta* start,
+                                       const exageo_mle_opts* o, exageo_theta* theta_hat, double* loglik,
+                                       int* nevals, double* trace) {
+  if (!c) return EXAGEO_EINVAL;
+  if (!o || o->method < 0 || o->method > 1) return set_error(c, EXAGEO_EINVAL, "bad exageo_mle_opts");
+  return run_mle(c, n, x, y, z, lo, hi, start, o->xtol_rel, o->max_evals, theta_hat, loglik, nevals, trace,
+                 o->profile != 0, o->method);
 }

@@ -132,3 +132,45 @@ def test_mle_profile_sigma2_bound_active(ctx):
     assert ll == pytest.approx(ctx.loglik(x, y, z, th).loglik, rel=1e-12)
     thf, llf, _, _ = ctx.mle(x, y, z, lo, hi, (0.1, 0.1, 0.5), xtol_rel=1e-9)
     assert ll >= llf - 1e-9 * abs(llf)
+
+
+@pytest.mark.parametrize("profile", [False, True])
+def test_mle_trust_region_matches_oracle_estimate(ctx, profile):
+    # the quadratic-model trust region (BOBYQA class) reaches the oracle's estimate too
+    g = json.load(open(GOLDEN))
+    n = g["n"]
+    x, y = ex.gen_locations(n, g["seed"])
+    z = oracle.simulate(x, y, tuple(g["theta_true"]), si.normals(n, g["seed"]))
+    th, ll, ne, trace = ctx.mle(x, y, z, tuple(g["lo"]), tuple(g["hi"]), tuple(g["start"]), xtol_rel=1e-10,
+                                max_evals=3000, profile=profile, method="trust-region")
+    for a, b in zip(th, g["theta_hat"]):
+        assert a == pytest.approx(b, rel=1e-4), (th, g["theta_hat"])
+    assert ll == pytest.approx(g["loglik"], rel=1e-10)
+    assert ne == len(trace) and np.max(trace[:, 3]) == ll
+
+
+@pytest.mark.parametrize("nu_true", [0.5, 1.0])
+def test_mle_trust_region_config2_fewer_evals(ctx, nu_true):
+    n = 1600
+    x, y = ex.gen_locations(n, 2)
+    z = ctx.simulate(x, y, si.normals(n, 2), (1.0, 0.1, nu_true))
+    start = tuple(math.sqrt(a * b) for a, b in zip(LO, HI))
+    for profile in (False, True):
+        thn, lln, nen, _ = ctx.mle(x, y, z, LO, HI, start, xtol_rel=1e-9, max_evals=3000, profile=profile)
+        tht, llt, net, _ = ctx.mle(x, y, z, LO, HI, start, xtol_rel=1e-9, max_evals=3000, profile=profile,
+                                   method="trust-region")
+        assert llt >= lln - 1e-9 * abs(lln)
+        for a, b in zip(tht, thn):
+            assert a == pytest.approx(b, rel=1e-4)
+        assert net < nen, (profile, net, nen)
+
+
+def test_mle_trust_region_bound_active(ctx):
+    n = 400
+    x, y = ex.gen_locations(n, 4)
+    z = oracle.simulate(x, y, (1.0, 0.1, 0.5), si.normals(n, 4))
+    lo, hi = (0.01, 0.01, 0.1), (5.0, 0.05, 2.0)  # the range bound binds (truth 0.1)
+    th, ll, _, _ = ctx.mle(x, y, z, lo, hi, (1.0, 0.02, 0.5), xtol_rel=1e-9, method="trust-region")
+    assert th[1] == pytest.approx(0.05, rel=1e-12)
+    thn, lln, _, _ = ctx.mle(x, y, z, lo, hi, (1.0, 0.02, 0.5), xtol_rel=1e-9)
+    assert ll >= lln - 1e-9 * abs(lln)

@@ -1,6 +1,8 @@
 """Host-side logic of the CUDA path that needs no GPU: the trailing-update tile
 enumeration (SyrkMap: every lower 128-block of the requested column range exactly
-once, pointers consistent with the panel layout), compiled with nvcc as host code."""
+once, pointers consistent with the panel layout), compiled with nvcc as host code; and
+the MLE's quadratic-model trust-region minimiser (trust_region.h) on functions with known
+minimisers (box-active optimum, +inf region, Rosenbrock), compiled with g++."""
 import os
 import shutil
 import subprocess
@@ -21,3 +23,12 @@ def test_syrkmap_enumeration(tmp_path):
     out = subprocess.run([exe], capture_output=True, text=True)
     assert out.returncode == 0, out.stdout + out.stderr
     assert out.stdout.startswith("OK")
+
+
+@pytest.mark.skipif(shutil.which("g++") is None, reason="g++ not available")
+def test_trust_region_minimiser(tmp_path):
+    exe = str(tmp_path / "test_trust_region")
+    subprocess.check_call(["g++", "-O2", "-std=c++17", "-o", exe, os.path.join(ROOT, "tools", "test_trust_region.cpp")])
+    out = subprocess.run([exe], capture_output=True, text=True)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert out.stdout.count(" ok") == 7, out.stdout

@@ -5,8 +5,9 @@ held-out 10%, MSE against the truth.
 
 Field: jittered grid (R1-R3), z = L(theta_true) e by exageo_simulate (Alg. 1); the hold-out
 set is the m = n/10 sites with the smallest keys of the SplitMix64 hold-out substream
-(synth_inputs.holdout_mask). The MLE is exageo_mle_profile (theta1 in closed form; --full for
-the 3-D search) from the geometric midpoint of the bounds; prediction is exageo_predict at
+(synth_inputs.holdout_mask). The MLE profiles theta1 out (--full: 3-D search) and uses the
+quadratic-model trust region (--method nelder-mead for the simplex search) from the geometric
+midpoint of the bounds; prediction is exageo_predict at
 theta_hat and, for reference, at theta_true. Configs[4] names 8 GPUs; at n = 160k the
 observed 144k x 144k lower triangle (83 GB) fits one B200, so this runs on one.
 """
@@ -31,7 +32,8 @@ def main():
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--max-evals", type=int, default=60)
     ap.add_argument("--xtol", type=float, default=1e-3)
-    ap.add_argument("--full", action="store_true", help="3-D search (exageo_mle) instead of the profiled one")
+    ap.add_argument("--full", action="store_true", help="3-D search instead of the profiled one")
+    ap.add_argument("--method", default="trust-region", choices=["trust-region", "nelder-mead"])
     a = ap.parse_args()
     theta_true = (1.0, 0.1, 0.5)
     lo, hi = (0.01, 0.01, 0.1), (5.0, 2.0, 2.0)
@@ -39,7 +41,7 @@ def main():
     n, m = a.n, a.n // 10
     out = {"config": "BASELINE configs[4] (1 GPU)", "n": n, "m_holdout": m, "theta_true": theta_true,
            "bounds": [lo, hi], "start": start, "xtol_rel": a.xtol, "max_evals": a.max_evals,
-           "search": "exageo_mle" if a.full else "exageo_mle_profile"}
+           "search": ("3-D" if a.full else "theta1 profiled") + " / " + a.method}
     x, y = ex.gen_locations(n, a.seed)
     with ex.Context(device=0) as c:
         t0 = time.perf_counter()
@@ -49,7 +51,7 @@ def main():
         xo, yo, zo = x[~hold], y[~hold], z[~hold]
         t0 = time.perf_counter()
         th, ll, ne, trace = c.mle(xo, yo, zo, lo, hi, start, xtol_rel=a.xtol, max_evals=a.max_evals,
-                                  profile=not a.full)
+                                  profile=not a.full, method=a.method)
         sec = time.perf_counter() - t0
         out.update({"theta_hat": th, "loglik": ll, "evals": ne, "mle_s": sec, "s_per_eval": sec / max(ne, 1),
                     "budget_exhausted": ne >= a.max_evals, "trace": trace.tolist()})
