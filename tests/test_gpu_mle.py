@@ -3,6 +3,7 @@ against the ORACLE's estimate (tests/golden/mle_n400.json, written by
 tools/make_golden_mle.py from oracle.mle) within 1e-4 relative (BASELINE north_star), and
 the stationarity pins evaluated with the oracle: profile identity in theta1 and
 coordinate-wise local maximum; BASELINE configs[1] (n = 1600, nu in {0.5, 1.0})."""
+import ctypes
 import json
 import math
 import os
@@ -87,6 +88,18 @@ def test_mle_invalid_bounds(ctx):
     with pytest.raises(ex.ExageoError) as ei:
         ctx.mle([0.1, 0.2], [0.1, 0.3], [1.0, 2.0], (1, 1, 1), (0.5, 2, 2), (1, 1, 1))
     assert ei.value.status == ex.EINVAL
+    with pytest.raises(ex.ExageoError) as ei:
+        ctx.mle([0.1, 0.2], [0.1, 0.3], [1.0, 2.0], (1, 1, 1), (2, 2, 2), (1, 1, 1), method="trust-region",
+                max_evals=0)
+    assert ei.value.status == ex.EINVAL
+    o = ex.MleOpts(1e-6, 10, 0, 7)  # unknown method
+    th, ll, ne = ex.Theta(), ctypes.c_double(), ctypes.c_int()
+    lo, hi, st = ex.Theta(1, 1, 1), ex.Theta(2, 2, 2), ex.Theta(1, 1, 1)
+    xs = np.array([0.1, 0.2])
+    rc = ctx._lib.exageo_mle_ex(ctx._ctx, 2, ex._p(xs), ex._p(xs), ex._p(xs), ctypes.byref(lo), ctypes.byref(hi),
+                                ctypes.byref(st), ctypes.byref(o), ctypes.byref(th), ctypes.byref(ll),
+                                ctypes.byref(ne), None)
+    assert rc == ex.EINVAL
 
 
 def test_mle_profile_matches_oracle_estimate(ctx):
