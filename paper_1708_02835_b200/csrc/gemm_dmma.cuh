@@ -163,11 +163,10 @@ struct SyrkMap {
   }
 };
 
-template <int BM_, int BN_, int BK_, int WARPS_M_, int WARPS_N_, int STAGES_, int MINB_, bool XPF_ = false>
+template <int BM_, int BN_, int BK_, int WARPS_M_, int WARPS_N_, int STAGES_, int MINB_>
 struct Cfg {
   static constexpr int BM = BM_, BN = BN_, BK = BK_, WARPS_M = WARPS_M_, WARPS_N = WARPS_N_, STAGES = STAGES_,
                        MINB = MINB_;
-  static constexpr bool XPF = XPF_;  // cross-stage fragment pipelining (see gemm_nt_dmma)
   static constexpr int NT = WARPS_M * WARPS_N * 32;
   static constexpr int LDA_S = BM + 4, LDB_S = BN + 4;  // = 4 (mod 16) doubles
   static constexpr int SMEM = STAGES * BK * (LDA_S + LDB_S) * (int)sizeof(double);
@@ -242,52 +241,6 @@ __global__ void __launch_bounds__(C::NT, C::MINB) gemm_nt_dmma(Map map, const in
         }
       }
 
-  if constexpr (C::XPF) {
-    // Cross-stage fragment pipelining: the fragments of k-step g+1 are loaded before the
-    // DMMAs of step g; the barrier for stage kt+1 sits before the last k-step of stage kt,
-    // so the first LDS of a stage never waits behind a barrier.
-    constexpr int KS = BK / 4;
-    static_assert(KS % 2 == 0, "XPF needs an even number of k4 steps per stage");
-    double af[2][MI], bf[2][NI];
-    auto frag = [&](int buf, int kt, int kk) {
-      const double* a_s = sA + (kt % STAGES) * BK * LDA_S + wm * WM + fr + (kk * 4 + fk) * LDA_S;
-      const double* b_s = sB + (kt % STAGES) * BK * LDB_S + wn * WN + fr + (kk * 4 + fk) * LDB_S;
-#pragma unroll
-      for (int i = 0; i < MI; ++i) af[buf][i] = LOADC ? -a_s[i * 8] : a_s[i * 8];
-#pragma unroll
-      for (int j = 0; j < NI; ++j) bf[buf][j] = b_s[j * 8];
-    };
-    cp_async_wait<STAGES - 2>();
-    __syncthreads();
-    {
-      const int nk = STAGES - 1;
-      if (nk < KT) load_stage(nk % STAGES, nk);
-      cp_async_commit();
-    }
-    frag(0, 0, 0);
-    for (int kt = 0; kt < KT; ++kt) {
-#pragma unroll
-      for (int kk = 0; kk < KS; ++kk) {
-        const int cur = kk & 1;
-        if (kk == KS - 1) {
-          if (kt + 1 < KT) {
-            cp_async_wait<STAGES - 2>();
-            __syncthreads();  // every warp holds its step-(kt, last) fragments: slot kt is free
-            const int nk = kt + STAGES;
-            if (nk < KT) load_stage(nk % STAGES, nk);
-            cp_async_commit();
-            frag(cur ^ 1, kt + 1, 0);
-          }
-        } else {
-          frag(cur ^ 1, kt, kk + 1);
-        }
-#pragma unroll
-        for (int i = 0; i < MI; ++i)
-#pragma unroll
-          for (int j = 0; j < NI; ++j) dmma(acc[i][j], af[cur][i], bf[cur][j]);
-      }
-    }
-  } else
   for (int kt = 0; kt < KT; ++kt) {
     if (ACC && !LOADC && kt == KT / 2) {
       // pull this tile's C into L2 ahead of the read-modify-write epilogue (128-byte lines)
@@ -340,164 +293,13 @@ __global__ void __launch_bounds__(C::NT, C::MINB) gemm_nt_dmma(Map map, const in
   }
 }
 
-// ---- barrier-free variant: bulk copies (cp.async.bulk, the TMA engine's 1-D path)
-// completing on per-stage "full" mbarriers, per-warp "empty" arrivals releasing a
-// stage; thread 0 of warp 0 doubles as the producer. No CTA-wide barrier in the loop:
-// each warp proceeds as soon as its stage has landed.
-__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(b)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(b)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred P1;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-      "@!P1 bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(b)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-                   smem_u32(dst)),
-               "l"(src), "r"(bytes), "r"(smem_u32(bar))
-               : "memory");
-}
-
-template <class C>
-constexpr int smem_bulk() {
-  return C::SMEM + 2 * C::STAGES * (int)sizeof(uint64_t);
-}
-
-template <class C, bool ACC, class Map>
-__global__ void __launch_bounds__(C::NT, C::MINB) gemm_nt_dmma_bulk(Map map, const int* __restrict__ info) {
-  constexpr int BM = C::BM, BN = C::BN, BK = C::BK, STAGES = C::STAGES;
-  constexpr int LDA_S = C::LDA_S, LDB_S = C::LDB_S;
-  constexpr int WM = BM / C::WARPS_M, WN = BN / C::WARPS_N;
-  constexpr int MI = WM / 8, NI = WN / 8;
-  constexpr int NWARPS = C::WARPS_M * C::WARPS_N;
-  constexpr unsigned STAGE_BYTES = BK * (BM + BN) * sizeof(double);
-
-  GemmTile t;
-  if (!map.template operator()<BM, BN>((int64_t)blockIdx.x, t)) return;
-
-  extern __shared__ __align__(16) double smem[];
-  double* sA = smem;
-  double* sB = smem + STAGES * BK * LDA_S;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * BK * (LDA_S + LDB_S));
-  uint64_t* empty = full + STAGES;
-
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = warp % C::WARPS_M, wn = warp / C::WARPS_M;
-  const int KT = t.K / BK;
-
-  if (tid == 0) {
-    for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], NWARPS);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  }
-  __syncthreads();
-
-  auto issue = [&](int kt) {  // thread 0 only
-    const int s = kt % STAGES;
-    mbar_expect_tx(&full[s], STAGE_BYTES);
-    double* a_s = sA + s * BK * LDA_S;
-    double* b_s = sB + s * BK * LDB_S;
-#pragma unroll
-    for (int col = 0; col < BK; ++col) {
-      bulk_g2s(a_s + col * LDA_S, t.A + (int64_t)(kt * BK + col) * t.lda, BM * sizeof(double), &full[s]);
-      bulk_g2s(b_s + col * LDB_S, t.B + (int64_t)(kt * BK + col) * t.ldb, BN * sizeof(double), &full[s]);
-    }
-  };
-  if (tid == 0)
-    for (int kt = 0; kt < STAGES - 1 && kt < KT; ++kt) issue(kt);
-  if (info != nullptr && *(volatile const int*)info != 0) {
-    // drain the issued copies before the CTA exits
-    for (int kt = 0; kt < STAGES - 1 && kt < KT; ++kt) mbar_wait(&full[kt], 0);
-    return;
-  }
-
-  double acc[MI][NI][2];
-#pragma unroll
-  for (int i = 0; i < MI; ++i)
-#pragma unroll
-    for (int j = 0; j < NI; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-
-  const int fr = lane >> 2, fk = lane & 3;
-  for (int kt = 0; kt < KT; ++kt) {
-    if (ACC && kt == KT / 2) {
-      constexpr int LPC = BM / 16;
-      for (int l = tid; l < BN * LPC; l += C::NT) {
-        const double* p = t.C + (int64_t)(l / LPC) * t.ldc + (l % LPC) * 16;
-        asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p));
-      }
-    }
-    if (warp == 0) {  // producer duty: refill the stage released at kt - 1
-      const int nk = kt + STAGES - 1;
-      if (nk < KT) {
-        if (nk >= STAGES) mbar_wait(&empty[nk % STAGES], ((nk / STAGES) - 1) & 1);
-        if (lane == 0) issue(nk);
-      }
-      __syncwarp();
-    }
-    const int s = kt % STAGES;
-    mbar_wait(&full[s], (kt / STAGES) & 1);
-    const double* a_s = sA + s * BK * LDA_S + wm * WM + fr;
-    const double* b_s = sB + s * BK * LDB_S + wn * WN + fr;
-#pragma unroll
-    for (int kk = 0; kk < BK; kk += 4) {
-      double af[MI], bf[NI];
-#pragma unroll
-      for (int i = 0; i < MI; ++i) af[i] = a_s[(kk + fk) * LDA_S + i * 8];
-#pragma unroll
-      for (int j = 0; j < NI; ++j) bf[j] = b_s[(kk + fk) * LDB_S + j * 8];
-#pragma unroll
-      for (int i = 0; i < MI; ++i)
-#pragma unroll
-        for (int j = 0; j < NI; ++j) dmma(acc[i][j], af[i], bf[j]);
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
-  }
-  if (!ACC) __syncthreads();  // C may alias A: every warp must be done before any write
-
-#pragma unroll
-  for (int i = 0; i < MI; ++i) {
-    const int r = wm * WM + i * 8 + fr;
-    if (r >= t.m_valid) continue;
-#pragma unroll
-    for (int j = 0; j < NI; ++j) {
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int c = wn * WN + j * 8 + fk * 2 + e;
-        if (c >= t.n_valid) continue;
-        double* p = t.C + (int64_t)c * t.ldc + r;
-        if (ACC) *p = *p - acc[i][j][e];
-        else *p = acc[i][j][e];
-      }
-    }
-  }
-}
-
 template <class C, bool ACC, class Map>
 cudaError_t set_smem() {
   cudaError_t e =
       cudaFuncSetAttribute(gemm_nt_dmma<C, ACC, Map>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(gemm_nt_dmma<C, ACC, Map, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-  if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(gemm_nt_dmma_bulk<C, ACC, Map>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              smem_bulk<C>());
+  return cudaFuncSetAttribute(gemm_nt_dmma<C, ACC, Map, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              C::SMEM);
 }
 
 template <class C, bool ACC, class Map, bool PRE = false>
@@ -505,13 +307,6 @@ void launch(const Map& map, const int* info, cudaStream_t s) {
   const int64_t nblk = map.blocks(C::BM, C::BN);
   if (nblk <= 0) return;
   gemm_nt_dmma<C, ACC, Map, PRE><<<(unsigned)nblk, C::NT, C::SMEM, s>>>(map, info);
-}
-
-template <class C, bool ACC, class Map>
-void launch_bulk(const Map& map, const int* info, cudaStream_t s) {
-  const int64_t nblk = map.blocks(C::BM, C::BN);
-  if (nblk <= 0) return;
-  gemm_nt_dmma_bulk<C, ACC, Map><<<(unsigned)nblk, C::NT, smem_bulk<C>(), s>>>(map, info);
 }
 
 }  // namespace gemm

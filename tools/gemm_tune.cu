@@ -1,7 +1,9 @@
 // gemm_tune.cu -- timing harness for DMMA contraction configurations (development tool).
 // Times the step-k bulk trailing update U2(k) (SyrkMap over panels k+2 .. T-1) on a
-// synthetic panel workspace, for the cp.async+barrier kernel and the bulk-copy+mbarrier
-// kernel. Reports algorithmic TFLOP/s (the true lower triangle incl. the z row).
+// synthetic panel workspace for several tile configurations of the product kernel.
+// Reports algorithmic TFLOP/s (the true lower triangle incl. the z row). (A bulk-copy +
+// mbarrier variant and cross-stage fragment pipelining were measured in earlier revisions
+// of gemm_dmma.cuh: 29.7 and 31.7-32.5 TF.)
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I paper_1708_02835_b200/csrc \
 //        -o tools/gemm_tune tools/gemm_tune.cu
 #include <cstdio>
@@ -37,8 +39,7 @@ void run(const char* name, const Layout& L, double* ws, int k, int reps) {
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   auto go = [&]() {
-    if (BULK == 1) launch_bulk<C, true>(map, nullptr, 0);
-    else if (BULK == 2) launch<C, true, SyrkMap, true>(map, nullptr, 0);
+    if (BULK == 2) launch<C, true, SyrkMap, true>(map, nullptr, 0);
     else launch<C, true>(map, nullptr, 0);
   };
   go();
@@ -55,7 +56,7 @@ void run(const char* name, const Layout& L, double* ws, int k, int reps) {
     tot += ms;
   }
   cudaError_t err = cudaGetLastError();
-  printf("%-44s %s k=%3d blocks=%8lld best %8.3f ms  %6.2f TF  (avg %6.2f TF) %s\n", name, BULK == 1 ? "bulk " : (BULK == 2 ? "preC " : "cpasy"),
+  printf("%-44s %s k=%3d blocks=%8lld best %8.3f ms  %6.2f TF  (avg %6.2f TF) %s\n", name, BULK == 2 ? "preC " : "cpasy",
          k, (long long)map.blocks(C::BM, C::BN), best, flops / best / 1e9, flops / (tot / reps) / 1e9,
          err == cudaSuccess ? "" : cudaGetErrorString(err));
 }
