@@ -233,6 +233,17 @@ exageo_status exageo_predict(exageo_ctx* ctx, const exageo_theta* theta, int64_t
                              const double* y, const double* z, int64_t m, const double* xnew, const double* ynew,
                              double* znew);
 
+/* exageo_predict plus the kriging (conditional) variance of every new site,
+ *   var_i = theta1 - sigma_i^T Sigma22^{-1} sigma_i = theta1 - ||L^{-1} sigma_i||^2,
+ * sigma_i = Sigma21[:, i] (the simple-kriging variance belonging to Eq. (5)),
+ * from the same factor: batches of new sites, Sigma21 generated on the GPU, a blocked
+ * multi-right-hand-side forward solve with L (diagonal-tile substitution + DMMA update of
+ * the rows below), column sums of squares. var: host array of m doubles. Work ~ n^2 m flop.
+ * Single-rank contexts only (EXAGEO_EINVAL with world > 1 or virtual ranks). */
+exageo_status exageo_predict_var(exageo_ctx* ctx, const exageo_theta* theta, int64_t n, const double* x,
+                                 const double* y, const double* z, int64_t m, const double* xnew,
+                                 const double* ynew, double* znew, double* var);
+
 /* --- Stage-level entry points (same kernels as exageo_loglik_dev, exposed
  *     so that each step of Alg. 2 can be checked on its own). ---------- */
 

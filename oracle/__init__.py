@@ -208,6 +208,19 @@ def predict(x, y, z, xnew, ynew, theta) -> np.ndarray:
     return out
 
 
+def predict_var(x, y, xnew, ynew, theta) -> np.ndarray:
+    """Simple-kriging (conditional) variance of Eq. (5)'s predictor at each new site,
+    var_i = C(0) - sigma_i^T Sigma22^{-1} sigma_i with sigma_i = Sigma21[:, i],
+    as theta1 - ||L^{-1} sigma_i||^2 by the oracle's own Cholesky and forward substitution."""
+    L = cholesky(cov(x, y, x, y, theta))
+    S = cov(x, y, xnew, ynew, theta)  # n x m
+    out = np.empty(S.shape[1])
+    for i in range(S.shape[1]):
+        w = forward(L, S[:, i])
+        out[i] = float(theta[0]) - float(w @ w)
+    return out
+
+
 def num_threads() -> int:
     return int(lib().oracle_num_threads())
 

@@ -80,6 +80,8 @@ SIGNATURES = [
     ("exageo_read_lower", ctypes.c_int, [_C, _f64p, ctypes.c_int64]),
     ("exageo_read_zrow", ctypes.c_int, [_C, _f64p]),
     ("exageo_read_entries", ctypes.c_int, [_C, ctypes.c_int64, _i64p, _i64p, _f64p]),
+    ("exageo_predict_var", ctypes.c_int, [_C, ctypes.POINTER(Theta), ctypes.c_int64, _f64p, _f64p, _f64p,
+                                          ctypes.c_int64, _f64p, _f64p, _f64p, _f64p]),
     ("exageo_predict", ctypes.c_int, [_C, ctypes.POINTER(Theta), ctypes.c_int64, _f64p, _f64p, _f64p, ctypes.c_int64,
                                       _f64p, _f64p, _f64p]),
     ("exageo_mle", ctypes.c_int, [_C, ctypes.c_int64, _f64p, _f64p, _f64p, ctypes.POINTER(Theta),
@@ -319,6 +321,16 @@ class Context:
         self._check(self._lib.exageo_predict(self._ctx, ctypes.byref(t), z.size, _p(x), _p(y), _p(z), xnew.size,
                                              _p(xnew), _p(ynew), _p(out)))
         return out
+
+    def predict_var(self, x, y, z, xnew, ynew, theta):
+        """Kriging mean and variance at (xnew, ynew) (exageo_predict_var): (znew, var)."""
+        x, y, z, xnew, ynew = _f(x), _f(y), _f(z), _f(xnew), _f(ynew)
+        out = np.empty(xnew.size, np.float64)
+        var = np.empty(xnew.size, np.float64)
+        t = _theta(theta)
+        self._check(self._lib.exageo_predict_var(self._ctx, ctypes.byref(t), z.size, _p(x), _p(y), _p(z), xnew.size,
+                                                 _p(xnew), _p(ynew), _p(out), _p(var)))
+        return out, var
 
     def simulate(self, x, y, e, theta) -> np.ndarray:
         """Alg. 1: z = L(theta) e for given normal variates e."""

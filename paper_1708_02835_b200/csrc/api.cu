@@ -1021,6 +1021,64 @@ exageo_status exageo_predict(exageo_ctx* c, const exageo_theta* t, int64_t n, co
   return EXAGEO_OK;
 }
 
+exageo_status exageo_predict_var(exageo_ctx* c, const exageo_theta* t, int64_t n, const double* x, const double* y,
+                                 const double* z, int64_t m, const double* xnew, const double* ynew, double* znew,
+                                 double* var) {
+  if (!c) return fail(nullptr, EXAGEO_EINVAL, "NULL ctx");
+  if (!var) return fail(c, EXAGEO_EINVAL, "NULL var");
+  if (c->world != 1 || c->virt) return fail(c, EXAGEO_EINVAL, "the kriging variance needs a single-rank context");
+  // mean (Eq. 5) -- leaves L of Sigma22 in the workspace
+  exageo_status st = exageo_predict(c, t, n, x, y, z, m, xnew, ynew, znew);
+  if (st != EXAGEO_OK) return st;
+  // var_i = theta1 - sigma_i^T Sigma22^{-1} sigma_i = theta1 - ||L^{-1} sigma_i||^2, sigma_i = Sigma21[:, i]:
+  // batches of mc new sites, S = Sigma21 (N x mc, identity padding rows zero), forward solve
+  // panel by panel (diagonal tile substitution, then the DMMA update of the rows below).
+  const Layout& G = c->G;
+  RankState& R = c->rs[0];
+  const int64_t N = G.N;
+  const int nb = G.nb;
+  int64_t mc = std::max<int64_t>(64, ((int64_t)2 << 30) / (8 * N) / 64 * 64);  // <= 2 GB per batch
+  mc = std::min<int64_t>(mc, (m + 63) / 64 * 64);
+  const size_t total = 2 * (size_t)n + 2 * (size_t)mc + (size_t)N * mc + (size_t)mc * nb + (size_t)mc;
+  double* d = nullptr;
+  CUDA_TRY(c, cudaMalloc(&d, sizeof(double) * total));
+  struct Free {
+    double* p;
+    ~Free() { cudaFree(p); }
+  } guard{d};
+  double *dx = d, *dy = dx + n, *dxn = dy + n, *dyn = dxn + mc, *S = dyn + mc, *Bt = S + (size_t)N * mc,
+         *dv = Bt + (size_t)mc * nb;
+  CUDA_TRY(c, cudaMemcpyAsync(dx, x, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(c, cudaMemcpyAsync(dy, y, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
+  const MaternConsts mc_consts = make_consts(*t, c);
+  for (int64_t i0 = 0; i0 < m; i0 += mc) {
+    const int cols = (int)std::min<int64_t>(mc, m - i0);
+    CUDA_TRY(c, cudaMemcpyAsync(dxn, xnew + i0, sizeof(double) * cols, cudaMemcpyHostToDevice, c->stream));
+    CUDA_TRY(c, cudaMemcpyAsync(dyn, ynew + i0, sizeof(double) * cols, cudaMemcpyHostToDevice, c->stream));
+    CUDA_TRY(c, cudaMemsetAsync(S, 0, sizeof(double) * (size_t)N * mc, c->stream));
+    launch_matern_dense(mc_consts, n, dx, dy, cols, dxn, dyn, S, N, c->mtab, c->stream);
+    for (int j = 0; j < G.T; ++j) {
+      const double* P = R.ws + R.L.off(j);
+      const int64_t jb = (int64_t)j * nb;
+      launch_diag_solve_cols(P, G.ld(j), nb, S + jb, N, cols, c->stream);
+      const int64_t rows = N - jb - nb;
+      if (rows > 0) {  // S[jb+nb:, :] -= L[jb+nb:, jb:jb+nb] V_j
+        launch_transpose(S + jb, N, nb, (int)mc, Bt, c->stream);
+        launch_gemm_panel(rows, cols, nb, P + nb, G.ld(j), Bt, mc, S + jb + nb, N, true, nullptr, c->stream);
+        c->kernels += 2;
+      }
+      c->kernels += 1;
+    }
+    launch_column_var(S, N, n, cols, t->sigma2, dv, c->stream);
+    c->kernels += 2;
+    st = check_launch(c);
+    if (st != EXAGEO_OK) return st;
+    CUDA_TRY(c, cudaMemcpyAsync(var + i0, dv, sizeof(double) * cols, cudaMemcpyDeviceToHost, c->stream));
+  }
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return EXAGEO_OK;
+}
+
 exageo_status exageo_stage_generate_dev(exageo_ctx* c, const exageo_theta* t, int64_t n, const double* x,
                                         const double* y, const double* z) {
   if (!c) return fail(nullptr, EXAGEO_EINVAL, "NULL ctx");

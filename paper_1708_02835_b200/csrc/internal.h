@@ -143,6 +143,13 @@ void launch_trmv_sum(int64_t n, int64_t N, const double* part, int nparts, doubl
 int trsv_chunks(int64_t rows);
 void launch_backsolve_panel(const double* P, int64_t ld, int nb, int64_t row_after, int64_t rows,
                             const double* w, double* wj, double* part, cudaStream_t s);
+// Kriging variance (trsv.cu): multi-RHS forward solve pieces. diag_solve: S (nb x cols, ld
+// lds) <- L_jj^{-1} S with the panel's diagonal tile; transpose: Bt = S^T (cols x rows);
+// column_var: var_c = theta1 - sum_{k<n} V_kc^2.
+void launch_diag_solve_cols(const double* P, int64_t ld, int nb, double* S, int64_t lds, int cols, cudaStream_t s);
+void launch_transpose(const double* S, int64_t lds, int rows, int cols, double* Bt, cudaStream_t s);
+void launch_column_var(const double* V, int64_t ldv, int64_t n, int cols, double theta1, double* var,
+                       cudaStream_t s);
 // K8 (matern.cu): znew_i = sum_j C(||snew_i - s_j||; theta) w_j (Eq. (5), Alg. 3 l.8), the
 // covariance block Sigma12 generated on the fly and never stored. part: krige_chunks(n) * m.
 int krige_chunks(int64_t n);

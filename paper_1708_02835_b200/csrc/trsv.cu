@@ -91,7 +91,73 @@ __global__ void tile_solve_kernel(const double* __restrict__ P, int64_t ld, int 
   wj[c] = rhs[c];
 }
 
+// ---- multi-right-hand-side forward solve L V = S for the kriging variance (exageo_predict_var)
+// Diagonal block: one CTA per right-hand side (column of S, nb threads), right-looking
+// substitution with the panel's nb x nb diagonal tile (lower part only; its upper part holds
+// unused covariance values).
+__global__ void diag_solve_cols_kernel(const double* __restrict__ P, int64_t ld, int nb, double* __restrict__ S,
+                                       int64_t lds) {
+  extern __shared__ double sv[];
+  double* col = S + (int64_t)blockIdx.x * lds;
+  const int r = threadIdx.x;
+  sv[r] = col[r];
+  __syncthreads();
+  for (int k = 0; k < nb; ++k) {
+    if (r == k) sv[k] = sv[k] / P[(int64_t)k * ld + k];
+    __syncthreads();
+    if (r > k) sv[r] -= P[(int64_t)k * ld + r] * sv[k];
+  }
+  col[r] = sv[r];
+}
+
+// Bt (cols x rows, ld cols) = S (rows x cols, ld lds)^T, 32 x 32 tiles through shared memory.
+__global__ void transpose_kernel(const double* __restrict__ S, int64_t lds, int rows, int cols,
+                                 double* __restrict__ Bt) {
+  __shared__ double t[32][33];
+  const int r0 = blockIdx.x * 32, c0 = blockIdx.y * 32;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int r = r0 + threadIdx.x, c = c0 + i;
+    t[i][threadIdx.x] = (r < rows && c < cols) ? S[(int64_t)c * lds + r] : 0.0;
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int c = c0 + threadIdx.x, r = r0 + i;
+    if (r < rows && c < cols) Bt[(int64_t)r * cols + c] = t[threadIdx.x][i];
+  }
+}
+
+// var_c = theta1 - sum_{k < n} V_kc^2 (fixed-order block tree per column).
+__global__ void __launch_bounds__(256) column_var_kernel(const double* __restrict__ V, int64_t ldv, int64_t n,
+                                                         double theta1, double* __restrict__ var) {
+  __shared__ double red[8];
+  const double* col = V + (int64_t)blockIdx.x * ldv;
+  double a = 0.0;
+  for (int64_t k = threadIdx.x; k < n; k += blockDim.x) a += col[k] * col[k];
+  for (int o = 16; o > 0; o >>= 1) a += __shfl_down_sync(0xffffffffu, a, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = a;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s2 = 0.0;
+    for (int q = 0; q < 8; ++q) s2 += red[q];
+    var[blockIdx.x] = theta1 - s2;
+  }
+}
+
 }  // namespace
+
+void launch_diag_solve_cols(const double* P, int64_t ld, int nb, double* S, int64_t lds, int cols, cudaStream_t s) {
+  diag_solve_cols_kernel<<<cols, nb, nb * sizeof(double), s>>>(P, ld, nb, S, lds);
+}
+
+void launch_transpose(const double* S, int64_t lds, int rows, int cols, double* Bt, cudaStream_t s) {
+  dim3 grid((rows + 31) / 32, (cols + 31) / 32);
+  transpose_kernel<<<grid, dim3(32, 8), 0, s>>>(S, lds, rows, cols, Bt);
+}
+
+void launch_column_var(const double* V, int64_t ldv, int64_t n, int cols, double theta1, double* var,
+                       cudaStream_t s) {
+  column_var_kernel<<<cols, 256, 0, s>>>(V, ldv, n, theta1, var);
+}
 
 int trsv_chunks(int64_t rows) { return rows > 0 ? (int)((rows + kRowChunk - 1) / kRowChunk) : 0; }
 

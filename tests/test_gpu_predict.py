@@ -86,3 +86,28 @@ def test_holdout_mle_and_kriging(ctx):
     ref = oracle.predict(x[~hold], y[~hold], z[~hold], x[hold], y[hold], th)
     assert np.abs(pred - ref).max() <= 1e-9
     assert mse < 0.5 * float(np.var(z))  # kriging beats the prior mean by a wide margin
+
+
+@pytest.mark.parametrize("n,m,nb,theta", [(800, 100, 128, (1.0, 0.1, 0.5)), (1500, 37, 256, (1.4, 0.07, 1.2)),
+                                          (333, 5, 128, (0.8, 0.2, 2.5))])
+def test_predict_var_matches_oracle(n, m, nb, theta):
+    x, y = ex.gen_locations(n, 21)
+    z = oracle.simulate(x, y, (1.0, 0.1, 0.5), si.normals(n, 22))
+    rng = np.random.default_rng(n)
+    xn = np.concatenate([rng.random(m - 2), [x[3], 50.0]])  # includes an observed and a far site
+    yn = np.concatenate([rng.random(m - 2), [y[3], 50.0]])
+    with ex.Context(device=0, nb=nb) as c:
+        mean, var = c.predict_var(x, y, z, xn, yn, theta)
+        np.testing.assert_array_equal(mean, c.predict(x, y, z, xn, yn, theta))
+    ref = oracle.predict_var(x, y, xn, yn, theta)
+    assert np.abs(var - ref).max() <= 1e-9 * theta[0]
+    assert abs(var[-2]) <= 1e-9 * theta[0] and var[-1] == theta[0]
+    assert np.all(var >= -1e-9) and np.all(var <= theta[0])
+
+
+def test_predict_var_rejects_distributed():
+    x, y = ex.gen_locations(200, 1)
+    with ex.Context(device=0, virtual_ranks=2) as c:
+        with pytest.raises(ex.ExageoError) as ei:
+            c.predict_var(x, y, np.ones(200), [0.5], [0.5], (1.0, 0.1, 0.5))
+        assert ei.value.status == ex.EINVAL

@@ -198,3 +198,25 @@ def test_predict_kriging():
     # far away -> prior mean 0
     far = oracle.predict(x, y, z, [1e4], [1e4], theta)
     assert far[0] == 0.0
+
+
+def test_predict_var_pins():
+    # oracle.predict_var: simple-kriging variance C(0) - sigma^T Sigma^{-1} sigma
+    theta = (1.3, 0.1, 0.8)
+    # n = 1: closed form theta1 - C(r)^2 / theta1
+    x, y = np.array([0.2]), np.array([0.3])
+    xn, yn = np.array([0.25, 0.9]), np.array([0.31, 0.1])
+    got = oracle.predict_var(x, y, xn, yn, theta)
+    for i in range(2):
+        c = oracle.matern(math.hypot(xn[i] - 0.2, yn[i] - 0.3), theta)
+        assert got[i] == pytest.approx(theta[0] - c * c / theta[0], rel=1e-13)
+    # brute force with numpy's dense solve (independent of the oracle's Cholesky)
+    xs, ys = oracle.gen_locations(30, 3)
+    xn, yn = np.array([0.5, 0.01, 0.77]), np.array([0.5, 0.99, 0.2])
+    S22 = oracle.cov(xs, ys, xs, ys, theta)
+    s = oracle.cov(xs, ys, xn, yn, theta)
+    ref = theta[0] - np.einsum("ij,ij->j", s, np.linalg.solve(S22, s))
+    np.testing.assert_allclose(oracle.predict_var(xs, ys, xn, yn, theta), ref, rtol=1e-9, atol=1e-12)
+    # an observed site has zero variance; a far site has the prior variance theta1
+    v = oracle.predict_var(xs, ys, [xs[4], 1e4], [ys[4], 1e4], theta)
+    assert abs(v[0]) < 1e-10 and v[1] == theta[0]
