@@ -17,7 +17,7 @@ for n, m in [(20000, 2000), (60000, 4000)]:
     rng = np.random.default_rng(0)
     xn, yn = rng.random(m), rng.random(m)
     with ex.Context(device=0) as c:
-        c.predict(x, y, z, xn[:10], yn[:10], TH)
+        c.predict_var(x, y, z, xn[:10], yn[:10], TH)  # warm-up (module loading, allocations)
         t0 = time.perf_counter()
         mean = c.predict(x, y, z, xn, yn, TH)
         t1 = time.perf_counter()
