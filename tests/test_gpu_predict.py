@@ -86,6 +86,10 @@ def test_holdout_mle_and_kriging(ctx):
     ref = oracle.predict(x[~hold], y[~hold], z[~hold], x[hold], y[hold], th)
     assert np.abs(pred - ref).max() <= 1e-9
     assert mse < 0.5 * float(np.var(z))  # kriging beats the prior mean by a wide margin
+    # the expected MSE (1/m) tr(Sigma11 - Sigma12 Sigma22^-1 Sigma21) = mean kriging variance
+    # agrees with the realised MSE to sampling accuracy (m = 160 correlated sites)
+    _, var = ctx.predict_var(x[~hold], y[~hold], z[~hold], x[hold], y[hold], th)
+    assert 0.5 < mse / float(np.mean(var)) < 2.0
 
 
 @pytest.mark.parametrize("n,m,nb,theta", [(800, 100, 128, (1.0, 0.1, 0.5)), (1500, 37, 256, (1.4, 0.07, 1.2)),
