@@ -101,11 +101,14 @@ __global__ void diag_solve_cols_kernel(const double* __restrict__ P, int64_t ld,
   double* col = S + (int64_t)blockIdx.x * lds;
   const int r = threadIdx.x;
   sv[r] = col[r];
+  double lk = P[r];  // L_r0; the next column's entry is loaded one step ahead (L2 latency off the chain)
   __syncthreads();
   for (int k = 0; k < nb; ++k) {
-    if (r == k) sv[k] = sv[k] / P[(int64_t)k * ld + k];
+    const double lnext = (k + 1 < nb) ? P[(int64_t)(k + 1) * ld + r] : 0.0;
+    if (r == k) sv[k] = sv[k] / lk;
     __syncthreads();
-    if (r > k) sv[r] -= P[(int64_t)k * ld + r] * sv[k];
+    if (r > k) sv[r] -= lk * sv[k];
+    lk = lnext;
   }
   col[r] = sv[r];
 }
