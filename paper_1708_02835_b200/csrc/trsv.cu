@@ -92,25 +92,38 @@ __global__ void tile_solve_kernel(const double* __restrict__ P, int64_t ld, int 
 }
 
 // ---- multi-right-hand-side forward solve L V = S for the kriging variance (exageo_predict_var)
-// Diagonal block: one CTA per right-hand side (column of S, nb threads), right-looking
-// substitution with the panel's nb x nb diagonal tile (lower part only; its upper part holds
-// unused covariance values).
+// Diagonal block: one CTA per kRhs right-hand sides (columns of S, nb threads: thread r owns
+// row r of each), right-looking substitution with the panel's nb x nb diagonal tile (lower
+// part only; its upper part holds unused covariance values). Each loaded L_rk serves kRhs
+// columns; the next column's entry is loaded one step ahead (L2 latency off the chain).
+constexpr int kRhs = 4;
 __global__ void diag_solve_cols_kernel(const double* __restrict__ P, int64_t ld, int nb, double* __restrict__ S,
-                                       int64_t lds) {
-  extern __shared__ double sv[];
-  double* col = S + (int64_t)blockIdx.x * lds;
-  const int r = threadIdx.x;
-  sv[r] = col[r];
-  double lk = P[r];  // L_r0; the next column's entry is loaded one step ahead (L2 latency off the chain)
-  __syncthreads();
+                                       int64_t lds, int cols) {
+  extern __shared__ double sv[];  // [kRhs][nb]
+  const int r = threadIdx.x, c0 = blockIdx.x * kRhs;
+  double v[kRhs];
+#pragma unroll
+  for (int q = 0; q < kRhs; ++q) v[q] = (c0 + q < cols) ? S[(int64_t)(c0 + q) * lds + r] : 0.0;
+  double lk = P[r];
   for (int k = 0; k < nb; ++k) {
     const double lnext = (k + 1 < nb) ? P[(int64_t)(k + 1) * ld + r] : 0.0;
-    if (r == k) sv[k] = sv[k] / lk;
+    if (r == k) {
+#pragma unroll
+      for (int q = 0; q < kRhs; ++q) {
+        v[q] = v[q] / lk;
+        sv[q * nb + k] = v[q];
+      }
+    }
     __syncthreads();
-    if (r > k) sv[r] -= lk * sv[k];
+    if (r > k) {
+#pragma unroll
+      for (int q = 0; q < kRhs; ++q) v[q] -= lk * sv[q * nb + k];
+    }
     lk = lnext;
   }
-  col[r] = sv[r];
+#pragma unroll
+  for (int q = 0; q < kRhs; ++q)
+    if (c0 + q < cols) S[(int64_t)(c0 + q) * lds + r] = v[q];
 }
 
 // Bt (cols x rows, ld cols) = S (rows x cols, ld lds)^T, 32 x 32 tiles through shared memory.
@@ -149,7 +162,7 @@ __global__ void __launch_bounds__(256) column_var_kernel(const double* __restric
 }  // namespace
 
 void launch_diag_solve_cols(const double* P, int64_t ld, int nb, double* S, int64_t lds, int cols, cudaStream_t s) {
-  diag_solve_cols_kernel<<<cols, nb, nb * sizeof(double), s>>>(P, ld, nb, S, lds);
+  diag_solve_cols_kernel<<<(cols + kRhs - 1) / kRhs, nb, kRhs * nb * sizeof(double), s>>>(P, ld, nb, S, lds, cols);
 }
 
 void launch_transpose(const double* S, int64_t lds, int rows, int cols, double* Bt, cudaStream_t s) {
