@@ -3,6 +3,7 @@
 // step j, the SM clock at: A = after the barrier (thread of row j+1, slot owner of column
 // j+1), B = after its f = a_rj / d_j, C = after its slot loop, and D = thread 0 after the
 // barrier.
+#include <cmath>
 #include <cstdio>
 #include <vector>
 
@@ -313,6 +314,146 @@ __global__ void __launch_bounds__(256) potrf_2d3(double* __restrict__ a, int64_t
   }
 }
 
+
+// Factor-only step loop (no W bookkeeping on the pivot chain) + W = L^{-1} afterwards by
+// blocked inversion: 16 x 16 diagonal blocks by per-lane substitution, off-diagonal blocks
+// W_IJ = -W_II sum_K L~_IK W_KJ in three distance levels (256 threads, one entry each).
+__device__ double g_W4[64 * 64];
+__device__ long long g_ph[6];
+__global__ void __launch_bounds__(256) potrf_2d4(double* __restrict__ a, int64_t lda) {
+  extern __shared__ double smem_p[];
+  double* colA = smem_p;                 // 64 x 65
+  double* Wt = smem_p + PB * LDS_P;      // 64 x 65: Wt[c * 65 + r] = w~_rc
+  double* dummy = smem_p + 2 * PB * LDS_P;  // 4 x 256
+  double* Xs = dummy + 4 * 256;          // 3 x 256
+  double* Ls = Xs + 3 * 256;             // 64 x 65: scaled L~_rc = colA[c][r] / d_c (r > c)
+  __shared__ double rdv[PB], ilj[PB], lj[PB];
+  const int tid = threadIdx.x, tr = tid >> 4, tc = tid & 15;
+  if (tid == 0) g_ph[0] = clock64();
+  double v[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int r = tr + 16 * i, c = tc + 16 * k;
+      v[i][k] = (c <= r) ? a[(int64_t)c * lda + r] : 0.0;
+    }
+  __syncthreads();
+  if (tc == 0) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) colA[tr + 16 * i] = v[i][0];
+  }
+  int bad = -1;
+  __syncthreads();
+  if (tid == 0) g_ph[1] = clock64();
+  for (int j = 0; j < PB; ++j) {
+    __syncthreads();
+    const double* cj = colA + j * LDS_P;
+    const double d = cj[j];
+    if (!(d > 0.0)) {
+      bad = j;
+      break;
+    }
+    const double rd = __drcp_rn(d);
+    double f[4], src[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) f[i] = (tr + 16 * i > j) ? cj[tr + 16 * i] * rd : 0.0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) src[k] = cj[tc + 16 * k];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) v[i][k] = fma(-f[i], src[k], v[i][k]);
+    const int j1 = j + 1;
+    if (j1 < PB) {
+      const int k1 = j1 >> 4;
+      const bool pub = tc == (j1 & 15);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        double cv = v[i][0];
+#pragma unroll
+        for (int kk = 1; kk < 4; ++kk) cv = (kk == k1) ? v[i][kk] : cv;
+        double* dst = pub ? &colA[j1 * LDS_P + tr + 16 * i] : &dummy[i * 256 + tid];
+        *dst = cv;
+      }
+    }
+  }
+  if (bad >= 0) return;
+  __syncthreads();
+  if (tid == 0) g_ph[2] = clock64();
+  if (tid < PB) {
+    const double dj = colA[tid * LDS_P + tid];
+    rdv[tid] = __drcp_rn(dj);
+    lj[tid] = sqrt(dj);
+    ilj[tid] = 1.0 / lj[tid];
+  }
+  __syncthreads();
+  for (int idx = tid; idx < PB * PB; idx += 256) {
+    const int rr = idx & 63, c = idx >> 6;
+    Ls[c * LDS_P + rr] = (rr > c) ? colA[c * LDS_P + rr] * rdv[c] : 0.0;
+  }
+  __syncthreads();
+  // A: diagonal 16 x 16 blocks of w~ = L~^{-1}, L~_rc = colA[c][r] / d_c; warp I, lane c
+  {
+    const int I = tid >> 5, c = tid & 31;
+    if (I < 4 && c < 16) {
+      const int b = 16 * I;
+      double w[16];
+#pragma unroll
+      for (int m = 0; m < 16; ++m) w[m] = (m == c) ? 1.0 : 0.0;
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+#pragma unroll
+        for (int r = k + 1; r < 16; ++r) w[r] = fma(-Ls[(b + k) * LDS_P + b + r], w[k], w[r]);
+      }
+#pragma unroll
+      for (int r = 0; r < 16; ++r) Wt[(b + c) * LDS_P + b + r] = (r >= c) ? w[r] : 0.0;
+    }
+  }
+  __syncthreads();
+  if (tid == 0) g_ph[3] = clock64();
+  // B: off-diagonal blocks by distance
+  for (int dist = 1; dist < 4; ++dist) {
+    const int nblk = 4 - dist;
+    for (int e = tid; e < nblk * 256; e += 256) {  // X = sum_K L~_IK w~_KJ
+      const int bI = e / 256 + dist, bJ = bI - dist, r = (e % 256) / 16, c = e % 16;
+      double x0 = 0.0, x1 = 0.0;
+      for (int K = bJ; K < bI; ++K) {
+        const double* lrow = Ls + (16 * K) * LDS_P + 16 * bI + r;  // L~[16 bI + r][16 K + k], k-stride LDS_P
+        const double* wcol = Wt + (16 * bJ + c) * LDS_P + 16 * K;    // w~[16 K + k][16 bJ + c]
+#pragma unroll
+        for (int kk = 0; kk < 16; kk += 2) {
+          x0 = fma(lrow[kk * LDS_P], wcol[kk], x0);
+          x1 = fma(lrow[(kk + 1) * LDS_P], wcol[kk + 1], x1);
+        }
+      }
+      Xs[e] = x0 + x1;
+    }
+    __syncthreads();
+    for (int e = tid; e < nblk * 256; e += 256) {  // w~_IJ = -w~_II X (w~_II zero above its diagonal)
+      const int blk = e / 256, bI = blk + dist, bJ = bI - dist, r = (e % 256) / 16, c = e % 16;
+      const double* wrow = Wt + (16 * bI) * LDS_P + 16 * bI + r;  // w~[16 bI + r][16 bI + m], m-stride LDS_P
+      const double* xcol = Xs + blk * 256 + c;                     // X[m][c], m-stride 16
+      double w0 = 0.0, w1 = 0.0;
+#pragma unroll
+      for (int m = 0; m < 16; m += 2) {
+        w0 = fma(wrow[m * LDS_P], xcol[m * 16], w0);
+        w1 = fma(wrow[(m + 1) * LDS_P], xcol[(m + 1) * 16], w1);
+      }
+      Wt[(16 * bJ + c) * LDS_P + 16 * bI + r] = -(w0 + w1);
+    }
+    __syncthreads();
+  }
+  if (tid == 0) g_ph[4] = clock64();
+  for (int idx = tid; idx < PB * PB; idx += 256) {
+    const int rr = idx % PB, c = idx / PB;
+    a[(int64_t)c * lda + rr] = (rr > c) ? colA[c * LDS_P + rr] * ilj[c] : (rr == c ? lj[c] : 0.0);
+    g_W4[c * PB + rr] = (rr >= c) ? Wt[c * LDS_P + rr] * ilj[rr] : 0.0;
+  }
+  __syncthreads();
+  if (tid == 0) g_ph[5] = clock64();
+}
+
 template <int V>
 void run(const char* name, double* a, int64_t lda) {
   const int smem = 2 * PB * LDS_P * sizeof(double);
@@ -320,6 +461,7 @@ void run(const char* name, double* a, int64_t lda) {
   cudaFuncSetAttribute(potrf_2d, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaFuncSetAttribute(potrf_2d2, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaFuncSetAttribute(potrf_2d3, cudaFuncAttributeMaxDynamicSharedMemorySize, smem + 256 * 4 * 8);
+  cudaFuncSetAttribute(potrf_2d4, cudaFuncAttributeMaxDynamicSharedMemorySize, smem + 7 * 256 * 8 + PB * LDS_P * 8);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
@@ -327,7 +469,8 @@ void run(const char* name, double* a, int64_t lda) {
   for (int rep = 0; rep < 20; ++rep) {
     make_spd<<<64, 256>>>(a, lda, 64);
     cudaEventRecord(e0);
-    if (V == 4) potrf_2d3<<<1, 256, smem + 256 * 4 * 8>>>(a, lda);
+    if (V == 5) potrf_2d4<<<1, 256, smem + 7 * 256 * 8 + PB * LDS_P * 8>>>(a, lda);
+    else if (V == 4) potrf_2d3<<<1, 256, smem + 256 * 4 * 8>>>(a, lda);
     else if (V == 3) potrf_2d2<<<1, 256, smem>>>(a, lda);
     else if (V == 2) potrf_2d<<<1, 256, smem>>>(a, lda);
     else potrf_traced<V><<<1, 64 * TPR, smem>>>(a, lda);
@@ -381,6 +524,31 @@ int main() {
   for (int c = 0; c < 64; ++c)
     for (int r = c; r < 64; ++r) diff += h0[c * 64 + r] != h2[c * 64 + r];
   printf("2-D branch-free vs baseline: %d lower entries differ (bitwise)\n", diff);
+  run<5>("2-D factor-only loop + blocked inverse afterwards", a, lda);
+  cudaMemcpy2D(h2.data(), 64 * 8, a, lda * 8, 64 * 8, 64, cudaMemcpyDeviceToHost);
+  {
+    // the L of V5 is scaled (L_rc = a_rc / sqrt(d_c)); compare L L^T with the SPD input and W L with I
+    std::vector<double> W(64 * 64);
+    cudaMemcpyFromSymbol(W.data(), g_W4, sizeof(double) * 64 * 64);
+    double e1 = 0, e2 = 0;
+    for (int i = 0; i < 64; ++i)
+      for (int j = 0; j < 64; ++j) {
+        double s1 = 0, s2 = 0;
+        for (int k = 0; k < 64; ++k) {
+          const double lik = k <= i ? h2[k * 64 + i] : 0.0, ljk = k <= j ? h2[k * 64 + j] : 0.0;
+          s1 += lik * ljk;
+          s2 += W[k * 64 + i] * (j <= k ? h2[j * 64 + k] : 0.0);
+        }
+        const double aij = (i == j) ? 64.0 : 1.0 / (1.0 + i + j);
+        e1 = std::fmax(e1, std::fabs(s1 - aij));
+        e2 = std::fmax(e2, std::fabs(s2 - (i == j ? 1.0 : 0.0)));
+      }
+    printf("V5 check: max|LL^T-A|=%.3e max|WL-I|=%.3e\n", e1, e2);
+    long long ph[6];
+    cudaMemcpyFromSymbol(ph, g_ph, sizeof(ph));
+    printf("V5 phases (cycles): init+load %lld, factor loop %lld (%.0f/step), diag inverses %lld, off-diag %lld, write-out %lld\n",
+           ph[1] - ph[0], ph[2] - ph[1], (ph[2] - ph[1]) / 64.0, ph[3] - ph[2], ph[4] - ph[3], ph[5] - ph[4]);
+  }
   printf("err=%s\n", cudaGetErrorString(cudaGetLastError()));
   return 0;
 }
