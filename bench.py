@@ -315,11 +315,14 @@ def run_gpu(args):
     chol_ms = statistics.mean(i["ms_chol"] for i in infos)
     chol_tf = (n**3 / 3.0) / (chol_ms * 1e-3) / 1e12
     launches = sum(i["kernels"] for i in infos)
-    traffic = None
+    traffic, traffic_of = None, None
     prof = os.path.join(ROOT, "profiles", "trailing_dram_bytes.json")
     if os.path.exists(prof):
         try:
-            traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+            tj = json.load(open(prof))
+            traffic = tj.get("dram_bytes_per_launch")
+            traffic_of = (f"{tj.get('launch')}: {tj.get('flops_per_launch', 0):.3e} algorithmic flop "
+                          f"(ncu --set full, {tj.get('source')})")
         except Exception:
             traffic = None
 
@@ -353,6 +356,7 @@ def run_gpu(args):
             "roofline": {"bound": "tensor", "kernel": "gemm_nt_dmma<SyrkMap> (bulk trailing update U2)",
                          "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                          "frac": (achieved / FP64_PEAK_TFLOPS) if achieved else None, "traffic": traffic,
+                         "traffic_of": traffic_of,
                          "launches": tr_n, "share_of_step": (tr_ms / args.steps) / ms_per_step,
                          "peak_source": FP64_PEAK_SOURCE,
                          "flops_per_launch": "2*nb per (row, col) pair of the true lower triangle updated "
