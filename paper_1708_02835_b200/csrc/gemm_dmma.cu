@@ -1,3 +1,4 @@
+#include <cstdlib>
 // gemm_dmma.cu -- instantiations and launchers of the DMMA contraction kernels
 // (gemm_dmma.cuh) used by the tiled Cholesky schedule in api.cu.
 #include "gemm_dmma.cuh"
@@ -39,6 +40,16 @@ void launch_gemm_panel(int64_t M, int N, int K, const double* A, int64_t lda, co
   else launch<PanelCfg, false>(map, info, s);
 }
 
+// super-panel size of the trailing update (single rank); EXAGEO_SYRK_GROUP overrides (tuning)
+int syrk_group() {
+  static const int g = [] {
+    const char* e = getenv("EXAGEO_SYRK_GROUP");
+    const int v = e ? atoi(e) : 8;
+    return v >= 1 && v <= 64 ? v : 8;
+  }();
+  return g;
+}
+
 void launch_syrk_panels(const Layout& L, double* ws, const double* Pk, int k, int J0, int npan, const int* info,
                         cudaStream_t s) {
   if (npan <= 0) return;
@@ -50,6 +61,7 @@ void launch_syrk_panels(const Layout& L, double* ws, const double* Pk, int k, in
   map.J0 = J0;
   map.npan = npan;
   map.row_end = (int64_t)L.sb_end(k) * L.nb;  // N unless IND
+  map.group = L.world == 1 ? syrk_group() : 1;     // super panels: panel k's rows read once per 8 panels
   launch<TrailCfg, true, SyrkMap, true>(map, info, s);
 }
 

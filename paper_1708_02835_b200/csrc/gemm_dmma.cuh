@@ -82,9 +82,13 @@ struct DenseMap {
 // block, cut into 128 x 128 blocks: column block cb in [0, cpt), cpt = nb / 128,
 // row block rb in [cb, Mr] (rb = Mr = (N - J nb) / 128 is the z row block).
 // A 128-block is split into (128/BM) x (128/BN) CTA tiles; consecutive bids share
-// a 128-block. Order: panel by panel; inside a panel row block by row block
-// (the row's A operand is reused cpt times back to back; the panel's B operand,
-// nb rows of panel k, stays L2-resident for the whole sweep).
+// a 128-block. Order: super panel by super panel -- `group` consecutive panels taken as one
+// panel of width group * nb (single-rank layouts; group = 1 otherwise) -- and inside a
+// super panel row block by row block: the row's A operand (rows of panel k) is reused
+// group * cpt times back to back, and the super panel's B operand (group * nb rows of
+// panel k, 16 MB for 8 x 512) stays L2-resident for its sweep. With group = 1 panel k's
+// rows are re-streamed from HBM once per trailing panel (ncu: 40 GB of the 119 GB of
+// U2(0) at n = 100k); grouping divides that by the group size.
 // Operand: Pk = panel k (this rank's own storage or the received copy), ld(k).
 struct SyrkMap {
   Layout L;
@@ -95,6 +99,7 @@ struct SyrkMap {
   int npan;          // number of panels (J0, J0 + world, ...)
   int64_t row_end;   // rows updated: [J nb, row_end) and the z block (N for the exact problem;
                      // the end of the diagonal super tile for IND: zero tiles are skipped)
+  int group = 1;     // panels per super panel (1 unless world == 1)
 
   __host__ __device__ int cpt() const { return L.nb / 128; }
   __host__ __device__ int64_t Mr0() const { return (row_end - (int64_t)J0 * L.nb) / 128; }
@@ -108,6 +113,13 @@ struct SyrkMap {
     const int64_t c = cpt(), D = (int64_t)L.world * c * c;
     return i * panel_blocks(0) - D * (i * (i - 1) / 2);
   }
+  // the same for full super panels (world == 1) of width W = group cpt blocks: a super panel
+  // is a panel of width W, so Sg(s) = s a_g - W^2 s (s - 1) / 2, a_g = W (Mr0 + 1) - W (W - 1) / 2
+  __host__ __device__ int64_t Sg(int64_t sp) const {
+    const int64_t W = (int64_t)group * cpt();
+    const int64_t ag = W * (Mr0() + 1) - W * (W - 1) / 2;
+    return sp * ag - W * W * (sp * (sp - 1) / 2);
+  }
 
   template <int BM, int BN>
   __host__ __device__ __forceinline__ bool operator()(int64_t bid, GemmTile& t) const {
@@ -116,18 +128,23 @@ struct SyrkMap {
     const int sub = (int)(bid % SPLIT);
     const int half = sub % SPLIT_C, rhalf = sub / SPLIT_C;
     const int64_t q = bid / SPLIT;
-    // panel: largest i with Sp(i) <= q  (quadratic guess, exact integer fix-up)
-    const double a = (double)panel_blocks(0), D = (double)L.world * cpt() * cpt();
-    const double beta = a + 0.5 * D;
-    const double disc = beta * beta - 2.0 * D * (double)q;
-    int64_t i = (int64_t)((beta - sqrt(disc > 0.0 ? disc : 0.0)) / D);
-    if (i >= npan) i = npan - 1;
+    const int64_t nsup = (npan + group - 1) / group;  // super panels (group = 1: panels)
+    // super panel: largest i with Sg(i) <= q  (quadratic guess, exact integer fix-up)
+    const int64_t Wf = (int64_t)group * cpt();
+    const double Dg = (double)(group == 1 ? L.world * cpt() * cpt() : Wf * Wf);
+    const double a = (double)(group == 1 ? panel_blocks(0) : Sg(1));
+    const double beta = a + 0.5 * Dg;
+    const double disc = beta * beta - 2.0 * Dg * (double)q;
+    int64_t i = (int64_t)((beta - sqrt(disc > 0.0 ? disc : 0.0)) / Dg);
+    if (i >= nsup) i = nsup - 1;
     if (i < 0) i = 0;
-    while (i > 0 && Sp(i) > q) --i;
-    while (i + 1 < npan && Sp(i + 1) <= q) ++i;
-    int64_t qq = q - Sp(i);
-    const int J = J0 + (int)i * L.world;
-    const int64_t w = cpt();
+    auto S = [&](int64_t v) { return group == 1 ? Sp(v) : Sg(v); };
+    while (i > 0 && S(i) > q) --i;
+    while (i + 1 < nsup && S(i + 1) <= q) ++i;
+    int64_t qq = q - S(i);
+    const int gn = (int)((npan - i * group) < group ? (npan - i * group) : group);  // panels in it
+    const int Jfirst = J0 + (int)(i * group) * L.world;
+    const int64_t w = (int64_t)gn * cpt();  // width in 128-blocks
     const int64_t head = w * (w + 1) / 2;
     int64_t rb, cb;
     if (qq < head) {  // diagonal 128-blocks of the panel: row rb holds columns 0..rb
@@ -140,10 +157,12 @@ struct SyrkMap {
       rb = w + qq / w;
       cb = qq % w;
     }
+    const int64_t Sb = (int64_t)Jfirst * L.nb;       // first row / column of the super panel
+    const int64_t Mri = Mr0() - i * group * L.world * cpt();  // row block index of the z block
+    const int64_t gc = Sb + cb * 128 + half * BN;    // global column of the tile
+    const int J = (int)(gc / L.nb);                  // its panel (group > 1: world == 1)
     const int64_t Jb = (int64_t)J * L.nb;
-    const int64_t Mri = Mr0() - i * L.world * w;    // row block index of the z block
-    const int64_t gc = Jb + cb * 128 + half * BN;   // global column of the tile
-    const int64_t gr = (rb == Mri ? L.N : Jb + rb * 128) + rhalf * BM;  // global row (N.. = z block)
+    const int64_t gr = (rb == Mri ? L.N : Sb + rb * 128) + rhalf * BM;  // global row (N.. = z block)
     const int64_t kb = (int64_t)k * L.nb;
     const int64_t ldk = L.ld(k);
     t.A = Pk + (gr - kb);

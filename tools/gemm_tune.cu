@@ -20,7 +20,7 @@ __global__ void fill(double* p, int64_t n) {
 }
 
 template <class C, int BULK>
-void run(const char* name, const Layout& L, double* ws, int k, int reps) {
+void run(const char* name, const Layout& L, double* ws, int k, int reps, int group = 1) {
   if (set_smem<C, true, SyrkMap>() != cudaSuccess) {
     printf("%-40s smem attr failed\n", name);
     return;
@@ -33,6 +33,7 @@ void run(const char* name, const Layout& L, double* ws, int k, int reps) {
   map.J0 = k + 2;
   map.npan = L.T - k - 2;
   map.row_end = L.N;
+  map.group = group;
   const double m = (double)(L.n - (int64_t)(k + 2) * L.nb);
   const double flops = 2.0 * L.nb * (m * (m + 1) / 2 + m);
   cudaEvent_t e0, e1;
@@ -78,13 +79,11 @@ int main(int argc, char** argv) {
   cudaDeviceSynchronize();
   printf("n=%lld T=%d workspace %.2f GB\n", (long long)n, L.T, bytes / 1e9);
   for (int k : {0, L.T / 2}) {
-    run<Cfg<64, 64, 16, 2, 2, 2, 4>, 2>("64x64x16 st2 preC (product)", L, ws, k, 3);
-    run<Cfg<64, 64, 16, 2, 2, 2, 5>, 2>("64x64x16 st2 preC 5 CTA/SM", L, ws, k, 3);
-    run<Cfg<64, 64, 16, 2, 2, 3, 4>, 2>("64x64x16 st3 preC", L, ws, k, 3);
-    run<Cfg<64, 64, 32, 2, 2, 2, 3>, 2>("64x64x32 st2 preC 3 CTA/SM", L, ws, k, 3);
-    run<Cfg<64, 128, 16, 2, 2, 2, 2>, 2>("64x128x16 st2 preC warp 32x64", L, ws, k, 3);
-    run<Cfg<128, 64, 16, 2, 2, 2, 2>, 2>("128x64x16 st2 preC warp 64x32", L, ws, k, 3);
-    run<Cfg<64, 128, 16, 2, 2, 3, 2>, 2>("64x128x16 st3 preC warp 32x64", L, ws, k, 3);
+    for (int g : {1, 2, 4, 8, 16}) {
+      char name[64];
+      snprintf(name, sizeof(name), "64x64x16 st2 preC, super panels of %d", g);
+      run<Cfg<64, 64, 16, 2, 2, 2, 4>, 2>(name, L, ws, k, 3, g);
+    }
   }
   return 0;
 }

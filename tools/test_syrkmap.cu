@@ -13,7 +13,7 @@ using namespace exageo;
 using namespace exageo::gemm;
 
 template <int BM, int BN>
-int check(int T, int nb, int world, int rank, int k, int J0, int npan, int64_t row_end = 0) {
+int check(int T, int nb, int world, int rank, int k, int J0, int npan, int64_t row_end = 0, int group = 1) {
   Layout L;
   L.nb = nb;
   L.T = T;
@@ -30,6 +30,7 @@ int check(int T, int nb, int world, int rank, int k, int J0, int npan, int64_t r
   m.J0 = J0;
   m.npan = npan;
   m.row_end = row_end > 0 ? row_end : L.N;
+  m.group = group;
   const int64_t nblk = m.blocks(BM, BN);
   std::set<std::tuple<int64_t, int64_t>> seen;
   const int64_t kb = (int64_t)k * nb;
@@ -170,6 +171,28 @@ int main() {
         ++n;
       }
   bad += check<64, 64>(586, 512, 8, 3, 5, 11, 72);
+  // super panels (single rank): group consecutive panels enumerated as one wide panel
+  for (int group : {2, 3, 8})
+    for (int nb : {128, 256, 512})
+      for (int T : {2, 5, 20, 37})
+        for (int k = 0; k + 2 <= T; ++k) {
+          for (int J0 : {k + 1, k + 2}) {
+            const int npan = T - J0;
+            if (npan <= 0) continue;
+            bad += check<64, 64>(T, nb, 1, 0, k, J0, npan, 0, group);
+            bad += check<128, 64>(T, nb, 1, 0, k, J0, npan, 0, group);
+            bad += check<64, 64>(T, nb, 1, 0, k, J0, npan, (int64_t)((J0 + npan) * nb), group);
+            n += 3;
+          }
+        }
+  // IND with super panels: rows limited to the IND super tile of k
+  for (int group : {2, 8})
+    for (int k = 0; k < 20; ++k) {
+      const int e = (k / 3 + 1) * 3 < 20 ? (k / 3 + 1) * 3 : 20;
+      if (k + 1 < e) bad += check<64, 64>(20, 256, 1, 0, k, k + 1, e - k - 1, (int64_t)e * 256, group);
+      ++n;
+    }
+  bad += check<64, 64>(196, 512, 1, 0, 0, 2, 194, 0, 8);
   printf("%s: %d failures in %d enumerations\n", bad ? "FAIL" : "OK", bad, n + 2);
   return bad ? 1 : 0;
 }
