@@ -478,7 +478,7 @@ void destroy_graph(exageo_ctx* c) {
 std::vector<const void*> graph_key(const exageo_ctx* c, const double* x, const double* y, const double* z,
                                    int kind) {
   std::vector<const void*> k = {(const void*)(intptr_t)c->G.n, (const void*)(intptr_t)c->G.nb, x, y, z,
-                                c->parts, c->out3, c->h_res, c->mtab, (const void*)(intptr_t)(kind == 0)};
+                                c->parts, c->out3, c->h_res, c->mtab, (const void*)(intptr_t)kind};
   for (const auto& R : c->rs) {
     for (const void* p : {(const void*)R.ws, (const void*)R.slots, (const void*)R.recv[0], (const void*)R.recv[1],
                           (const void*)R.W, (const void*)R.scratch, (const void*)R.info})
@@ -547,7 +547,7 @@ exageo_status run_graph(exageo_ctx* c, const exageo_theta* t, int64_t n, const d
       if (ty != cudaGraphNodeTypeKernel) continue;
       cudaKernelNodeParams kp;
       CUDA_TRY(c, cudaGraphKernelNodeGetParams(nd, &kp));
-      if (kp.func == gen_panels_kernel_fn() || kp.func == matern_table_kernel_fn()) c->gen_nodes.push_back(nd);
+      if (kp.func == gen_panels_kernel_fn(mc.kind) || kp.func == matern_table_kernel_fn()) c->gen_nodes.push_back(nd);
     }
     if (c->gen_nodes.size() != c->rs.size() + (mc.kind == 0 ? 1 : 0)) {
       destroy_graph(c);
@@ -569,7 +569,7 @@ exageo_status run_graph(exageo_ctx* c, const exageo_theta* t, int64_t n, const d
       cudaKernelNodeParams kp;
       CUDA_TRY(c, cudaGraphKernelNodeGetParams(nd, &kp));
       void* args[7];
-      const bool gen = kp.func == gen_panels_kernel_fn();
+      const bool gen = kp.func == gen_panels_kernel_fn(mc.kind);
       const int nargs = gen ? 7 : 2, imc = gen ? 2 : 0;
       // gen_panels_kernel(Layout, ws, MaternConsts, x, y, z, tab); matern_table_kernel(MaternConsts, tab)
       for (int i = 0; i < nargs; ++i) args[i] = kp.kernelParams[i];

@@ -100,7 +100,7 @@ const void* matern_table_kernel_fn();  // CUDA-graph node identification
 // tab = the table built by launch_matern_table for this theta (used when kind == 0).
 void launch_gen_panels(const Layout& L, double* ws, const MaternConsts& mc, const double* x, const double* y,
                        const double* z, const double* tab, cudaStream_t s);
-const void* gen_panels_kernel_fn();  // the K1 kernel (CUDA-graph node identification)
+const void* gen_panels_kernel_fn(int kind);  // the K1 kernel for MaternConsts::kind (CUDA-graph nodes)
 // Dense Matern block and kriging sums (build the table themselves into tab when needed).
 void launch_matern_dense(const MaternConsts& mc, int64_t m, const double* x1, const double* y1, int64_t n,
                          const double* x2, const double* y2, double* C, int64_t ldc, double* tab, cudaStream_t s);

@@ -200,6 +200,23 @@ __device__ __forceinline__ double matern_eval(double r, const MaternConsts& c, c
   return matern_x(x, c);
 }
 
+// The same with the covariance family fixed at compile time (K1's bulk path: each
+// instantiation carries only its own evaluator, so the closed forms keep a small register
+// footprint and full occupancy).
+template <int KIND>
+__device__ __forceinline__ double matern_eval_k(double r, const MaternConsts& c, const double* __restrict__ tab) {
+  if (r == 0.0) return c.theta1;
+  const double x = r * c.inv_theta2;
+  if constexpr (KIND == 1) return c.theta1 * exp(-x);
+  if constexpr (KIND == 2) return c.theta1 * (1.0 + x) * exp(-x);
+  if constexpr (KIND == 3) return c.theta1 * (1.0 + x + x * x * (1.0 / 3.0)) * exp(-x);
+  if constexpr (KIND == 0) {
+    if (tab != nullptr && x >= kTabX0 && x < kTabXMax) return matern_tab(x, tab);
+    return matern_x(x, c);
+  }
+  return 0.0;
+}
+
 // Distance between s1 = (x1, y1) and s2 = (x2, y2): Euclidean (R15), or the great-circle
 // distance by the haversine formula with x = longitude, y = latitude in
 // degrees: d = 2 R asin(sqrt(hav(dphi) + cos(phi1) cos(phi2) hav(dlambda))), hav(a) = sin^2(a/2).
@@ -218,13 +235,14 @@ __device__ __forceinline__ double dist2d(double x1, double y1, double x2, double
 
 // Entry (global row r, global column c) of the generated panel (slow path): identity
 // padding outside n, IND-annihilated tiles, the diagonal theta1 (R9), else Eq. (2).
-__device__ __noinline__ double gen_entry(const Layout& L, const MaternConsts& mc, const double* __restrict__ x,
+template <int KIND>
+__device__ __forceinline__ double gen_entry(const Layout& L, const MaternConsts& mc, const double* __restrict__ x,
                                             const double* __restrict__ y, int64_t r, int64_t c, double xc,
                                             double yc, const double* __restrict__ tab) {
   if (r >= L.n || c >= L.n) return (r == c) ? 1.0 : 0.0;
   if (!L.in_super_tile(r, c)) return 0.0;  // IND: annihilated off-diagonal tile
   if (r == c) return mc.theta1;
-  return matern_eval(dist2d(x[r], y[r], xc, yc, mc), mc, tab);
+  return matern_eval_k<KIND>(dist2d(x[r], y[r], xc, yc, mc), mc, tab);
 }
 
 constexpr int kGenCols = 8;  // columns per CTA: one (x, y) row load and index test serve 8 entries
@@ -233,6 +251,7 @@ constexpr int kGenCols = 8;  // columns per CTA: one (x, y) row load and index t
 // -> walks the rows of those columns, two rows per thread and step, coalesced double2
 // stores down each column. Rows below the diagonal tile inside n (the bulk) take the
 // check-free path.
+template <int KIND>
 __global__ void __launch_bounds__(256) gen_panels_kernel(Layout L, double* __restrict__ ws, MaternConsts mc,
                                                          const double* __restrict__ x, const double* __restrict__ y,
                                                          const double* __restrict__ z, const double* __restrict__ tab) {
@@ -256,8 +275,8 @@ __global__ void __launch_bounds__(256) gen_panels_kernel(Layout L, double* __res
       const double x0 = x[r0], y0 = y[r0], x1 = x[r0 + 1], y1 = y[r0 + 1];
 #pragma unroll 1
       for (int k = 0; k < kGenCols; ++k) {  // rolled: one inlined copy of the evaluator
-        const double v0 = matern_eval(dist2d(x0, y0, xc[k], yc[k], mc), mc, tab);
-        const double v1 = matern_eval(dist2d(x1, y1, xc[k], yc[k], mc), mc, tab);
+        const double v0 = matern_eval_k<KIND>(dist2d(x0, y0, xc[k], yc[k], mc), mc, tab);
+        const double v1 = matern_eval_k<KIND>(dist2d(x1, y1, xc[k], yc[k], mc), mc, tab);
         *reinterpret_cast<double2*>(col0 + k * ld + rr) = make_double2(v0, v1);
       }
     } else {
@@ -269,7 +288,7 @@ __global__ void __launch_bounds__(256) gen_panels_kernel(Layout L, double* __res
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int64_t lr = rr + e;
-          if (lr < R) v[e] = gen_entry(L, mc, x, y, jb + lr, c, xck, yck, tab);
+          if (lr < R) v[e] = gen_entry<KIND>(L, mc, x, y, jb + lr, c, xck, yck, tab);
           else v[e] = (lr == R && c < L.n && z != nullptr) ? z[c] : 0.0;  // z row block
         }
         *reinterpret_cast<double2*>(col0 + k * ld + rr) = make_double2(v[0], v[1]);
@@ -343,13 +362,25 @@ void launch_krige(const MaternConsts& mc, int64_t m, const double* xn, const dou
   krige_sum_kernel<<<(unsigned)((m + 255) / 256), 256, 0, s>>>(m, part, nch, znew);
 }
 
-const void* gen_panels_kernel_fn() { return (const void*)gen_panels_kernel; }
+const void* gen_panels_kernel_fn(int kind) {
+  switch (kind) {
+    case 1: return (const void*)gen_panels_kernel<1>;
+    case 2: return (const void*)gen_panels_kernel<2>;
+    case 3: return (const void*)gen_panels_kernel<3>;
+    default: return (const void*)gen_panels_kernel<0>;
+  }
+}
 
 void launch_gen_panels(const Layout& L, double* ws, const MaternConsts& mc, const double* x, const double* y,
                        const double* z, const double* tab, cudaStream_t s) {
   if (L.owned() == 0) return;
   dim3 grid(L.nb / kGenCols, L.owned());
-  gen_panels_kernel<<<grid, 256, 0, s>>>(L, ws, mc, x, y, z, mc.kind == 0 ? tab : nullptr);
+  switch (mc.kind) {
+    case 1: gen_panels_kernel<1><<<grid, 256, 0, s>>>(L, ws, mc, x, y, z, nullptr); break;
+    case 2: gen_panels_kernel<2><<<grid, 256, 0, s>>>(L, ws, mc, x, y, z, nullptr); break;
+    case 3: gen_panels_kernel<3><<<grid, 256, 0, s>>>(L, ws, mc, x, y, z, nullptr); break;
+    default: gen_panels_kernel<0><<<grid, 256, 0, s>>>(L, ws, mc, x, y, z, tab); break;
+  }
 }
 
 void launch_matern_dense(const MaternConsts& mc, int64_t m, const double* x1, const double* y1, int64_t n,
