@@ -187,3 +187,18 @@ def test_mle_trust_region_bound_active(ctx):
     assert th[1] == pytest.approx(0.05, rel=1e-12)
     thn, lln, _, _ = ctx.mle(x, y, z, lo, hi, (1.0, 0.02, 0.5), xtol_rel=1e-9)
     assert ll >= lln - 1e-9 * abs(lln)
+
+
+def test_mle_monte_carlo_median_near_truth(ctx):
+    # statistical sanity: over independent fields the estimates centre on the
+    # truth (not exact; 12 replicas at n = 900)
+    n, truth = 900, (1.0, 0.1, 0.7)
+    x, y = ex.gen_locations(n, 1)
+    start = tuple(math.sqrt(a * b) for a, b in zip(LO, HI))
+    est = []
+    for r in range(12):
+        z = ctx.simulate(x, y, si.normals(n, 500 + r), truth)
+        th, _, _, _ = ctx.mle(x, y, z, LO, HI, start, xtol_rel=1e-6, profile=True, method="trust-region")
+        est.append(th)
+    med = np.median(np.array(est), axis=0)
+    assert abs(med[0] - 1.0) < 0.25 and abs(med[1] - 0.1) < 0.025 and abs(med[2] - 0.7) < 0.07, med
