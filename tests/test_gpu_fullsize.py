@@ -93,3 +93,20 @@ def test_simulate_roundtrip_full_size(ctx):
     z = ctx.simulate(x, y, e, THETA)
     r = ctx.loglik(x, y, z, THETA)
     assert r.quad == pytest.approx(float(e @ e), rel=1e-9)
+
+
+@pytest.mark.parametrize("theta", [(1.3, 0.1, 1.27), (0.8, 0.03, 0.61)])
+def test_sampled_entries_general_nu_full_size(ctx, theta):
+    # general nu at full size: the generator reads the per-theta Chebyshev table (K1T)
+    x, y = ex.gen_locations(N, 2)
+    z = si.normals(N, 2)
+    ctx.stage_generate_dev(dev(x), dev(y), dev(z), theta)
+    rng = np.random.default_rng(1)
+    rows = rng.integers(0, N, 2000)
+    cols = (rng.random(2000) * (rows + 1)).astype(np.int64)
+    got = ctx.read_entries(rows, cols)
+    d = np.array([math.hypot(x[r] - x[c], y[r] - y[c]) if r != c else 0.0 for r, c in zip(rows, cols)])
+    ref = np.array([oracle.matern(v, theta) for v in d])
+    mask = ref > 1e-290
+    bound = 5e-14 * ref[mask] + 4e-16 * (d[mask] / theta[1]) * ref[mask]
+    assert np.all(np.abs(got[mask] - ref[mask]) <= bound)
