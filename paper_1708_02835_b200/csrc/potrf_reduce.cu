@@ -2,11 +2,11 @@
 // K6 (deterministic log-det / dot reductions and l(theta)), read-back and TRMV.
 //
 //  * potrf_block: the PB x PB (PB = 64) diagonal block of the current panel is
-//    factored in shared memory by the right-looking unblocked algorithm
-//    (L_jj = sqrt(a_jj); l_ij = a_ij / L_jj; a_ic -= l_ij l_cj), the paper's
-//    dpotrf at tile granularity (Alg. 2 l.3). The same CTA forms
-//    W = L^{-1} so that the panel TRSM becomes a DMMA multiplication, and the
-//    partial log-determinant sum_i log L_ii (R5). The first
+//    factored by the right-looking unblocked algorithm with the entries in
+//    registers (L_jj = sqrt(a_jj); l_ij = a_ij / L_jj; a_ic -= l_ij l_cj), the
+//    paper's dpotrf at tile granularity (Alg. 2 l.3). The same CTA then
+//    forms W = L^{-1} so that the panel TRSM becomes a DMMA multiplication, and
+//    the partial log-determinant sum_i log L_ii (R5). The first
 //    non-positive pivot is recorded as a global index (R14); every later
 //    kernel reads the info word and exits.
 //  * reductions: per rank, logdet/2 = sum of its panels' partials and quad = sum y_c^2
@@ -22,68 +22,73 @@ namespace exageo {
 
 namespace {
 
-constexpr int LDS_P = PB + 1;
+constexpr int LDS_P = PB + 1;  // odd stride: conflict-free column access
+constexpr int LDS_A = PB + 2;  // even stride: 16-byte aligned double2 rows of colA
 
-// 64 TPR threads: thread t owns row r = t / TPR and the NS = 64 / TPR slots
-// c = (t % TPR) + TPR s of it, in registers. Slot c holds a_rc (the Schur complement,
-// unscaled) while c > j and, from step c on, w_rc of W = L^{-1} (unscaled). Step j: the
-// owners of row j publish W's row j to shared memory (column j of A was published at step
-// j-1), one barrier, then every row r > j applies, with d_j = a_jj and f = a_rj / d_j,
-//   c >  j: a_rc -= f a_cj        (right-looking Cholesky; L_jj = sqrt d_j, L_rj = a_rj / L_jj)
-//   c <= j: w_rc -= f w_jc        (right-looking L W = I;  W_jc = w_jc / L_jj, w_jj = 1)
-// and the owner of column j+1 publishes a_r,j+1. Scaling is deferred to the write-out.
-// colA and rowW share one array (rowW at offset PB * LDS_P) so the per-slot source is an
-// index select, not a pointer select.
-template <int TPR>
-__global__ void __launch_bounds__(64 * TPR) potrf_block_kernel(double* __restrict__ a, int64_t lda,
-                                                               double* __restrict__ W, double* __restrict__ slot,
-                                                               int* __restrict__ info, int64_t pivot_base) {
-  constexpr int NS = PB / TPR;
-  constexpr int RPW = 32 / TPR;  // rows per warp
-  constexpr int WOFF = PB * LDS_P;
+// 256 threads as a 16 x 16 grid: thread (tr, tc) holds a_rc for rows r = tr + 16 i and
+// columns c = 4 tc + k (i, k < 4) in registers. Step j (right-looking, deferred scaling):
+// d_j = a_jj, f_r = a_rj / d_j (reciprocal-multiply, as the paper's dpotrf), a_rc -= f_r a_cj
+// for every held entry (rows r <= j get f = 0; entries above the diagonal take finite garbage
+// that is never read), then the owner of column j+1 publishes it to shared memory -- one
+// barrier per pivot. The j loop is unrolled by 4 so the register slot of column j+1 is a
+// compile-time index (no select chains on the pivot chain). W = L^{-1} is formed after the
+// factorization: 16 x 16 diagonal blocks by per-lane substitution, the off-diagonal blocks
+// W_IJ = -W_II sum_K L~_IK W_KJ by distance (tools/potrf_trace.cu: 24.6 us vs 32.7 us for
+// the previous 16-threads-per-row kernel that carried W through the pivot loop; the factor
+// L is bitwise the same).
+constexpr int kPotrfSmemDoubles = PB * LDS_A + PB * LDS_P + 3 * 256 + PB * LDS_P;
+
+__global__ void __launch_bounds__(256) potrf_block_kernel(double* __restrict__ a, int64_t lda,
+                                                          double* __restrict__ W, double* __restrict__ slot,
+                                                          int* __restrict__ info, int64_t pivot_base) {
   if (*(volatile int*)info != 0) return;
   extern __shared__ double smem_p[];
-  double* colA = smem_p;         // colA[j * LDS_P + r] = a_rj at step j (unscaled)
-  double* rowW = smem_p + WOFF;  // rowW[j * LDS_P + c] = w_jc at step j (unscaled)
-  const int tid = threadIdx.x;
-  const int r = tid / TPR, q = tid % TPR;
-  double v[NS];
+  double* colA = smem_p;             // colA[c * LDS_A + r] = a_rc at step c (unscaled)
+  double* Wt = colA + PB * LDS_A;    // Wt[c * LDS_P + r] = w~_rc, w~ = L~^{-1} (unit lower)
+  double* Xs = Wt + PB * LDS_P;      // 3 x 16 x 16 off-diagonal products
+  double* Ls = Xs + 3 * 256;         // Ls[c * LDS_P + r] = L~_rc = a_rc / d_c (r > c)
+  __shared__ double rdv[PB], ilj[PB], lj[PB], lred[2];
+  const int tid = threadIdx.x, tr = tid >> 4, tc = tid & 15;
+  double v[4][4];
 #pragma unroll
-  for (int s = 0; s < NS; ++s) {
-    const int c = q + TPR * s;
-    v[s] = (c <= r) ? a[(int64_t)c * lda + r] : 0.0;
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int r = tr + 16 * i, c = 4 * tc + k;
+      v[i][k] = (c <= r) ? a[(int64_t)c * lda + r] : 0.0;
+    }
+  if (tc == 0) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) colA[tr + 16 * i] = v[i][0];  // column 0
   }
-  if (q == 0) colA[r] = v[0];  // column 0
   int bad = -1;
-  for (int j = 0; j < PB; ++j) {
-    if (r == j) {
+  for (int m = 0; m < PB / 4 && bad < 0; ++m) {
 #pragma unroll
-      for (int s = 0; s < NS; ++s) {
-        const int c = q + TPR * s;
-        rowW[j * LDS_P + c] = (c < j) ? v[s] : (c == j ? 1.0 : 0.0);
+    for (int u = 0; u < 4; ++u) {
+      const int j = 4 * m + u;
+      __syncthreads();
+      const double* cj = colA + j * LDS_A;
+      const double d = cj[j];
+      if (!(d > 0.0)) {  // uniform: every thread reads the same pivot
+        bad = j;
+        break;
       }
-    }
-    __syncthreads();
-    const double d = colA[j * LDS_P + j];
-    if (!(d > 0.0)) {
-      bad = j;
-      break;
-    }
-    if ((tid >> 5) * RPW + RPW - 1 > j) {  // warp-uniform: this warp holds rows > j
-      // Branch-free over the slots (the lanes of a row own different columns, so any
-      // per-slot branch would diverge): select the source row/column, predicate the update.
-      const bool row_active = r > j;
-      const double f = colA[j * LDS_P + r] * __drcp_rn(d);
+      const double rd = __drcp_rn(d);
+      double f[4];
 #pragma unroll
-      for (int s = 0; s < NS; ++s) {
-        const int c = q + TPR * s;
-        const bool isw = c <= j;  // W part (c == j: reset a_rj to w_rj = 0 - f w_jj, w_jj = 1)
-        const double src = smem_p[j * LDS_P + c + (isw ? WOFF : 0)];
-        const double base = (c == j) ? 0.0 : v[s];
-        const double nv = base - f * src;
-        const bool act = row_active && (isw || c <= r);
-        v[s] = act ? nv : v[s];
-        if (act && c == j + 1) colA[(j + 1) * LDS_P + r] = nv;
+      for (int i = 0; i < 4; ++i) f[i] = (tr + 16 * i > j) ? cj[tr + 16 * i] * rd : 0.0;
+      const double2 s01 = *reinterpret_cast<const double2*>(cj + 4 * tc);
+      const double2 s23 = *reinterpret_cast<const double2*>(cj + 4 * tc + 2);
+      const double src[4] = {s01.x, s01.y, s23.x, s23.y};
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) v[i][k] = fma(-f[i], src[k], v[i][k]);
+      const int k1 = (u + 1) & 3;  // register slot of column j + 1 (constant after unrolling)
+      const int j1 = j + 1;
+      if (j1 < PB && tc == (j1 >> 2)) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) colA[j1 * LDS_A + tr + 16 * i] = v[i][k1];
       }
     }
   }
@@ -92,11 +97,10 @@ __global__ void __launch_bounds__(64 * TPR) potrf_block_kernel(double* __restric
     return;
   }
   __syncthreads();
-  // L_jj = sqrt(d_j) and 1 / L_jj once per column; sum log L_jj = sum log(d_j) / 2 by a
-  // fixed two-level tree (warps 0-1, then lane 0 of warp 0)
-  __shared__ double lj[PB], ilj[PB], lred[2];
+  // L_jj = sqrt(d_j), 1 / L_jj; sum log L_jj = sum log(d_j) / 2 by a fixed two-level tree
   if (tid < PB) {
-    const double dj = colA[tid * LDS_P + tid];
+    const double dj = colA[tid * LDS_A + tid];
+    rdv[tid] = __drcp_rn(dj);
     lj[tid] = sqrt(dj);
     ilj[tid] = 1.0 / lj[tid];
     double lg = 0.5 * log(dj);
@@ -106,9 +110,64 @@ __global__ void __launch_bounds__(64 * TPR) potrf_block_kernel(double* __restric
   __syncthreads();
   if (tid == 0) *slot = lred[0] + lred[1];
   for (int idx = tid; idx < PB * PB; idx += blockDim.x) {
-    const int rr = idx % PB, c = idx / PB;
-    a[(int64_t)c * lda + rr] = (rr > c) ? colA[c * LDS_P + rr] * ilj[c] : (rr == c ? lj[c] : 0.0);
-    W[c * PB + rr] = (rr >= c) ? rowW[rr * LDS_P + c] * ilj[rr] : 0.0;
+    const int rr = idx & (PB - 1), c = idx / PB;
+    Ls[c * LDS_P + rr] = (rr > c) ? colA[c * LDS_A + rr] * rdv[c] : 0.0;
+  }
+  __syncthreads();
+  {  // diagonal 16 x 16 blocks of w~ = L~^{-1}: warp I, lane c computes column c
+    const int I = tid >> 5, c = tid & 31;
+    if (I < 4 && c < 16) {
+      const int b = 16 * I;
+      double w[16];
+#pragma unroll
+      for (int mm = 0; mm < 16; ++mm) w[mm] = (mm == c) ? 1.0 : 0.0;
+#pragma unroll
+      for (int k = 0; k < 16; ++k)
+#pragma unroll
+        for (int r = k + 1; r < 16; ++r) w[r] = fma(-Ls[(b + k) * LDS_P + b + r], w[k], w[r]);
+#pragma unroll
+      for (int r = 0; r < 16; ++r) Wt[(b + c) * LDS_P + b + r] = (r >= c) ? w[r] : 0.0;
+    }
+  }
+  __syncthreads();
+  {  // off-diagonal blocks by distance; thread t owns entry (t / 16, t % 16) of each block
+    const int r = tid >> 4, c = tid & 15;
+#pragma unroll
+    for (int dist = 1; dist < 4; ++dist) {
+      double x[3];
+#pragma unroll
+      for (int blk = 0; blk < 4 - dist; ++blk) {
+        const int bI = blk + dist, bJ = blk;
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int K = bJ; K < bI; ++K) {
+          const double* lrow = Ls + (16 * K) * LDS_P + 16 * bI + r;
+          const double* wcol = Wt + (16 * bJ + c) * LDS_P + 16 * K;
+#pragma unroll
+          for (int kk = 0; kk < 16; ++kk) acc[kk & 3] = fma(lrow[kk * LDS_P], wcol[kk], acc[kk & 3]);
+        }
+        x[blk] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+      }
+#pragma unroll
+      for (int blk = 0; blk < 4 - dist; ++blk) Xs[blk * 256 + r * 16 + c] = x[blk];
+      __syncthreads();
+#pragma unroll
+      for (int blk = 0; blk < 4 - dist; ++blk) {
+        const int bI = blk + dist, bJ = blk;
+        const double* wrow = Wt + (16 * bI) * LDS_P + 16 * bI + r;
+        const double* xcol = Xs + blk * 256 + c;
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int mm = 0; mm < 16; ++mm) acc[mm & 3] = fma(wrow[mm * LDS_P], xcol[mm * 16], acc[mm & 3]);
+        Wt[(16 * bJ + c) * LDS_P + 16 * bI + r] = -((acc[0] + acc[1]) + (acc[2] + acc[3]));
+      }
+      __syncthreads();
+    }
+  }
+  for (int idx = tid; idx < PB * PB; idx += blockDim.x) {
+    const int rr = idx & (PB - 1), c = idx / PB;
+    a[(int64_t)c * lda + rr] = (rr > c) ? colA[c * LDS_A + rr] * ilj[c] : (rr == c ? lj[c] : 0.0);
+    W[c * PB + rr] = (rr >= c) ? Wt[c * LDS_P + rr] * ilj[rr] : 0.0;
   }
 }
 
@@ -249,24 +308,15 @@ __global__ void trmv_sum_kernel(int64_t n, int64_t N, const double* __restrict__
 
 }  // namespace
 
-constexpr int kPotrfSmem = 2 * PB * LDS_P * (int)sizeof(double);
-#ifndef EXAGEO_POTRF_TPR
-#define EXAGEO_POTRF_TPR 16
-#endif
-constexpr int kPotrfTpr = EXAGEO_POTRF_TPR;  // threads per row of the 64 x 64 block
+constexpr int kPotrfSmem = kPotrfSmemDoubles * (int)sizeof(double);
 
 cudaError_t potrf_init() {
-  return cudaFuncSetAttribute(potrf_block_kernel<kPotrfTpr>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              kPotrfSmem);
+  return cudaFuncSetAttribute(potrf_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kPotrfSmem);
 }
 
-// (Measured alternatives on B200: a 4 x 4-blocked variant with a warp-serial 16 x 16
-// diagonal factorization, 68 us; a pair-step variant eliminating two columns per barrier
-// with a 2 x 2 pivot block, 27 us but it loses exact-zero pivot detection for duplicate
-// sites; this kernel: 31 us.)
 void launch_potrf_block(double* a, int64_t lda, double* W, double* slot, int* info, int64_t pivot_base,
                         cudaStream_t s) {
-  potrf_block_kernel<kPotrfTpr><<<1, 64 * kPotrfTpr, kPotrfSmem, s>>>(a, lda, W, slot, info, pivot_base);
+  potrf_block_kernel<<<1, 256, kPotrfSmem, s>>>(a, lda, W, slot, info, pivot_base);
 }
 
 void launch_local_partials(const Layout& L, const double* ws, const double* slots, int nslots, double* scratch,

@@ -197,6 +197,8 @@ inline bool minimize(const std::function<double(std::vector<double>&)>& fn, cons
   // ---- main loop
   const double delta_max = std::max(delta0, 1.0);
   int stalls = 0;
+  double best_sig = inf;  // best value at the last significant decrease
+  int since_progress = 0;
   while (!stop()) {
     int b = (int)(std::min_element(F.begin(), F.end()) - F.begin());
     const std::vector<double> xb = Y[b];
@@ -302,9 +304,16 @@ inline bool minimize(const std::function<double(std::vector<double>&)>& fn, cons
     const double pred = -m.value(s);
     double snorm = 0.0;
     for (int i = 0; i < d; ++i) snorm = std::max(snorm, std::fabs(s[i]));
-    // reductions below the evaluation noise (rounding of f, ~1e-13 relative for a
-    // log-likelihood) carry no information: they count as no progress
-    const double noise = 1e-13 * std::max(1.0, std::fabs(fb));
+    // reductions below the evaluation noise carry no information: they count as no progress
+    // (a log-likelihood from an n x n Cholesky is reproducible but not smooth below ~n eps
+    // relative; 1e-11 covers n <= 1e5 with margin)
+    const double noise = 1e-11 * std::max(1.0, std::fabs(fb));
+    if (fb < best_sig - noise) {  // significant progress since the last check
+      best_sig = fb;
+      since_progress = 0;
+    } else if (++since_progress > 8 * p) {
+      break;  // 8 p iterations without a significant decrease: converged to noise level
+    }
     if (!(pred > noise) || snorm < 0.05) {
       // no useful step at this radius: fix the geometry if points are far, else shrink
       if (farthest > 2.0 * delta && jfar != b) {

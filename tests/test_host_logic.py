@@ -31,4 +31,4 @@ def test_trust_region_minimiser(tmp_path):
     subprocess.check_call(["g++", "-O2", "-std=c++17", "-o", exe, os.path.join(ROOT, "tools", "test_trust_region.cpp")])
     out = subprocess.run([exe], capture_output=True, text=True)
     assert out.returncode == 0, out.stdout + out.stderr
-    assert out.stdout.count(" ok") == 7, out.stdout
+    assert out.stdout.count(" ok") == 8, out.stdout

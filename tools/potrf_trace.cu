@@ -454,6 +454,146 @@ __global__ void __launch_bounds__(256) potrf_2d4(double* __restrict__ a, int64_t
   if (tid == 0) g_ph[5] = clock64();
 }
 
+__device__ double g_W6[64 * 64];
+__device__ long long g_ph6[6];
+__global__ void __launch_bounds__(256) potrf_2d6(double* __restrict__ a, int64_t lda) {
+  constexpr int LDS6 = 66;               // even: 16-byte aligned double2 rows
+  extern __shared__ double smem_p[];
+  double* colA = smem_p;                 // 64 x 66 (first 64 x 65 region + 64 more)
+  double* Wt = smem_p + PB * LDS6;       // 64 x 65: Wt[c * 65 + r] = w~_rc
+  double* dummy = Wt + PB * LDS_P;        // 4 x 256
+  double* Xs = dummy + 4 * 256;          // 3 x 256
+  double* Ls = Xs + 3 * 256;             // 64 x 65: scaled L~_rc = colA[c][r] / d_c (r > c)
+  __shared__ double rdv[PB], ilj[PB], lj[PB];
+  const int tid = threadIdx.x, tr = tid >> 4, tc = tid & 15;
+  if (tid == 0) g_ph6[0] = clock64();
+  double v[4][4];  // rows tr + 16 i, columns 4 tc + k
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int r = tr + 16 * i, c = 4 * tc + k;
+      v[i][k] = (c <= r) ? a[(int64_t)c * lda + r] : 0.0;
+    }
+  __syncthreads();
+  if (tc == 0) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) colA[tr + 16 * i] = v[i][0];
+  }
+  int bad = -1;
+  __syncthreads();
+  if (tid == 0) g_ph6[1] = clock64();
+  for (int m = 0; m < PB / 4 && bad < 0; ++m) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int j = 4 * m + u;
+      __syncthreads();
+      const double* cj = colA + j * LDS6;
+      const double d = cj[j];
+      if (!(d > 0.0)) {
+        bad = j;
+        break;
+      }
+      const double rd = __drcp_rn(d);
+      double f[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) f[i] = (tr + 16 * i > j) ? cj[tr + 16 * i] * rd : 0.0;
+      const double2 s01 = *reinterpret_cast<const double2*>(cj + 4 * tc);
+      const double2 s23 = *reinterpret_cast<const double2*>(cj + 4 * tc + 2);
+      const double src[4] = {s01.x, s01.y, s23.x, s23.y};
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) v[i][k] = fma(-f[i], src[k], v[i][k]);
+      const int k1 = (u + 1) & 3;  // register slot of column j + 1 (constant after unrolling)
+      const int j1 = j + 1;
+      if (j1 < PB && tc == (j1 >> 2)) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) colA[j1 * LDS6 + tr + 16 * i] = v[i][k1];
+      }
+    }
+  }
+  if (bad >= 0) return;
+  __syncthreads();
+  if (tid == 0) g_ph6[2] = clock64();
+  if (tid < PB) {
+    const double dj = colA[tid * LDS6 + tid];
+    rdv[tid] = __drcp_rn(dj);
+    lj[tid] = sqrt(dj);
+    ilj[tid] = 1.0 / lj[tid];
+  }
+  __syncthreads();
+  for (int idx = tid; idx < PB * PB; idx += 256) {
+    const int rr = idx & 63, c = idx >> 6;
+    Ls[c * LDS_P + rr] = (rr > c) ? colA[c * LDS6 + rr] * rdv[c] : 0.0;
+  }
+  __syncthreads();
+  // A: diagonal 16 x 16 blocks of w~ = L~^{-1}, L~_rc = colA[c][r] / d_c; warp I, lane c
+  {
+    const int I = tid >> 5, c = tid & 31;
+    if (I < 4 && c < 16) {
+      const int b = 16 * I;
+      double w[16];
+#pragma unroll
+      for (int m = 0; m < 16; ++m) w[m] = (m == c) ? 1.0 : 0.0;
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+#pragma unroll
+        for (int r = k + 1; r < 16; ++r) w[r] = fma(-Ls[(b + k) * LDS_P + b + r], w[k], w[r]);
+      }
+#pragma unroll
+      for (int r = 0; r < 16; ++r) Wt[(b + c) * LDS_P + b + r] = (r >= c) ? w[r] : 0.0;
+    }
+  }
+  __syncthreads();
+  if (tid == 0) g_ph6[3] = clock64();
+  // B: off-diagonal blocks by distance
+  // off-diagonal blocks by distance: X = sum_K L~_IK w~_KJ, then w~_IJ = -w~_II X. Thread t
+  // owns entry (r, c) = (t / 16, t % 16) of every block of a level (blocks in registers).
+  {
+    const int r = tid >> 4, c = tid & 15;
+#pragma unroll
+    for (int dist = 1; dist < 4; ++dist) {
+      double x[3];
+#pragma unroll
+      for (int blk = 0; blk < 4 - dist; ++blk) {
+        const int bI = blk + dist, bJ = blk;
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int K = bJ; K < bI; ++K) {
+          const double* lrow = Ls + (16 * K) * LDS_P + 16 * bI + r;
+          const double* wcol = Wt + (16 * bJ + c) * LDS_P + 16 * K;
+#pragma unroll
+          for (int kk = 0; kk < 16; ++kk) acc[kk & 3] = fma(lrow[kk * LDS_P], wcol[kk], acc[kk & 3]);
+        }
+        x[blk] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+      }
+#pragma unroll
+      for (int blk = 0; blk < 4 - dist; ++blk) Xs[blk * 256 + r * 16 + c] = x[blk];
+      __syncthreads();
+#pragma unroll
+      for (int blk = 0; blk < 4 - dist; ++blk) {
+        const int bI = blk + dist, bJ = blk;
+        const double* wrow = Wt + (16 * bI) * LDS_P + 16 * bI + r;
+        const double* xcol = Xs + blk * 256 + c;
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int mm = 0; mm < 16; ++mm) acc[mm & 3] = fma(wrow[mm * LDS_P], xcol[mm * 16], acc[mm & 3]);
+        Wt[(16 * bJ + c) * LDS_P + 16 * bI + r] = -((acc[0] + acc[1]) + (acc[2] + acc[3]));
+      }
+      __syncthreads();
+    }
+  }
+  if (tid == 0) g_ph6[4] = clock64();
+  for (int idx = tid; idx < PB * PB; idx += 256) {
+    const int rr = idx % PB, c = idx / PB;
+    a[(int64_t)c * lda + rr] = (rr > c) ? colA[c * LDS6 + rr] * ilj[c] : (rr == c ? lj[c] : 0.0);
+    g_W6[c * PB + rr] = (rr >= c) ? Wt[c * LDS_P + rr] * ilj[rr] : 0.0;
+  }
+  __syncthreads();
+  if (tid == 0) g_ph6[5] = clock64();
+}
+
 template <int V>
 void run(const char* name, double* a, int64_t lda) {
   const int smem = 2 * PB * LDS_P * sizeof(double);
@@ -462,6 +602,8 @@ void run(const char* name, double* a, int64_t lda) {
   cudaFuncSetAttribute(potrf_2d2, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaFuncSetAttribute(potrf_2d3, cudaFuncAttributeMaxDynamicSharedMemorySize, smem + 256 * 4 * 8);
   cudaFuncSetAttribute(potrf_2d4, cudaFuncAttributeMaxDynamicSharedMemorySize, smem + 7 * 256 * 8 + PB * LDS_P * 8);
+  cudaFuncSetAttribute(potrf_2d6, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       smem + 7 * 256 * 8 + PB * LDS_P * 8 + 64 * 8);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
@@ -469,7 +611,8 @@ void run(const char* name, double* a, int64_t lda) {
   for (int rep = 0; rep < 20; ++rep) {
     make_spd<<<64, 256>>>(a, lda, 64);
     cudaEventRecord(e0);
-    if (V == 5) potrf_2d4<<<1, 256, smem + 7 * 256 * 8 + PB * LDS_P * 8>>>(a, lda);
+    if (V == 6) potrf_2d6<<<1, 256, smem + 7 * 256 * 8 + PB * LDS_P * 8 + 64 * 8>>>(a, lda);
+    else if (V == 5) potrf_2d4<<<1, 256, smem + 7 * 256 * 8 + PB * LDS_P * 8>>>(a, lda);
     else if (V == 4) potrf_2d3<<<1, 256, smem + 256 * 4 * 8>>>(a, lda);
     else if (V == 3) potrf_2d2<<<1, 256, smem>>>(a, lda);
     else if (V == 2) potrf_2d<<<1, 256, smem>>>(a, lda);
@@ -549,6 +692,27 @@ int main() {
     printf("V5 phases (cycles): init+load %lld, factor loop %lld (%.0f/step), diag inverses %lld, off-diag %lld, write-out %lld\n",
            ph[1] - ph[0], ph[2] - ph[1], (ph[2] - ph[1]) / 64.0, ph[3] - ph[2], ph[4] - ph[3], ph[5] - ph[4]);
   }
+  run<6>("2-D factor-only, columns 4tc+k, unrolled by 4 + blocked inverse", a, lda);
+  {
+    std::vector<double> L6(64 * 64), W(64 * 64);
+    cudaMemcpy2D(L6.data(), 64 * 8, a, lda * 8, 64 * 8, 64, cudaMemcpyDeviceToHost);
+    cudaMemcpyFromSymbol(W.data(), g_W6, sizeof(double) * 64 * 64);
+    int dl = 0;
+    double e2 = 0;
+    for (int c = 0; c < 64; ++c)
+      for (int r = c; r < 64; ++r) dl += L6[c * 64 + r] != h2[c * 64 + r];
+    for (int i = 0; i < 64; ++i)
+      for (int j = 0; j < 64; ++j) {
+        double s2 = 0;
+        for (int k = 0; k < 64; ++k) s2 += W[k * 64 + i] * (j <= k ? L6[j * 64 + k] : 0.0);
+        e2 = std::fmax(e2, std::fabs(s2 - (i == j ? 1.0 : 0.0)));
+      }
+    long long ph[6];
+    cudaMemcpyFromSymbol(ph, g_ph6, sizeof(ph));
+    printf("V6 check: L entries differing from V5: %d, max|WL-I|=%.3e; phases: init %lld, loop %lld (%.0f/step), diag inv %lld, off-diag %lld, out %lld\n",
+           dl, e2, ph[1] - ph[0], ph[2] - ph[1], (ph[2] - ph[1]) / 64.0, ph[3] - ph[2], ph[4] - ph[3], ph[5] - ph[4]);
+  }
+
   printf("err=%s\n", cudaGetErrorString(cudaGetLastError()));
   return 0;
 }

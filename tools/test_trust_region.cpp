@@ -57,6 +57,18 @@ int main() {
          return f * (1.0 + 1e-14 * u);
        },
        {0.5, 0.5, 0.5}, {-2.0, -2.0, -2.0}, {2.0, 2.0, 2.0}, {0.2, -0.1, 0.3}, 1e-5, 300},
+      {"3d quadratic + 1e-10 relative noise, above the noise floor (must terminate)",
+       [](const std::vector<double>& x) {
+         static unsigned long long st = 1234567891011ull;
+         st ^= st << 13;
+         st ^= st >> 7;
+         st ^= st << 17;
+         const double u = (double)(st >> 11) * 0x1.0p-53 - 0.5;
+         const double f = 300.0 + 800.0 * ((x[0] - 0.2) * (x[0] - 0.2) + 2 * (x[1] + 0.1) * (x[1] + 0.1) +
+                                          (x[2] - 0.3) * (x[2] - 0.3));
+         return f * (1.0 + 1e-10 * u);
+       },
+       {0.5, 0.5, 0.5}, {-2.0, -2.0, -2.0}, {2.0, 2.0, 2.0}, {0.2, -0.1, 0.3}, 1e-4, 400},
       {"3d log-likelihood-like (exp terms)",
        [](const std::vector<double>& x) {
          return std::exp(x[0]) - x[0] + std::exp(0.5 * x[1]) - 0.5 * x[1] + std::cosh(x[2] - 0.4) + 0.2 * x[0] * x[1];
@@ -71,8 +83,8 @@ int main() {
       a = std::log(1 - 0.2 * b);
       b = 2 * std::log(1 - 0.4 * a);
     }
-    cases[6].xstar = {a, b, 0.4};
-    cases[6].tol = 1e-5;
+    cases[7].xstar = {a, b, 0.4};
+    cases[7].tol = 1e-5;
   }
   int fails = 0;
   for (auto& c : cases) {
