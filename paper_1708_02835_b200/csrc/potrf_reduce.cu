@@ -23,6 +23,13 @@ namespace exageo {
 namespace {
 
 constexpr int LDS_P = PB + 1;  // odd stride: conflict-free column access
+
+// c (8 x 8, two per lane) += a (8 x 4 row fragment) * b (4 x 8 column fragment), FP64 DMMA
+__device__ __forceinline__ void dmma64(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
 constexpr int LDS_A = PB + 2;  // even stride: 16-byte aligned double2 rows of colA
 
 // 256 threads as a 16 x 16 grid: thread (tr, tc) holds a_rc for rows r = tr + 16 i and
@@ -61,19 +68,13 @@ __global__ void __launch_bounds__(256) potrf_block_kernel(double* __restrict__ a
 #pragma unroll
     for (int i = 0; i < 4; ++i) colA[tr + 16 * i] = v[i][0];  // column 0
   }
-  int bad = -1;
-  for (int m = 0; m < PB / 4 && bad < 0; ++m) {
+  for (int m = 0; m < PB / 4; ++m) {
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const int j = 4 * m + u;
       __syncthreads();
       const double* cj = colA + j * LDS_A;
-      const double d = cj[j];
-      if (!(d > 0.0)) {  // uniform: every thread reads the same pivot
-        bad = j;
-        break;
-      }
-      const double rd = __drcp_rn(d);
+      const double rd = __drcp_rn(cj[j]);  // a bad pivot is found by the scan after the loop
       double f[4];
 #pragma unroll
       for (int i = 0; i < 4; ++i) f[i] = (tr + 16 * i > j) ? cj[tr + 16 * i] * rd : 0.0;
@@ -92,11 +93,17 @@ __global__ void __launch_bounds__(256) potrf_block_kernel(double* __restrict__ a
       }
     }
   }
-  if (bad >= 0) {
-    if (tid == 0) *info = (int)(pivot_base + bad + 1);
+  __syncthreads();
+  // first non-positive (or NaN) pivot: d_j as used at step j; later pivots may be garbage
+  __shared__ int badj;
+  if (tid == 0) badj = PB;
+  __syncthreads();
+  if (tid < PB && !(colA[tid * LDS_A + tid] > 0.0)) atomicMin(&badj, tid);
+  __syncthreads();
+  if (badj < PB) {
+    if (tid == 0) *info = (int)(pivot_base + badj + 1);
     return;
   }
-  __syncthreads();
   // L_jj = sqrt(d_j), 1 / L_jj; sum log L_jj = sum log(d_j) / 2 by a fixed two-level tree
   if (tid < PB) {
     const double dj = colA[tid * LDS_A + tid];
@@ -130,36 +137,60 @@ __global__ void __launch_bounds__(256) potrf_block_kernel(double* __restrict__ a
     }
   }
   __syncthreads();
-  {  // off-diagonal blocks by distance; thread t owns entry (t / 16, t % 16) of each block
-    const int r = tid >> 4, c = tid & 15;
-#pragma unroll
+  {  // off-diagonal blocks by distance on the FP64 tensor cores: warp blk owns block
+    // (I, J) = (blk + dist, blk): X = sum_K L~_IK w~_KJ, then w~_IJ = -w~_II X, each a
+    // 16 x 16 product of 2 x 2 m8n8k4 tiles (A row fragments, B column fragments)
+    const int warp = tid >> 5, lane = tid & 31, fr = lane >> 2, fk = lane & 3;
+    double* Xw = Xs + warp * 256;  // this warp's X, column-major 16 x 16 (ld 16)
+#pragma unroll 1
     for (int dist = 1; dist < 4; ++dist) {
-      double x[3];
-#pragma unroll
-      for (int blk = 0; blk < 4 - dist; ++blk) {
-        const int bI = blk + dist, bJ = blk;
-        double acc[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
+      if (warp < 4 - dist) {
+        const int bI = warp + dist, bJ = warp;
+        double acc[2][2][2] = {};
+#pragma unroll 1
         for (int K = bJ; K < bI; ++K) {
-          const double* lrow = Ls + (16 * K) * LDS_P + 16 * bI + r;
-          const double* wcol = Wt + (16 * bJ + c) * LDS_P + 16 * K;
 #pragma unroll
-          for (int kk = 0; kk < 16; ++kk) acc[kk & 3] = fma(lrow[kk * LDS_P], wcol[kk], acc[kk & 3]);
+          for (int kk = 0; kk < 16; kk += 4) {
+            double af[2], bf[2];
+#pragma unroll
+            for (int t = 0; t < 2; ++t) {
+              af[t] = Ls[(16 * K + kk + fk) * LDS_P + 16 * bI + 8 * t + fr];   // L~[m][k]
+              bf[t] = Wt[(16 * bJ + 8 * t + fr) * LDS_P + 16 * K + kk + fk];   // w~[k][n]
+            }
+#pragma unroll
+            for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+              for (int nt = 0; nt < 2; ++nt) dmma64(acc[mt][nt], af[mt], bf[nt]);
+          }
         }
-        x[blk] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
-      }
 #pragma unroll
-      for (int blk = 0; blk < 4 - dist; ++blk) Xs[blk * 256 + r * 16 + c] = x[blk];
-      __syncthreads();
+        for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-      for (int blk = 0; blk < 4 - dist; ++blk) {
-        const int bI = blk + dist, bJ = blk;
-        const double* wrow = Wt + (16 * bI) * LDS_P + 16 * bI + r;
-        const double* xcol = Xs + blk * 256 + c;
-        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+          for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
-        for (int mm = 0; mm < 16; ++mm) acc[mm & 3] = fma(wrow[mm * LDS_P], xcol[mm * 16], acc[mm & 3]);
-        Wt[(16 * bJ + c) * LDS_P + 16 * bI + r] = -((acc[0] + acc[1]) + (acc[2] + acc[3]));
+            for (int e = 0; e < 2; ++e) Xw[(8 * nt + 2 * fk + e) * 16 + 8 * mt + fr] = acc[mt][nt][e];
+        __syncwarp();
+        double acc2[2][2][2] = {};
+#pragma unroll
+        for (int kk = 0; kk < 16; kk += 4) {
+          double af[2], bf[2];
+#pragma unroll
+          for (int t = 0; t < 2; ++t) {
+            af[t] = Wt[(16 * bI + kk + fk) * LDS_P + 16 * bI + 8 * t + fr];  // w~_II[m][k]
+            bf[t] = Xw[(8 * t + fr) * 16 + kk + fk];                           // X[k][n]
+          }
+#pragma unroll
+          for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt) dmma64(acc2[mt][nt], af[mt], bf[nt]);
+        }
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+            for (int e = 0; e < 2; ++e)
+              Wt[(16 * bJ + 8 * nt + 2 * fk + e) * LDS_P + 16 * bI + 8 * mt + fr] = -acc2[mt][nt][e];
       }
       __syncthreads();
     }
