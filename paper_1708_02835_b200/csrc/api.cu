@@ -245,6 +245,13 @@ void factor_panel(exageo_ctx* c, RankState& R, int k, cudaStream_t s) {
   const int m = (k - L.rank) / L.world;  // local panel index
   for (int sb = 0; sb < nsub; ++sb) {
     const int64_t c0 = (int64_t)sb * PB;
+    if ((int64_t)k * L.nb + c0 >= L.n) {
+      // the rest of the (last) panel is identity padding (R12): generated as I with zero
+      // rows/columns around it and never touched by an update, it already is its own factor
+      // (L = I, log L_ii = 0) -- skip its POTRF/TRSM/GEMM launches
+      cudaMemsetAsync(R.slots + (int64_t)m * nsub + sb, 0, sizeof(double) * (nsub - sb), s);
+      break;
+    }
     if (sb > 0) {
       launch_gemm_panel(ldk - c0, PB, (int)c0, Pk + c0, ldk, Pk + c0, ldk, Pk + c0 * ldk + c0, ldk, true, R.info, s);
       c->kernels += 1;
