@@ -252,14 +252,19 @@ void factor_panel(exageo_ctx* c, RankState& R, int k, cudaStream_t s) {
       cudaMemsetAsync(R.slots + (int64_t)m * nsub + sb, 0, sizeof(double) * (nsub - sb), s);
       break;
     }
+    // at small n the panel chain is the critical path: its kernels use programmatic
+    // dependent launch (each launches while its predecessor runs and waits on the device)
+    const bool pdl = L.n <= 32768;
+    const bool first = sb == 0;  // follows U1 / an event wait: ordinary launch
     if (sb > 0) {
-      launch_gemm_panel(ldk - c0, PB, (int)c0, Pk + c0, ldk, Pk + c0, ldk, Pk + c0 * ldk + c0, ldk, true, R.info, s);
+      launch_gemm_panel(ldk - c0, PB, (int)c0, Pk + c0, ldk, Pk + c0, ldk, Pk + c0 * ldk + c0, ldk, true, R.info, s,
+                        pdl);
       c->kernels += 1;
     }
     launch_potrf_block(Pk + c0 * ldk + c0, ldk, R.W, R.slots + (int64_t)m * nsub + sb, R.info,
-                       (int64_t)k * L.nb + c0, s);
+                       (int64_t)k * L.nb + c0, s, pdl && !first);
     double* below = Pk + c0 * ldk + c0 + PB;
-    launch_gemm_panel(ldk - c0 - PB, PB, PB, below, ldk, R.W, PB, below, ldk, false, R.info, s);
+    launch_gemm_panel(ldk - c0 - PB, PB, PB, below, ldk, R.W, PB, below, ldk, false, R.info, s, pdl);
     c->kernels += 2;
   }
 }

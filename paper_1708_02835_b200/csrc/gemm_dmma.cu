@@ -23,7 +23,7 @@ cudaError_t gemm_init() {
 }
 
 void launch_gemm_panel(int64_t M, int N, int K, const double* A, int64_t lda, const double* B, int64_t ldb,
-                       double* C, int64_t ldc, bool accumulate, const int* info, cudaStream_t s) {
+                       double* C, int64_t ldc, bool accumulate, const int* info, cudaStream_t s, bool pdl) {
   if (M <= 0 || N <= 0 || K <= 0) return;
   DenseMap map;
   map.A = A;
@@ -36,8 +36,8 @@ void launch_gemm_panel(int64_t M, int N, int K, const double* A, int64_t lda, co
   map.N = N;
   map.K = K;
   map.mblocks = (int)((M + PanelCfg::BM - 1) / PanelCfg::BM);
-  if (accumulate) launch<PanelCfg, true, DenseMap, true>(map, info, s);
-  else launch<PanelCfg, false>(map, info, s);
+  if (accumulate) launch<PanelCfg, true, DenseMap, true>(map, info, s, pdl);
+  else launch<PanelCfg, false>(map, info, s, pdl);
 }
 
 // super-panel size of the trailing update (single rank); EXAGEO_SYRK_GROUP overrides (tuning)

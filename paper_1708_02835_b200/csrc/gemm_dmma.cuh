@@ -204,6 +204,10 @@ __global__ void __launch_bounds__(C::NT, C::MINB) gemm_nt_dmma(Map map, const in
   static_assert(BK % 4 == 0 && WM % 8 == 0 && WN % 8 == 0, "tile shape");
   static_assert((LDA_S % 16) == 4 && (LDB_S % 16) == 4, "conflict-free fragment loads");
 
+  // programmatic dependent launch (panel kernels at small n): wait for the preceding kernel
+  // of the stream before touching memory, then let the next one launch and wait in turn
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   GemmTile t;
   if (!map.template operator()<BM, BN>((int64_t)blockIdx.x, t)) return;
 
@@ -322,10 +326,24 @@ cudaError_t set_smem() {
 }
 
 template <class C, bool ACC, class Map, bool PRE = false>
-void launch(const Map& map, const int* info, cudaStream_t s) {
+void launch(const Map& map, const int* info, cudaStream_t s, bool pdl = false) {
   const int64_t nblk = map.blocks(C::BM, C::BN);
   if (nblk <= 0) return;
-  gemm_nt_dmma<C, ACC, Map, PRE><<<(unsigned)nblk, C::NT, C::SMEM, s>>>(map, info);
+  if (!pdl) {
+    gemm_nt_dmma<C, ACC, Map, PRE><<<(unsigned)nblk, C::NT, C::SMEM, s>>>(map, info);
+    return;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)nblk);
+  cfg.blockDim = dim3(C::NT);
+  cfg.dynamicSmemBytes = C::SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, gemm_nt_dmma<C, ACC, Map, PRE>, map, info);
 }
 
 }  // namespace gemm

@@ -109,7 +109,8 @@ void launch_matern_dense(const MaternConsts& mc, int64_t m, const double* x1, co
 // C (M x N, ldc) =     A (M x K, lda) * B (N x K, ldb)^T      (accumulate = false; may alias A when N == K <= 64)
 // Variant tuned for N = 64 panel columns.
 void launch_gemm_panel(int64_t M, int N, int K, const double* A, int64_t lda, const double* B, int64_t ldb,
-                       double* C, int64_t ldc, bool accumulate, const int* info, cudaStream_t s);
+                       double* C, int64_t ldc, bool accumulate, const int* info, cudaStream_t s,
+                       bool pdl = false);
 // Trailing update by panel k (operand Pk, leading dimension ld(k): a rank's own panel k
 // or its received copy) of the owned panels J0, J0 + world, ..., (npan of them):
 // A_rc -= sum_t L_rt L_ct for every lower element and the z row of those panels.
@@ -118,7 +119,8 @@ void launch_syrk_panels(const Layout& L, double* ws, const double* Pk, int k, in
 // Factor the PB x PB diagonal block at `a` (ld) in place, write W = L^{-1} (PB x PB,
 // ld PB) and slot = sum log L_ii; info = first bad global pivot + 1.
 void launch_potrf_block(double* a, int64_t lda, double* W, double* logdet_slot, int* info, int64_t pivot_base,
-                        cudaStream_t s);
+                        cudaStream_t s,
+                        bool pdl = false);
 // out2 = {sum of this rank's log-det partials (nslots), sum of y_c^2 over this rank's columns};
 // scratch: kQuadBlocks doubles.
 void launch_local_partials(const Layout& L, const double* ws, const double* slots, int nslots, double* scratch,

@@ -48,6 +48,8 @@ constexpr int kPotrfSmemDoubles = PB * LDS_A + PB * LDS_P + 3 * 256 + PB * LDS_P
 __global__ void __launch_bounds__(256) potrf_block_kernel(double* __restrict__ a, int64_t lda,
                                                           double* __restrict__ W, double* __restrict__ slot,
                                                           int* __restrict__ info, int64_t pivot_base) {
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");  // programmatic dependent launch
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   if (*(volatile int*)info != 0) return;
   extern __shared__ double smem_p[];
   double* colA = smem_p;             // colA[c * LDS_A + r] = a_rc at step c (unscaled)
@@ -346,8 +348,22 @@ cudaError_t potrf_init() {
 }
 
 void launch_potrf_block(double* a, int64_t lda, double* W, double* slot, int* info, int64_t pivot_base,
-                        cudaStream_t s) {
-  potrf_block_kernel<<<1, 256, kPotrfSmem, s>>>(a, lda, W, slot, info, pivot_base);
+                        cudaStream_t s, bool pdl) {
+  if (!pdl) {
+    potrf_block_kernel<<<1, 256, kPotrfSmem, s>>>(a, lda, W, slot, info, pivot_base);
+    return;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(1);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = kPotrfSmem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, potrf_block_kernel, a, lda, W, slot, info, pivot_base);
 }
 
 void launch_local_partials(const Layout& L, const double* ws, const double* slots, int nslots, double* scratch,
