@@ -64,11 +64,12 @@ void run(const char* name, const Layout& L, double* ws, int k, int reps, int gro
 
 int main(int argc, char** argv) {
   const int64_t n = argc > 1 ? atoll(argv[1]) : 40000;
+  const int nb = argc > 2 ? atoi(argv[2]) : 512;
   Layout L;
   L.n = n;
-  L.nb = 512;
-  L.T = (int)((n + 511) / 512);
-  L.N = (int64_t)L.T * 512;
+  L.nb = nb;
+  L.T = (int)((n + nb - 1) / nb);
+  L.N = (int64_t)L.T * nb;
   double* ws;
   const size_t bytes = (size_t)L.total() * 8 + 4096;
   if (cudaMalloc(&ws, bytes) != cudaSuccess) {
@@ -78,12 +79,13 @@ int main(int argc, char** argv) {
   fill<<<1024, 256>>>(ws, (int64_t)(bytes / 8));
   cudaDeviceSynchronize();
   printf("n=%lld T=%d workspace %.2f GB\n", (long long)n, L.T, bytes / 1e9);
-  for (int k : {0, L.T / 2}) {
-    for (int g : {1, 2, 4, 8, 16}) {
-      char name[64];
-      snprintf(name, sizeof(name), "64x64x16 st2 preC, super panels of %d", g);
-      run<Cfg<64, 64, 16, 2, 2, 2, 4>, 2>(name, L, ws, k, 3, g);
-    }
+  for (int k : {0, L.T / 2, (3 * L.T) / 4}) {
+    run<Cfg<64, 64, 16, 2, 2, 2, 4>, 2>("64x64x16 st2 preC (product)", L, ws, k, 3, 8);
+    run<Cfg<64, 64, 16, 2, 2, 3, 4>, 2>("64x64x16 st3 preC", L, ws, k, 3, 8);
+    run<Cfg<64, 64, 32, 2, 2, 2, 3>, 2>("64x64x32 st2 preC", L, ws, k, 3, 8);
+    run<Cfg<64, 64, 8, 2, 2, 4, 4>, 2>("64x64x8 st4 preC", L, ws, k, 3, 8);
+    run<Cfg<64, 64, 16, 2, 2, 2, 5>, 2>("64x64x16 st2 preC 5 CTA", L, ws, k, 3, 8);
+    run<Cfg<128, 64, 16, 2, 2, 2, 2>, 2>("128x64x16 st2 preC", L, ws, k, 3, 8);
   }
   return 0;
 }
