@@ -202,3 +202,21 @@ def test_mle_monte_carlo_median_near_truth(ctx):
         est.append(th)
     med = np.median(np.array(est), axis=0)
     assert abs(med[0] - 1.0) < 0.25 and abs(med[1] - 0.1) < 0.025 and abs(med[2] - 0.7) < 0.07, med
+
+
+def test_mle_trust_region_one_and_zero_free_parameters(ctx):
+    n = 600
+    x, y = ex.gen_locations(n, 6)
+    z = oracle.simulate(x, y, (1.0, 0.1, 0.8), si.normals(n, 6))
+    # profiled, beta fixed: a 1-D trust-region search over nu
+    lo, hi = (0.01, 0.1, 0.1), (5.0, 0.1, 2.0)
+    t1, l1, _, _ = ctx.mle(x, y, z, lo, hi, (1.0, 0.1, 0.5), xtol_rel=1e-8, profile=True, method="trust-region")
+    t2, l2, _, _ = ctx.mle(x, y, z, lo, hi, (1.0, 0.1, 0.5), xtol_rel=1e-8, profile=True)
+    assert t1[1] == 0.1 and t2[1] == 0.1
+    assert t1[2] == pytest.approx(t2[2], rel=1e-5) and l1 >= l2 - 1e-9 * abs(l2)
+    # profiled with beta and nu fixed: no search at all, theta1 = clamp(q / n) in closed form
+    lo, hi = (0.01, 0.1, 0.8), (5.0, 0.1, 0.8)
+    t3, l3, ne, _ = ctx.mle(x, y, z, lo, hi, (1.0, 0.1, 0.8), profile=True, method="trust-region")
+    assert ne == 1 and t3[1:] == (0.1, 0.8)
+    assert t3[0] == pytest.approx(oracle.profile_sigma2(x, y, z, 0.1, 0.8), rel=1e-10)
+    assert l3 == pytest.approx(ctx.loglik(x, y, z, t3).loglik, rel=1e-12)
