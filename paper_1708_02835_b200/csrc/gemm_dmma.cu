@@ -40,14 +40,19 @@ void launch_gemm_panel(int64_t M, int N, int K, const double* A, int64_t lda, co
   else launch<PanelCfg, false>(map, info, s, pdl);
 }
 
-// super-panel size of the trailing update (single rank); EXAGEO_SYRK_GROUP overrides (tuning)
-int syrk_group() {
-  static const int g = [] {
+// super-panel size of the trailing update (single rank): the super panel's B operand
+// (group * nb rows of panel k, group * nb^2 doubles) is kept near 16 MB so it stays
+// L2-resident (nb = 512: 8 panels; nb = 1024: 2; measured: 8 x 1024 = 64 MB thrashes and
+// re-reads 225 GB per U2(0) at n = 100k). EXAGEO_SYRK_GROUP overrides (tuning).
+int syrk_group(int nb) {
+  static const int forced = [] {
     const char* e = getenv("EXAGEO_SYRK_GROUP");
-    const int v = e ? atoi(e) : 8;
-    return v >= 1 && v <= 64 ? v : 8;
+    const int v = e ? atoi(e) : 0;
+    return v >= 1 && v <= 64 ? v : 0;
   }();
-  return g;
+  if (forced) return forced;
+  const int64_t g = ((int64_t)2 << 20) / ((int64_t)nb * nb);  // 2 Mi doubles = 16 MiB
+  return (int)(g < 1 ? 1 : (g > 8 ? 8 : g));
 }
 
 void launch_syrk_panels(const Layout& L, double* ws, const double* Pk, int k, int J0, int npan, const int* info,
@@ -61,7 +66,7 @@ void launch_syrk_panels(const Layout& L, double* ws, const double* Pk, int k, in
   map.J0 = J0;
   map.npan = npan;
   map.row_end = (int64_t)L.sb_end(k) * L.nb;  // N unless IND
-  map.group = L.world == 1 ? syrk_group() : 1;     // super panels: panel k's rows read once per 8 panels
+  map.group = L.world == 1 ? syrk_group(L.nb) : 1;  // super panels: panel k's rows read once per group
   launch<TrailCfg, true, SyrkMap, true>(map, info, s);
 }
 

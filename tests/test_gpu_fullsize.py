@@ -1,4 +1,4 @@
-"""Full-size GPU parity at BASELINE's headline size (n = 100k, nb = 512, the launch
+"""Full-size GPU parity at BASELINE's headline size (n = 100k, nb = 1024, the launch
 configuration bench.py times), where the O(n^3) oracle cannot run:
 
   * AR(1) / Kac-Murdock-Szego closed form of l (exact in O(n), nu = 1/2, collinear sites);
@@ -47,7 +47,7 @@ def test_ar1_closed_form_full_size(ctx):
     x, y = si.collinear_sites(N, h)
     z = si.normals(N, 5)
     r = ctx.loglik(x, y, z, (t1, t2, 0.5))
-    assert r.info["nb"] == 512 and r.info["ntiles"] == 196
+    assert r.info["nb"] == 1024 and r.info["ntiles"] == 98  # the bench's launch configuration
     rho = math.exp(-h / t2)
     logdet = N * math.log(t1) + (N - 1) * math.log1p(-rho * rho)
     w = np.empty(N)

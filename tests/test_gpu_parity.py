@@ -102,7 +102,8 @@ def test_generated_panels_match_oracle(n, nb, nu, beta):
 
 @pytest.mark.parametrize("n,nb,theta", [(700, 128, (1.0, 0.1, 0.5)), (1000, 256, (1.0, 0.1, 1.0)),
                                         (1100, 128, (1.5, 0.05, 1.5)), (257, 128, (1.0, 0.2, 0.9)),
-                                        (1300, 384, (1.0, 0.1, 0.7)), (2000, 384, (1.2, 0.08, 0.5))])
+                                        (1300, 384, (1.0, 0.1, 0.7)), (2000, 384, (1.2, 0.08, 0.5)),
+                                        (2500, 1024, (1.0, 0.1, 0.5)), (4500, 2048, (1.0, 0.1, 0.6))])
 def test_factor_and_solve_match_oracle(n, nb, theta):
     c = ex.Context(device=0, nb=nb)
     x, y = ex.gen_locations(n, 7)

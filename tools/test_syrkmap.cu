@@ -129,7 +129,7 @@ int check_offsets(int T, int nb, int world) {
 
 int main() {
   int bad = 0, n = 0;
-  for (int nb : {128, 256, 384, 512})
+  for (int nb : {128, 256, 384, 512, 1024, 2048})
     for (int T : {2, 3, 7, 20})
       for (int world : {1, 2, 3, 4, 8}) {
         bad += check_offsets(T, nb, world);
@@ -173,7 +173,7 @@ int main() {
   bad += check<64, 64>(586, 512, 8, 3, 5, 11, 72);
   // super panels (single rank): group consecutive panels enumerated as one wide panel
   for (int group : {2, 3, 8})
-    for (int nb : {128, 256, 384, 512})
+    for (int nb : {128, 256, 384, 512, 1024, 2048})
       for (int T : {2, 5, 20, 37})
         for (int k = 0; k + 2 <= T; ++k) {
           for (int J0 : {k + 1, k + 2}) {
