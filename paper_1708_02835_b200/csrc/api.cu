@@ -66,9 +66,10 @@ bool theta_ok(const exageo_theta* t) {
 // Tile size by n (tools/nb_sweep.py on B200): small n is bound by the panel critical
 // path (smaller tiles = shorter POTRF chains), large n by the trailing-update efficiency.
 // automatic tile size (tools/nb_sweep.py with the current kernels: 128 up to 12k, then 256,
-// 384 from 15k, 512 from 21k, 1024 from 90k; the differences near the switches are 1-4%)
+// 384 from 15k, 512 from 21k, 1024 from 48k: 1024 wins at 50/60/90/100k by 1.4-1.7% and
+// loses at 70/80k by 0.3-0.6%; the differences near the other switches are 1-4%)
 int auto_nb(int64_t n) {
-  if (n >= 90000) return 1024;
+  if (n >= 48000) return 1024;
   if (n >= 21000) return 512;
   if (n >= 15000) return 384;
   if (n >= 12000) return 256;
