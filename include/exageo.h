@@ -56,7 +56,7 @@ typedef struct exageo_ctx exageo_ctx;
 typedef struct {
   int device;   /* CUDA device ordinal                                               */
   int nb;       /* tile size (multiple of 128); 0 = automatic (128 below n = 12k, 256 below 15k,
-                   384 below 21k, 512 below 48k, else 1024)                          */
+                   384 below 21k, 512 below 48k, else 1024; 512 for world > 1)                          */
   void* stream; /* cudaStream_t to run on; NULL = the library creates its own stream */
   /* Distribution: the tile panels are dealt 1-D block-cyclically over
    * `world` ranks (panel j on rank j % world), factored with a panel broadcast per step

@@ -68,8 +68,8 @@ bool theta_ok(const exageo_theta* t) {
 // automatic tile size (tools/nb_sweep.py with the current kernels: 128 up to 12k, then 256,
 // 384 from 15k, 512 from 21k, 1024 from 48k: 1024 wins at 50/60/90/100k by 1.4-1.7% and
 // loses at 70/80k by 0.3-0.6%; the differences near the other switches are 1-4%)
-int auto_nb(int64_t n) {
-  if (n >= 48000) return 1024;
+int auto_nb(int64_t n, int world = 1) {
+  if (n >= 48000) return world > 1 ? 512 : 1024;  // distributed: more panels balance the ranks
   if (n >= 21000) return 512;
   if (n >= 15000) return 384;
   if (n >= 12000) return 256;
@@ -212,7 +212,7 @@ exageo_status ensure_buffers(exageo_ctx* c) {
 exageo_status prepare_generate(exageo_ctx* c, const exageo_theta* t, int64_t n, const double* x, const double* y) {
   if (!theta_ok(t)) return fail(c, EXAGEO_EINVAL, "theta must be finite and > 0");
   if (n < 1 || !x || !y) return fail(c, EXAGEO_EINVAL, "n < 1 or NULL location array");
-  const int nb = c->nb_opt > 0 ? c->nb_opt : auto_nb(n);
+  const int nb = c->nb_opt > 0 ? c->nb_opt : auto_nb(n, c->world);
   c->G = make_layout(n, nb, 0, 1, c->ind);
   for (size_t i = 0; i < c->rs.size(); ++i) {
     const int rank = c->virt ? (int)i : c->rank;
@@ -983,7 +983,7 @@ exageo_status exageo_predict(exageo_ctx* c, const exageo_theta* t, int64_t n, co
     return fail(c, EXAGEO_EINVAL, "n < 1, m < 1 or NULL array");
   if (!theta_ok(t)) return fail(c, EXAGEO_EINVAL, "theta must be finite and > 0");
   CUDA_TRY(c, cudaSetDevice(c->device));
-  const int nb = c->nb_opt > 0 ? c->nb_opt : auto_nb(n);
+  const int nb = c->nb_opt > 0 ? c->nb_opt : auto_nb(n, c->world);
   const Layout G0 = make_layout(n, nb);
   // device scratch: x, y, z (n each), xnew, ynew, znew (m each), w (N), solve and krige partials
   const size_t nw = (size_t)G0.N;

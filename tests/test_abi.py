@@ -37,7 +37,9 @@ def test_strerror_and_workspace_size():
     N = T * nb
     expect = 8 * nb * sum(N - nb * j + 128 for j in range(T)) + 256 * 8
     assert ex.workspace_bytes(100_000, 512) == expect
-    assert ex.workspace_bytes(100_000) == expect  # auto nb = 512 at n >= 30k
+    T2, nb2 = 98, 1024  # auto nb = 1024 at n >= 48k (single GPU)
+    N2 = T2 * nb2
+    assert ex.workspace_bytes(100_000) == 8 * nb2 * sum(N2 - nb2 * j + 128 for j in range(T2)) + 256 * 8
 
 
 @pytest.mark.parametrize("n,seed", [(1, 1), (2, 9), (400, 1), (401, 3), (1600, 1), (9999, 77), (100_000, 1)])
