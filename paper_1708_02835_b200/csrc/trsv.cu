@@ -32,6 +32,7 @@ __global__ void __launch_bounds__(256) gemv_t_kernel(const double* __restrict__ 
   double acc[kColsPerCta];
 #pragma unroll
   for (int q = 0; q < kColsPerCta; ++q) acc[q] = 0.0;
+#pragma unroll 4  // several rows' loads in flight per thread (the loop is HBM-latency bound)
   for (int64_t r = r_lo + threadIdx.x; r < r_hi; r += blockDim.x) {
     const double wr = w[row0 + r];
 #pragma unroll
