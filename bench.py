@@ -37,10 +37,37 @@ METRIC = "loglik evals/sec at n=100k (1 GPU)"
 UNIT = "evals/s"
 THETA = (1.0, 0.1, 0.5)
 SEED = 1
-# Peak FP64 (DMMA) of this B200: measured by tools/probes/fp64_peak.cu (sustained
-# DMMA.8x8x4 loop, 148 SMs at 1965 MHz) = 148 * 128 flop/clk * 1.965 GHz.
-FP64_PEAK_TFLOPS = 37.2
-FP64_PEAK_SOURCE = "measured: tools/probes/fp64_peak.cu sustained DMMA (= 148 SM x 128 flop/clk x 1.965 GHz)"
+
+
+def fp64_peaks():
+    """FP64 roofline denominators measured on this pool's B200 by tools/fp64_peak.sh and
+    committed as profiles/fp64_peak.txt (MEASURED_PEAKS.json has no FP64 entry): the
+    sustained DMMA.8x8x4 loop and cuBLAS DGEMM 8192^3 as the vendor yardstick."""
+    path = os.path.join(ROOT, "profiles", "fp64_peak.txt")
+    dmma, dgemm, clocks = None, None, None
+    for line in open(path):
+        if line.startswith("DMMA sustained:"):
+            dmma = float(line.split(":")[1].split()[0])
+        elif line.startswith("cublas dgemm 8192^3:"):
+            dgemm = float(line.split(":")[1].split()[0])
+        elif line.startswith("clocks:"):
+            clocks = line.strip()
+    if dmma is None or dgemm is None:
+        raise RuntimeError(f"{path}: DMMA / DGEMM lines missing (run tools/fp64_peak.sh on a B200)")
+    return dmma, dgemm, f"measured: profiles/fp64_peak.txt (tools/fp64_peak.sh; {clocks})"
+
+
+FP64_PEAK_TFLOPS, DGEMM_TFLOPS, FP64_PEAK_SOURCE = fp64_peaks()
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 def log(*a):
@@ -122,6 +149,21 @@ def oracle_sample(n_sample: int, n_target: int):
             "cores": oracle.num_threads()}
 
 
+def oracle_measured() -> list:
+    """Whole oracle evaluations actually run (not extrapolated): the committed goldens of
+    tools/make_golden_large.py at n = 20k / 40k, with their seconds, threads and CPU model."""
+    import glob
+
+    out = []
+    for f in sorted(glob.glob(os.path.join(ROOT, "tests", "golden", "loglik_n*.json"))):
+        g = json.load(open(f))
+        for c in g["cases"]:
+            out.append({"n": g["n"], "theta": c["theta"], "seconds": c["oracle_seconds"],
+                        "evals_per_s": 1.0 / c["oracle_seconds"], "threads": g["oracle_threads"],
+                        "cpu_model": g["cpu_model"], "host": g.get("host"), "source": os.path.relpath(f, ROOT)})
+    return out
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -145,7 +187,9 @@ def run_reference(args):
         "impl": "reference",
         "config": {"workload": f"loglik n={args.n} theta={THETA} (BASELINE configs[2])", "n": args.n,
                    "sample_n": n_sample},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": last["cores"], "kind": "oracle", "sample": sample},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": last["cores"], "kind": "oracle", "sample": sample,
+                         "extrapolated": True, "cpu_model": cpu_model(),
+                         "measured_whole_evaluations": oracle_measured()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -336,9 +380,12 @@ def run_gpu(args):
         if world == 1 and not args.no_cpu_baseline:
             s = oracle_sample(args.cpu_sample, n)
             cpu = {"value": 1.0 / s["t_target"], "unit": UNIT, "cores": s["cores"], "kind": "oracle",
+                   "extrapolated": True,
                    "sample": (f"oracle Alg. 2 at n={args.cpu_sample} on host cores ({s['t_total']:.1f}s: "
                               f"gen {s['t_gen']:.1f}s scaled (n/{args.cpu_sample})^2, chol+solve "
-                              f"{s['t_chol']:.1f}s scaled (n/{args.cpu_sample})^3 to n={n})")}
+                              f"{s['t_chol']:.1f}s scaled (n/{args.cpu_sample})^3 to n={n})"),
+                   "cpu_model": cpu_model(),
+                   "measured_whole_evaluations": oracle_measured()}
         result = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
@@ -353,9 +400,12 @@ def run_gpu(args):
                          "reduce": statistics.mean(i["ms_reduce"] for i in infos)},
             "cholesky_tflops": chol_tf,
             "cholesky_frac_fp64_peak": chol_tf / FP64_PEAK_TFLOPS,
+            "cholesky_frac_cublas_dgemm": chol_tf / DGEMM_TFLOPS,
             "roofline": {"bound": "tensor", "kernel": "gemm_nt_dmma<SyrkMap> (bulk trailing update U2)",
                          "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                         "frac": (achieved / FP64_PEAK_TFLOPS) if achieved else None, "traffic": traffic,
+                         "frac": (achieved / FP64_PEAK_TFLOPS) if achieved else None,
+                         "frac_vs_cublas_dgemm": (achieved / DGEMM_TFLOPS) if achieved else None,
+                         "cublas_dgemm_8192_tflops": DGEMM_TFLOPS, "traffic": traffic,
                          "traffic_of": traffic_of,
                          "launches": tr_n, "share_of_step": (tr_ms / args.steps) / ms_per_step,
                          "peak_source": FP64_PEAK_SOURCE,
@@ -383,7 +433,8 @@ def main():
     ap.add_argument("--n", type=int, default=100_000)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-sample", type=int, default=5000)
-    ap.add_argument("--ref-sample", type=int, default=2000)
+    ap.add_argument("--ref-sample", type=int, default=5000, help="oracle sample n of --impl reference "
+                    "(the same sample as cpu_baseline, so the two CPU arms measure the same thing)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true", help="skip BASELINE configs 1-3 side measurements")
     args = ap.parse_args()

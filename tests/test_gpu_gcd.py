@@ -16,7 +16,7 @@ if not torch.cuda.is_available():
 
 import paper_1708_02835_b200 as ex  # noqa: E402
 
-LOG2PI = math.log(2 * math.pi)
+from tests._tol import LOG2PI, assert_ll  # noqa: E402,F401
 
 
 @pytest.fixture
@@ -50,7 +50,7 @@ def test_gcd_loglik_and_predict(gcd):
     with ex.Context(device=0, nb=128, distance="great_circle") as c:
         r = c.loglik(lon, lat, z, theta)
         ll, ld, qd = oracle.loglik(lon, lat, z, theta)
-        assert abs(r.loglik - ll) <= 1e-10 * max(abs(ll), 0.5 * abs(ld), 0.5 * qd, 0.5 * n * LOG2PI)
+        assert_ll(r.loglik, (ll, ld, qd), n, what=theta)
         lon2, lat2 = lonlat(20, 4)
         got = c.predict(lon, lat, z, lon2, lat2, theta)
         ref = oracle.predict(lon, lat, z, lon2, lat2, theta)

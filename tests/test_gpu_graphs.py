@@ -17,6 +17,7 @@ if not torch.cuda.is_available():
     pytest.skip("needs a CUDA device", allow_module_level=True)
 
 import paper_1708_02835_b200 as ex  # noqa: E402
+from tests._tol import assert_ll  # noqa: E402
 
 THETAS = [(1.0, 0.1, 0.5), (0.7, 0.05, 1.3), (2.0, 0.2, 0.8), (1.0, 0.1, 2.5), (0.3, 0.02, 0.6)]
 
@@ -48,8 +49,7 @@ def test_graph_matches_oracle_and_recaptures_on_shape_change():
             for th in THETAS[:3]:
                 r = g.loglik_dev(X, Y, Z, th)
                 ll, ld, qd = oracle.loglik(x, y, z, th)
-                tol = 1e-10 * max(abs(ll), 0.5 * abs(ld), 0.5 * qd, 0.5 * n * math.log(2 * math.pi))
-                assert abs(r.loglik - ll) <= tol
+                assert_ll(r.loglik, (ll, ld, qd), n, what=(n, th))
 
 
 def test_graph_not_pd_then_valid():

@@ -19,7 +19,7 @@ if not torch.cuda.is_available():
 
 import paper_1708_02835_b200 as ex  # noqa: E402
 
-LOG2PI = math.log(2 * math.pi)
+from tests._tol import LOG2PI, assert_ll  # noqa: E402,F401
 
 
 def block_sum_oracle(x, y, z, theta, width):
@@ -39,8 +39,7 @@ def test_ind_equals_sum_of_block_logliks(n, nb, s, theta):
     r = c.loglik(x, y, z, theta)
     c.close()
     ll, ld, qd = block_sum_oracle(x, y, z, theta, s * nb)
-    tol = 1e-10 * max(abs(ll), 0.5 * abs(ld), 0.5 * qd, 0.5 * n * LOG2PI)
-    assert abs(r.loglik - ll) <= tol
+    assert_ll(r.loglik, (ll, ld, qd), n, what=(n, nb, s))
     assert r.logdet == pytest.approx(ld, rel=1e-10)
 
 

@@ -23,11 +23,7 @@ if not torch.cuda.is_available():
 
 import paper_1708_02835_b200 as ex  # noqa: E402
 
-LOG2PI = math.log(2 * math.pi)
-
-
-def ll_tol(ll, logdet, quad, n):
-    return 1e-10 * max(abs(ll), 0.5 * abs(logdet), 0.5 * abs(quad), 0.5 * n * LOG2PI)
+from tests._tol import LOG2PI, assert_ll  # noqa: E402
 
 
 @pytest.fixture(scope="module")
@@ -119,7 +115,7 @@ def test_factor_and_solve_match_oracle(n, nb, theta):
     assert np.abs(yv - yo).max() / np.abs(yo).max() <= 1e-10
     ll, logdet, quad = c.stage_finish()
     llo, ldo, qo = oracle.loglik(x, y, z, theta)
-    assert abs(ll - llo) <= ll_tol(llo, ldo, qo, n)
+    assert_ll(ll, (llo, ldo, qo), n, what=(n, nb, theta))
     c.close()
 
 
@@ -131,7 +127,7 @@ def test_loglik_matches_oracle(ctx, n, theta):
     z = oracle.simulate(x, y, (1.0, 0.1, 0.5), e)
     r = ctx.loglik(x, y, z, theta)
     llo, ldo, qo = oracle.loglik(x, y, z, theta)
-    assert abs(r.loglik - llo) <= ll_tol(llo, ldo, qo, n), (r.loglik, llo)
+    assert_ll(r.loglik, (llo, ldo, qo), n, what=(n, theta))
     assert r.logdet == pytest.approx(ldo, rel=1e-10, abs=1e-10)
     assert r.quad == pytest.approx(qo, rel=1e-10)
 
@@ -145,7 +141,7 @@ def test_loglik_config1_n400(ctx):
         c = ex.Context(device=0, nb=nb)
         r = c.loglik(x, y, z, theta)
         llo, ldo, qo = oracle.loglik(x, y, z, theta)
-        assert abs(r.loglik - llo) <= ll_tol(llo, ldo, qo, n)
+        assert_ll(r.loglik, (llo, ldo, qo), n, what=nb)
         c.close()
 
 
@@ -179,7 +175,7 @@ def test_loglik_ar1_closed_form(ctx, n):
     z = si.normals(n, 31)
     r = ctx.loglik(x, y, z, (t1, t2, 0.5))
     ll, ld, qd = kms(z, t1, math.exp(-h / t2))
-    assert abs(r.loglik - ll) <= ll_tol(ll, ld, qd, n)
+    assert_ll(r.loglik, (ll, ld, qd), n, what=n)
     assert r.logdet == pytest.approx(ld, rel=1e-11)
 
 
@@ -266,7 +262,7 @@ def test_virtual_ranks_match_single_and_oracle(world, n, nb):
     c = ex.Context(device=0, nb=nb, virtual_ranks=world)
     r = c.loglik(x, y, z, theta)
     llo, ldo, qo = oracle.loglik(x, y, z, theta)
-    assert abs(r.loglik - llo) <= ll_tol(llo, ldo, qo, n)
+    assert_ll(r.loglik, (llo, ldo, qo), n, what=(world, n, nb))
     # same kernels and order per panel; only the final partial sums are grouped by rank
     assert r.loglik == pytest.approx(r1.loglik, rel=1e-13)
     # factor read back from the distributed panels equals the single-GPU factor bitwise

@@ -57,3 +57,33 @@ def test_jitter_formula_bits():
         r, l = q // 4 + 1, q % 4 + 1
         assert x[q] == ((r - 0.5) + (0.8 * u - 0.4)) / 4
         assert y[q] == ((l - 0.5) + (0.8 * v - 0.4)) / 4
+
+
+@pytest.mark.parametrize("n,seed", [(2, 3), (17, 1), (401, 3), (1000, 1), (10007, 5), (100_000, 1)])
+def test_subset_rule_r2_independent_selection(n, seed):
+    """DESIGN R2, written out independently in numpy (keys from the shared counter-based
+    draw of synth_inputs, selection by a stable lexicographic sort): of the g*g cells,
+    the n with the smallest (key, q) are kept and emitted in increasing q. An oracle that
+    kept the first n cells, the largest keys, or emitted in key order fails here."""
+    import synth_inputs as si
+
+    g = math.isqrt(n - 1) + 1
+    SUBSET = 0x4C4F43535542534B
+    keys = si.draws(seed, SUBSET, g * g)
+    q_all = np.arange(g * g, dtype=np.int64)
+    order = np.lexsort((q_all, keys))  # primary key: draw, ties by q
+    q_sel = np.sort(order[:n])
+    x, y = oracle.gen_locations(n, seed)
+    q = np.floor(x * g).astype(np.int64) * g + np.floor(y * g).astype(np.int64)
+    assert np.array_equal(q, q_sel)
+    if n < g * g:  # the rule is not "first n cells" for these sizes
+        assert not np.array_equal(q_sel, np.arange(n))
+    # jitter (R3) of the kept cells from the same shared draw, IEEE double, no contraction
+    JIT = 0x4C4F434A49545452
+    jb = si.draws(seed, JIT, 2 * g * g)
+    u = (jb[2 * q_sel] >> np.uint64(11)).astype(np.float64) * 2.0**-53
+    v = (jb[2 * q_sel + 1] >> np.uint64(11)).astype(np.float64) * 2.0**-53
+    r = (q_sel // g + 1).astype(np.float64)
+    l = (q_sel % g + 1).astype(np.float64)
+    assert np.array_equal(((r - 0.5) + (0.8 * u - 0.4)) / g, x)
+    assert np.array_equal(((l - 0.5) + (0.8 * v - 0.4)) / g, y)
