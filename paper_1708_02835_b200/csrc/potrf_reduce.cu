@@ -22,186 +22,344 @@ namespace exageo {
 
 namespace {
 
-constexpr int LDS_P = PB + 1;  // odd stride: conflict-free column access
-
-// c (8 x 8, two per lane) += a (8 x 4 row fragment) * b (4 x 8 column fragment), FP64 DMMA
+// c (8 x 8, two per lane) += a (8 x 4 row fragment) * b (4 x 8 column fragment), FP64 DMMA;
+// lane l holds a = A[l/4][l%4], b = B[l%4][l/4], c = C[l/4][2(l%4) + {0, 1}]
 __device__ __forceinline__ void dmma64(double (&c)[2], double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(c[0]), "+d"(c[1])
                : "d"(a), "d"(b));
 }
-constexpr int LDS_A = PB + 2;  // even stride: 16-byte aligned double2 rows of colA
 
-// 256 threads as a 16 x 16 grid: thread (tr, tc) holds a_rc for rows r = tr + 16 i and
-// columns c = 4 tc + k (i, k < 4) in registers. Step j (right-looking, deferred scaling):
-// d_j = a_jj, f_r = a_rj / d_j (reciprocal-multiply, as the paper's dpotrf), a_rc -= f_r a_cj
-// for every held entry (rows r <= j get f = 0; entries above the diagonal take finite garbage
-// that is never read), then the owner of column j+1 publishes it to shared memory -- one
-// barrier per pivot. The j loop is unrolled by 4 so the register slot of column j+1 is a
-// compile-time index (no select chains on the pivot chain). W = L^{-1} is formed after the
-// factorization: 16 x 16 diagonal blocks by per-lane substitution, the off-diagonal blocks
-// W_IJ = -W_II sum_K L~_IK W_KJ by distance (tools/potrf_trace.cu: 24.6 us vs 32.7 us for
-// the previous 16-threads-per-row kernel that carried W through the pivot loop; the factor
-// L is bitwise the same).
-constexpr int kPotrfSmemDoubles = PB * LDS_A + PB * LDS_P + 3 * 256 + PB * LDS_P;
+// ---- K2: 64 x 64 diagonal block: one warp factors 16-column strips, seven warps form W ------
+// Shared memory: the block A (col-major, ld LDA2 = 68 = 4 mod 16 doubles: the 64-bit fragment
+// loads of a half warp -- 4 rows x 4 columns -- hit 32 distinct banks), W = L^{-1} (same
+// layout), the inverses T_K = L_KK^{-1} of the four 16 x 16 diagonal blocks (ld LDT), the
+// pivots d_j and 1/sqrt(d_j).
+constexpr int LDA2 = PB + 4;
+constexpr int LDT = 20;
+constexpr int kPotrfSmemDoubles = 2 * PB * LDA2 + 4 * 16 * LDT + 2 * PB;
 
+#ifdef EXAGEO_POTRF_TRACE  // development: clock64 stamps of thread 0 (tools/potrf_bench.cu)
+__device__ long long g_potrf_trace[64];
+#define PTRACE(i)                                       \
+  do {                                                  \
+    if ((threadIdx.x & 31) == 0) g_potrf_trace[i] = clock64(); \
+  } while (0)
+#else
+#define PTRACE(i) \
+  do {            \
+  } while (0)
+#endif
+
+// 1 / d and 1 / sqrt(d) for normal positive d without a slow path: MUFU seed + Newton steps
+// (quadratic convergence from ~2^-22: two steps for 1/d, whose last one is the usual correctly
+// rounding update r += r (1 - d r); three for 1/sqrt(d)).
+// d <= 0 or NaN gives garbage that the pivot check discards.
+__device__ __forceinline__ double rcp_nr(double d) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+#pragma unroll
+  for (int it = 0; it < 2; ++it) r = fma(r, fma(-d, r, 1.0), r);
+  return r;
+}
+__device__ __forceinline__ double rsqrt_nr(double d) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
+  const double hd = 0.5 * d;
+#pragma unroll
+  for (int it = 0; it < 3; ++it) y = fma(y, fma(-hd * y, y, 0.5), y);  // y (3/2 - d y^2 / 2)
+  return y;
+}
+
+__device__ __forceinline__ void named_arrive(int id, int count) {
+  asm volatile("bar.arrive %0, %1;\n" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ void named_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(count) : "memory");
+}
+
+// 16 x 16 x 16 product on one warp: acc (2 x 2 tiles of 8 x 8) += A B, with A(m, k) and
+// B(k, n) read through accessors (shared memory).
+template <class FA, class FB>
+__device__ __forceinline__ void mm16(double (&acc)[2][2][2], FA A, FB B) {
+  const int lane = threadIdx.x & 31, fr = lane >> 2, fk = lane & 3;
+#pragma unroll
+  for (int kk = 0; kk < 16; kk += 4) {
+    double af[2], bf[2];
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      af[t] = A(8 * t + fr, kk + fk);
+      bf[t] = B(kk + fk, 8 * t + fr);
+    }
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) dmma64(acc[mt][nt], af[mt], bf[nt]);
+  }
+}
+template <class F>
+__device__ __forceinline__ void acc_store(const double (&acc)[2][2][2], F C) {
+  const int lane = threadIdx.x & 31, fr = lane >> 2, fk = lane & 3;
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) C(8 * mt + fr, 8 * nt + 2 * fk + e, acc[mt][nt][e]);
+}
+
+// Strip K of the block (columns c0 = 16K .. c0+15, rows c0 .. 63, H = 64 - c0 rows) on the
+// factor warps w = 0 .. NFW-1, in place in As. Left-looking: first A_strip -= L[c0:, :c0]
+// L[c0:c0+16, :c0]^T as m8n8k4 DMMA (warp w: strip rows 16w .. 16w+15; accumulators preloaded
+// with A, negated A fragments). Then the unblocked factorization in registers: in every factor
+// warp lanes 0..15 hold the 16 rows of the diagonal block (replicated: each warp repeats the
+// same operations, bitwise identical) and lanes 16..31 the off-diagonal rows 16 + 16w + l - 16.
+// Pivot j: d = a_jj (lane j), f_r = a_rj / d, a_rc -= f_r a_cj (c > j). The next pivot's own
+// update is lane-local (chain per pivot: shuffle -> reciprocal -> multiply -> FMA); the column
+// a_.j+1 of the diagonal block goes through a per-warp shared buffer, off that chain. Deferred
+// scaling as the paper's dpotrf with a reciprocal: identical rows give f = 1 and an exact zero
+// pivot. Returns the first bad pivot (strip-local) or -1 (same in every factor warp).
+constexpr int NFW = 3;  // factor warps
+
+template <int H>
+__device__ __forceinline__ int factor_strip(double* As, double* dv, double* rs, double* colbuf,
+                                            double* __restrict__ a, int64_t lda) {
+  constexpr int c0 = PB - H;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  constexpr int NW = (H - 16) / 16 > 0 ? (H - 16) / 16 : 1;  // factor warps with rows in this strip
+  if constexpr (c0 > 0) {
+    if (16 * w < H) {  // this warp's 16 strip rows of the update
+      const int fr = lane >> 2, fk = lane & 3;
+      const int rb = c0 + 16 * w;
+      double acc[2][2][2];
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) acc[mt][nt][e] = As[(c0 + 8 * nt + 2 * fk + e) * LDA2 + rb + 8 * mt + fr];
+#pragma unroll
+      for (int kk = 0; kk < c0; kk += 4) {
+        const double* col = As + (kk + fk) * LDA2 + fr;
+        double af[2], bf[2];
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+          af[t] = -col[rb + 8 * t];
+          bf[t] = col[c0 + 8 * t];
+        }
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < 2; ++nt) dmma64(acc[mt][nt], af[mt], bf[nt]);
+      }
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) As[(c0 + 8 * nt + 2 * fk + e) * LDA2 + rb + 8 * mt + fr] = acc[mt][nt][e];
+    }
+    named_sync(6, 32 * NFW);
+  }
+  int bad = -1;
+  if (w < NW) {
+    // strip-local row of this lane: diagonal rows 0..15, then this warp's off-diagonal rows
+    const int r = (lane < 16) ? lane : 16 + 16 * w + (lane - 16);
+    const bool valid = r < H;
+    double v[16], dd[16];
+#pragma unroll
+    for (int c = 0; c < 16; ++c) v[c] = (valid && c <= r) ? As[(c0 + c) * LDA2 + c0 + r] : 0.0;
+    double* cb = colbuf + w * 32;  // 16 doubles per pivot, double buffered
+    if (lane < 16) cb[lane] = v[0];
+    __syncwarp();
+    double dn = v[0];  // lane j: its own updated diagonal a_jj, ready before the broadcast
+#ifdef EXAGEO_POTRF_TRACE
+    long long tj[17];
+    tj[0] = clock64();
+#endif
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const double d = __shfl_sync(0xffffffffu, dn, j);
+      dd[j] = d;
+      bad = (bad < 0 && !(d > 0.0)) ? j : bad;
+      const double rd = rcp_nr(d);
+      const double f = (r > j) ? v[j] * rd : 0.0;
+      const double* cj = cb + 16 * (j & 1);  // a_cj, c = 0..15, of the diagonal block
+      if (j + 1 < 16) {
+        dn = fma(-f, v[j], v[j + 1]);  // lane j+1: a_{j+1,j+1} - f a_{j+1,j}, lane-local
+        v[j + 1] = fma(-f, cj[j + 1], v[j + 1]);
+        if (lane < 16) cb[16 * ((j + 1) & 1) + lane] = v[j + 1];  // column j+1 for the next pivot
+      }
+#pragma unroll
+      for (int c = j + 2; c < 16; ++c) v[c] = fma(-f, cj[c], v[c]);
+      __syncwarp();
+#ifdef EXAGEO_POTRF_TRACE
+      tj[j + 1] = clock64();
+#endif
+    }
+#ifdef EXAGEO_POTRF_TRACE
+    if (c0 == 0 && lane == 0 && w == 0)
+      for (int j = 0; j < 16; ++j) g_potrf_trace[32 + j] = tj[j + 1] - tj[j];
+#endif
+    // 1/sqrt(d_j) by lane j (own pivot), shared through rs; then L_rc = a_rc / sqrt(d_c) below
+    // the diagonal, L_cc = d_c / sqrt(d_c), zeros above -- into As and straight to global memory
+    double dm = dd[0];
+#pragma unroll
+    for (int j = 1; j < 16; ++j) dm = (lane == j) ? dd[j] : dm;
+    if (lane < 16 && w == 0) {
+      dv[c0 + lane] = dm;
+      rs[c0 + lane] = rsqrt_nr(dm);
+    }
+    named_sync(6, 32 * NFW);
+    if (valid && (lane >= 16 || w == 0)) {
+#pragma unroll
+      for (int c = 0; c < 16; ++c) {
+        const double is = rs[c0 + c];
+        const double l = (r > c) ? v[c] * is : ((r == c) ? dd[c] * is : 0.0);
+        As[(c0 + c) * LDA2 + c0 + r] = l;
+        a[(int64_t)(c0 + c) * lda + c0 + r] = l;
+      }
+    }
+  } else {
+    named_sync(6, 32 * NFW);
+  }
+  named_sync(6, 32 * NFW);
+  return bad;
+}
+
+// The paper's dpotrf at tile granularity (Alg. 2 l.3) for the PB x PB diagonal block
+// of the current panel, with W = L^{-1} for the panel TRSM as a DMMA product, the partial
+// log-determinant sum_j log L_jj = sum_j log(d_j) / 2 (R5), and the first
+// non-positive (or NaN) pivot as a global index (R14; every later kernel reads info and exits).
+//   warps 0..2: the four strips in order (factor_strip), announcing strip K on named barrier 1+K;
+//   warps 3..7: after strip K, T_K = L_KK^{-1} (warp 3, per-lane column substitution) and the
+//               W row block K: W_KC = -T_K G_KC, G_KC = sum_{M=C}^{K-1} L_KM W_MC (warp 4+C);
+//               they trail the factor warps by about one strip, off their critical path.
 __global__ void __launch_bounds__(256) potrf_block_kernel(double* __restrict__ a, int64_t lda,
                                                           double* __restrict__ W, double* __restrict__ slot,
                                                           int* __restrict__ info, int64_t pivot_base) {
   asm volatile("griddepcontrol.wait;\n" ::: "memory");  // programmatic dependent launch
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   if (*(volatile int*)info != 0) return;
+  PTRACE(0);
   extern __shared__ double smem_p[];
-  double* colA = smem_p;             // colA[c * LDS_A + r] = a_rc at step c (unscaled)
-  double* Wt = colA + PB * LDS_A;    // Wt[c * LDS_P + r] = w~_rc, w~ = L~^{-1} (unit lower)
-  double* Xs = Wt + PB * LDS_P;      // 3 x 16 x 16 off-diagonal products
-  double* Ls = Xs + 3 * 256;         // Ls[c * LDS_P + r] = L~_rc = a_rc / d_c (r > c)
-  __shared__ double rdv[PB], ilj[PB], lj[PB], lred[2];
-  const int tid = threadIdx.x, tr = tid >> 4, tc = tid & 15;
-  double v[4][4];
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int r = tr + 16 * i, c = 4 * tc + k;
-      v[i][k] = (c <= r) ? a[(int64_t)c * lda + r] : 0.0;
-    }
-  if (tc == 0) {
-#pragma unroll
-    for (int i = 0; i < 4; ++i) colA[tr + 16 * i] = v[i][0];  // column 0
-  }
-  for (int m = 0; m < PB / 4; ++m) {
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int j = 4 * m + u;
-      __syncthreads();
-      const double* cj = colA + j * LDS_A;
-      const double rd = __drcp_rn(cj[j]);  // a bad pivot is found by the scan after the loop
-      double f[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) f[i] = (tr + 16 * i > j) ? cj[tr + 16 * i] * rd : 0.0;
-      const double2 s01 = *reinterpret_cast<const double2*>(cj + 4 * tc);
-      const double2 s23 = *reinterpret_cast<const double2*>(cj + 4 * tc + 2);
-      const double src[4] = {s01.x, s01.y, s23.x, s23.y};
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int k = 0; k < 4; ++k) v[i][k] = fma(-f[i], src[k], v[i][k]);
-      const int k1 = (u + 1) & 3;  // register slot of column j + 1 (constant after unrolling)
-      const int j1 = j + 1;
-      if (j1 < PB && tc == (j1 >> 2)) {
-#pragma unroll
-        for (int i = 0; i < 4; ++i) colA[j1 * LDS_A + tr + 16 * i] = v[i][k1];
-      }
-    }
-  }
-  __syncthreads();
-  // first non-positive (or NaN) pivot: d_j as used at step j; later pivots may be garbage
+  double* As = smem_p;             // As[c * LDA2 + r]
+  double* Ws = As + PB * LDA2;     // Ws[c * LDA2 + r]
+  double* Ts = Ws + PB * LDA2;     // Ts[K * 16 * LDT + c * LDT + r]
+  double* dv = Ts + 4 * 16 * LDT;  // d_j
+  double* rs = dv + PB;            // 1 / sqrt(d_j)
+  __shared__ __align__(16) double colbuf[NFW * 32];
   __shared__ int badj;
+  __shared__ double lred[2], lgv[PB];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  {  // the lower triangle (and the diagonal blocks' upper halves, never read), 16-byte loads
+    double2 t[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int idx = tid + 256 * u, r2 = idx & 31, c = idx >> 5;  // 32 double2 per column
+      t[u] = (2 * r2 + 1 >= (c & ~15)) ? *reinterpret_cast<const double2*>(a + (int64_t)c * lda + 2 * r2)
+                                      : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int idx = tid + 256 * u, r2 = idx & 31, c = idx >> 5;
+      *reinterpret_cast<double2*>(As + c * LDA2 + 2 * r2) = t[u];
+    }
+  }
   if (tid == 0) badj = PB;
   __syncthreads();
-  if (tid < PB && !(colA[tid * LDS_A + tid] > 0.0)) atomicMin(&badj, tid);
+  PTRACE(1);
+  if (warp < NFW) {
+    int first = -1;
+#pragma unroll 1
+    for (int K = 0; K < 4; ++K) {
+      int b;
+      switch (K) {
+        case 0: b = factor_strip<64>(As, dv, rs, colbuf, a, lda); break;
+        case 1: b = factor_strip<48>(As, dv, rs, colbuf, a, lda); break;
+        case 2: b = factor_strip<32>(As, dv, rs, colbuf, a, lda); break;
+        default: b = factor_strip<16>(As, dv, rs, colbuf, a, lda); break;
+      }
+      if (first < 0 && b >= 0) first = 16 * K + b;
+      PTRACE(2 + K);
+      named_arrive(1 + K, 256);
+    }
+    if (tid == 0 && first >= 0) badj = first;
+  } else {
+    constexpr int NH = 256 - 32 * NFW;  // helper threads
+    // zeros above the diagonal blocks (rows 0 .. 16K-1 of column block K), as a dpotrf leaves them
+    for (int idx = tid - 32 * NFW; idx < 16 * 16 * 6; idx += NH) {
+      const int K = idx < 256 ? 1 : (idx < 768 ? 2 : 3);
+      const int base = K == 1 ? 0 : (K == 2 ? 256 : 768);
+      const int r = (idx - base) % (16 * K), c = 16 * K + (idx - base) / (16 * K);
+      a[(int64_t)c * lda + r] = 0.0;
+    }
+#pragma unroll 1
+    for (int K = 0; K < 4; ++K) {
+      const int k0 = 16 * K;
+      named_sync(1 + K, 256);  // strip K is in As
+      if (warp == NFW && lane < 16) {  // column c = lane of T_K: t_r = (delta_rc - sum_{m<r} L_rm t_m) / L_rr
+        const int c = lane;
+        double acc[16], t[16];
+#pragma unroll
+        for (int r = 0; r < 16; ++r) acc[r] = 0.0;
+#pragma unroll
+        for (int m = 0; m < 16; ++m) {
+          t[m] = (m < c) ? 0.0 : ((m == c ? 1.0 : 0.0) - acc[m]) * rs[k0 + m];
+#pragma unroll
+          for (int r = m + 1; r < 16; ++r) acc[r] = fma(As[(k0 + m) * LDA2 + k0 + r], t[m], acc[r]);
+        }
+        double* T = Ts + K * 16 * LDT;
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+          T[c * LDT + r] = t[r];
+          Ws[(k0 + c) * LDA2 + k0 + r] = t[r];
+        }
+      }
+      double g[2][2][2] = {};
+      const int C = warp - NFW - 1;
+      if (C >= 0 && C < K) {  // G_KC = sum_{M=C}^{K-1} L_KM W_MC
+#pragma unroll 1
+        for (int M = C; M < K; ++M)
+          mm16(g, [=](int m, int k) { return As[(16 * M + k) * LDA2 + k0 + m]; },
+               [=](int k, int n) { return Ws[(16 * C + n) * LDA2 + 16 * M + k]; });
+      }
+      named_sync(5, NH);  // T_K is in shared memory
+      if (C >= 0 && C < K) {  // W_KC = -T_K G_KC
+        const double* T = Ts + K * 16 * LDT;
+        // G to shared memory first: its accumulator layout is not the B fragment layout
+        acc_store(g, [=](int m, int n, double v) { Ws[(16 * C + n) * LDA2 + k0 + m] = v; });
+        __syncwarp();
+        double w[2][2][2] = {};
+        mm16(w, [=](int m, int k) { return -T[k * LDT + m]; },
+             [=](int k, int n) { return Ws[(16 * C + n) * LDA2 + k0 + k]; });
+        __syncwarp();
+        acc_store(w, [=](int m, int n, double v) { Ws[(16 * C + n) * LDA2 + k0 + m] = v; });
+      }
+      named_sync(5, NH);  // W row block K complete before the next G reads it
+      // W row block K to global memory (zeros right of the diagonal block); log-det terms
+      for (int idx = tid - 32 * NFW; idx < 16 * PB; idx += NH) {
+        const int r = idx & 15, c = idx >> 4;
+        W[c * PB + k0 + r] = (c < k0 + 16) ? Ws[c * LDA2 + k0 + r] : 0.0;
+      }
+      if (warp == NFW && lane < 16) lgv[k0 + lane] = 0.5 * log(dv[k0 + lane]);
+    }
+  }
   __syncthreads();
+  PTRACE(6);
   if (badj < PB) {
     if (tid == 0) *info = (int)(pivot_base + badj + 1);
     return;
   }
-  // L_jj = sqrt(d_j), 1 / L_jj; sum log L_jj = sum log(d_j) / 2 by a fixed two-level tree
+  // sum log L_jj = sum log(d_j) / 2, fixed two-level tree (L and W are already stored)
   if (tid < PB) {
-    const double dj = colA[tid * LDS_A + tid];
-    rdv[tid] = __drcp_rn(dj);
-    lj[tid] = sqrt(dj);
-    ilj[tid] = 1.0 / lj[tid];
-    double lg = 0.5 * log(dj);
+    double lg = lgv[tid];
     for (int o = 16; o > 0; o >>= 1) lg += __shfl_down_sync(0xffffffffu, lg, o);
     if ((tid & 31) == 0) lred[tid >> 5] = lg;
   }
   __syncthreads();
   if (tid == 0) *slot = lred[0] + lred[1];
-  for (int idx = tid; idx < PB * PB; idx += blockDim.x) {
-    const int rr = idx & (PB - 1), c = idx / PB;
-    Ls[c * LDS_P + rr] = (rr > c) ? colA[c * LDS_A + rr] * rdv[c] : 0.0;
-  }
-  __syncthreads();
-  {  // diagonal 16 x 16 blocks of w~ = L~^{-1}: warp I, lane c computes column c
-    const int I = tid >> 5, c = tid & 31;
-    if (I < 4 && c < 16) {
-      const int b = 16 * I;
-      double w[16];
-#pragma unroll
-      for (int mm = 0; mm < 16; ++mm) w[mm] = (mm == c) ? 1.0 : 0.0;
-#pragma unroll
-      for (int k = 0; k < 16; ++k)
-#pragma unroll
-        for (int r = k + 1; r < 16; ++r) w[r] = fma(-Ls[(b + k) * LDS_P + b + r], w[k], w[r]);
-#pragma unroll
-      for (int r = 0; r < 16; ++r) Wt[(b + c) * LDS_P + b + r] = (r >= c) ? w[r] : 0.0;
-    }
-  }
-  __syncthreads();
-  {  // off-diagonal blocks by distance on the FP64 tensor cores: warp blk owns block
-    // (I, J) = (blk + dist, blk): X = sum_K L~_IK w~_KJ, then w~_IJ = -w~_II X, each a
-    // 16 x 16 product of 2 x 2 m8n8k4 tiles (A row fragments, B column fragments)
-    const int warp = tid >> 5, lane = tid & 31, fr = lane >> 2, fk = lane & 3;
-    double* Xw = Xs + warp * 256;  // this warp's X, column-major 16 x 16 (ld 16)
-#pragma unroll 1
-    for (int dist = 1; dist < 4; ++dist) {
-      if (warp < 4 - dist) {
-        const int bI = warp + dist, bJ = warp;
-        double acc[2][2][2] = {};
-#pragma unroll 1
-        for (int K = bJ; K < bI; ++K) {
-#pragma unroll
-          for (int kk = 0; kk < 16; kk += 4) {
-            double af[2], bf[2];
-#pragma unroll
-            for (int t = 0; t < 2; ++t) {
-              af[t] = Ls[(16 * K + kk + fk) * LDS_P + 16 * bI + 8 * t + fr];   // L~[m][k]
-              bf[t] = Wt[(16 * bJ + 8 * t + fr) * LDS_P + 16 * K + kk + fk];   // w~[k][n]
-            }
-#pragma unroll
-            for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-              for (int nt = 0; nt < 2; ++nt) dmma64(acc[mt][nt], af[mt], bf[nt]);
-          }
-        }
-#pragma unroll
-        for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-          for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-            for (int e = 0; e < 2; ++e) Xw[(8 * nt + 2 * fk + e) * 16 + 8 * mt + fr] = acc[mt][nt][e];
-        __syncwarp();
-        double acc2[2][2][2] = {};
-#pragma unroll
-        for (int kk = 0; kk < 16; kk += 4) {
-          double af[2], bf[2];
-#pragma unroll
-          for (int t = 0; t < 2; ++t) {
-            af[t] = Wt[(16 * bI + kk + fk) * LDS_P + 16 * bI + 8 * t + fr];  // w~_II[m][k]
-            bf[t] = Xw[(8 * t + fr) * 16 + kk + fk];                           // X[k][n]
-          }
-#pragma unroll
-          for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-            for (int nt = 0; nt < 2; ++nt) dmma64(acc2[mt][nt], af[mt], bf[nt]);
-        }
-#pragma unroll
-        for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-          for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-            for (int e = 0; e < 2; ++e)
-              Wt[(16 * bJ + 8 * nt + 2 * fk + e) * LDS_P + 16 * bI + 8 * mt + fr] = -acc2[mt][nt][e];
-      }
-      __syncthreads();
-    }
-  }
-  for (int idx = tid; idx < PB * PB; idx += blockDim.x) {
-    const int rr = idx & (PB - 1), c = idx / PB;
-    a[(int64_t)c * lda + rr] = (rr > c) ? colA[c * LDS_A + rr] * ilj[c] : (rr == c ? lj[c] : 0.0);
-    W[c * PB + rr] = (rr >= c) ? Wt[c * LDS_P + rr] * ilj[rr] : 0.0;
-  }
+  PTRACE(7);
 }
 
 // Fixed-shape block sum (blockDim.x a multiple of 32): deterministic tree.
@@ -342,6 +500,10 @@ __global__ void trmv_sum_kernel(int64_t n, int64_t N, const double* __restrict__
 }  // namespace
 
 constexpr int kPotrfSmem = kPotrfSmemDoubles * (int)sizeof(double);
+
+#ifdef EXAGEO_POTRF_TRACE
+cudaError_t potrf_trace_read(long long* out) { return cudaMemcpyFromSymbol(out, g_potrf_trace, 64 * sizeof(long long)); }
+#endif
 
 cudaError_t potrf_init() {
   return cudaFuncSetAttribute(potrf_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kPotrfSmem);

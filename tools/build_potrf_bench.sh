@@ -1,0 +1,9 @@
+#!/bin/bash
+# Build tools/potrf_bench (K2 latency + correctness, panel GEMM timings) against the product kernels.
+set -e
+cd "$(dirname "$0")/.."
+C=paper_1708_02835_b200/csrc
+nvcc -O3 -std=c++17 -lineinfo -gencode arch=compute_100a,code=sm_100a -I include -I $C \
+  tools/potrf_bench.cu $C/potrf_reduce.cu $C/gemm_dmma.cu -o tools/potrf_bench
+nvcc -O3 -std=c++17 -lineinfo -gencode arch=compute_100a,code=sm_100a -I include -I $C -DEXAGEO_POTRF_TRACE \
+  tools/potrf_bench.cu $C/potrf_reduce.cu $C/gemm_dmma.cu -o tools/potrf_bench_trace

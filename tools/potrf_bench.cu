@@ -7,6 +7,11 @@
 #include "internal.h"
 
 using namespace exageo;
+#ifdef EXAGEO_POTRF_TRACE
+namespace exageo {
+cudaError_t potrf_trace_read(long long* out);
+}
+#endif
 
 __global__ void make_spd(double* a, int64_t lda, int n) {
   for (int idx = threadIdx.x + blockIdx.x * blockDim.x; idx < n * n; idx += blockDim.x * gridDim.x) {
@@ -48,6 +53,20 @@ int main() {
     cudaEventElapsedTime(&ms, e0, e1);
     printf("make_spd alone: %.2f us per call\n", 1000.f * ms / 20);
   }
+#ifdef EXAGEO_POTRF_TRACE
+  {
+    long long tr[64];
+    make_spd<<<64, 256>>>(a, lda, 64);
+    launch_potrf_block(a, lda, W, slot, info, 0, 0);
+    cudaDeviceSynchronize();
+    potrf_trace_read(tr);
+    printf("trace (cycles from kernel start): load %lld strips %lld %lld %lld %lld  W done %lld  end %lld\n",
+           tr[1] - tr[0], tr[2] - tr[0], tr[3] - tr[0], tr[4] - tr[0], tr[5] - tr[0], tr[6] - tr[0], tr[7] - tr[0]);
+    printf("K0 cycles per pivot:");
+    for (int j = 0; j < 16; ++j) printf(" %lld", tr[32 + j]);
+    printf("\n");
+  }
+#endif
   int h;
   cudaMemcpy(&h, info, sizeof(int), cudaMemcpyDeviceToHost);
   printf("info=%d err=%s\n", h, cudaGetErrorString(cudaGetLastError()));
