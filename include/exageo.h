@@ -58,9 +58,13 @@ typedef struct {
   int nb;       /* tile size (multiple of 128); 0 = automatic (128 below n = 12k, 256 below 15k,
                    384 below 21k, 512 below 48k, else 1024; 512 for world > 1)                          */
   void* stream; /* cudaStream_t to run on; NULL = the library creates its own stream */
-  /* Distribution: the tile panels are dealt 1-D block-cyclically over
-   * `world` ranks (panel j on rank j % world), factored with a panel broadcast per step
-   * and finished with an all-reduce. world <= 1: single GPU. */
+  /* Distribution: the tiles are dealt 2-D block-cyclically over a
+   * grid_rows x (world / grid_rows) process grid (1 x world by default: panel j on rank
+   * j % world); each step factors panel k on its process column, broadcasts its slices along
+   * the process rows and then the process columns (NCCL), and the evaluation finishes with
+   * an all-reduce. world <= 1: single GPU. Experimental beyond one GPU: the schedule is
+   * verified on virtual ranks and a single-rank communicator; multi-rank NCCL transport has
+   * not run on hardware (one-GPU build box). */
   int world;            /* number of ranks (one process per GPU, NCCL over NVLink)      */
   int rank;             /* this process's rank, 0 <= rank < world                        */
   const void* nccl_id;  /* 128-byte ncclUniqueId from exageo_nccl_unique_id on rank 0,
@@ -82,6 +86,11 @@ typedef struct {
                            shape and buffer set, then replay with theta patched into the
                            generator nodes): 0 = automatic (n <= 32768, no NCCL communicator,
                            a non-default stream), 1 = always when possible, -1 = never      */
+  int grid_rows;        /* P of the P x Q process grid (the 2-D block-cyclic
+                           distribution of P:450-453): tile (I, J) on rank (I mod P) Q + J mod Q,
+                           Q = ranks / P. 0 or 1 = 1 x ranks (panel j on rank j % ranks); must
+                           divide world (or virtual_ranks); P <= 8. NCCL row and column
+                           communicators are split from the world communicator.             */
 } exageo_opts;
 
 /* Per-evaluation details of exageo_loglik*. */
@@ -229,7 +238,9 @@ exageo_status exageo_mle_ex(exageo_ctx* ctx, int64_t n, const double* x, const d
  *   generated on the fly (never stored); zero mean (mu1 = mu2 = 0).
  * x, y, z: the n observed locations and measurements; xnew, ynew: the m prediction
  * locations; znew: m predictions. Host arrays. Non-PD -> EXAGEO_ENOTPD.
- * Collective on distributed contexts (each w_j is broadcast from its panel's owner). */
+ * Collective on distributed contexts: per panel j (from the last) the ranks of its process
+ * column reduce their partial sums onto the diagonal rank, which solves with L_jj and
+ * broadcasts w_j (1 x Q grids: the panel's owner solves alone). */
 exageo_status exageo_predict(exageo_ctx* ctx, const exageo_theta* theta, int64_t n, const double* x,
                              const double* y, const double* z, int64_t m, const double* xnew, const double* ynew,
                              double* znew);
@@ -240,7 +251,8 @@ exageo_status exageo_predict(exageo_ctx* ctx, const exageo_theta* theta, int64_t
  * from the same factor: batches of new sites, Sigma21 generated on the GPU, a blocked
  * multi-right-hand-side forward solve with L (diagonal-tile substitution + DMMA update of
  * the rows below), column sums of squares. var: host array of m doubles. Work ~ n^2 m flop.
- * Single-rank contexts only (EXAGEO_EINVAL with world > 1 or virtual ranks). */
+ * Single-rank contexts only (EXAGEO_EINVAL with world > 1 or virtual ranks), tile size
+ * nb <= 1024 (EXAGEO_EINVAL otherwise). */
 exageo_status exageo_predict_var(exageo_ctx* ctx, const exageo_theta* theta, int64_t n, const double* x,
                                  const double* y, const double* z, int64_t m, const double* xnew,
                                  const double* ynew, double* znew, double* var);

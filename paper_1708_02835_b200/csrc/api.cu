@@ -76,7 +76,7 @@ int auto_nb(int64_t n, int world = 1) {
   return 128;
 }
 
-Layout make_layout(int64_t n, int nb, int rank = 0, int world = 1, int ind = 0) {
+Layout make_layout(int64_t n, int nb, int rank = 0, int world = 1, int ind = 0, int P = 1) {
   Layout L;
   L.ind = ind;
   L.n = n;
@@ -85,6 +85,10 @@ Layout make_layout(int64_t n, int nb, int rank = 0, int world = 1, int ind = 0) 
   L.N = (int64_t)L.T * nb;
   L.rank = rank;
   L.world = world;
+  L.P = P;
+  L.Q = world / P;
+  L.p = rank / L.Q;
+  L.q = rank % L.Q;
   return L;
 }
 
@@ -145,19 +149,34 @@ exageo_status ensure_vec(exageo_ctx* c, int64_t n) {
 
 size_t local_bytes(const Layout& L) { return (size_t)L.total() * sizeof(double) + 256 * sizeof(double); }
 
+// bytes of the receive buffer for slice pp of a broadcast panel: the largest local panel of
+// process row pp (panel 0)
+size_t slice_bytes(const Layout& L, int pp) { return (size_t)L.ld_of(pp, 0) * L.nb * sizeof(double); }
+size_t lkk_bytes(int nb) { return ((size_t)nb * nb + (size_t)64 * nb) * sizeof(double); }
+
+cudaError_t alloc_or_fail(void** p, size_t bytes) {
+  cudaError_t e = cudaMalloc(p, bytes);
+  if (e != cudaSuccess) cudaGetLastError();
+  return e;
+}
+
 // Allocate (or check) every rank state's panel storage, receive buffers and slots.
 exageo_status ensure_buffers(exageo_ctx* c) {
   size_t need_all = 0;
   for (auto& R : c->rs) {
     need_all += R.ws_external ? 0 : (R.ws_bytes >= local_bytes(R.L) ? 0 : local_bytes(R.L));
-    if (c->world > 1 && R.recv_bytes < (size_t)R.L.ld(0) * R.L.nb * sizeof(double))
-      need_all += 2 * (size_t)R.L.ld(0) * R.L.nb * sizeof(double);
+    if (c->world > 1)
+      for (int pp = 0; pp < R.L.P; ++pp)
+        if (R.recv_bytes[pp] < slice_bytes(R.L, pp)) need_all += 2 * slice_bytes(R.L, pp);
   }
   if (need_all > 0) {
     size_t free_b = 0, total_b = 0;
     CUDA_TRY(c, cudaMemGetInfo(&free_b, &total_b));
     size_t reclaim = 0;
-    for (auto& R : c->rs) reclaim += (R.ws_external ? 0 : R.ws_bytes) + 2 * R.recv_bytes;
+    for (auto& R : c->rs) {
+      reclaim += R.ws_external ? 0 : R.ws_bytes;
+      for (int pp = 0; pp < kMaxP; ++pp) reclaim += 2 * R.recv_bytes[pp];
+    }
     if (need_all > free_b + reclaim)
       return fail(c, EXAGEO_ENOMEM,
                   "tile workspace needs " + std::to_string(need_all) + " bytes, " + std::to_string(free_b) + " free");
@@ -178,32 +197,64 @@ exageo_status ensure_buffers(exageo_ctx* c) {
       cudaFree(R.ws);
       R.ws = nullptr;
       R.ws_bytes = 0;
-      cudaError_t e = cudaMalloc(&R.ws, local_bytes(L));
-      if (e != cudaSuccess) {
-        cudaGetLastError();
-        return fail(c, EXAGEO_ENOMEM, std::string("cudaMalloc workspace: ") + cudaGetErrorString(e));
-      }
+      cudaError_t e = alloc_or_fail((void**)&R.ws, local_bytes(L));
+      if (e != cudaSuccess) return fail(c, EXAGEO_ENOMEM, std::string("cudaMalloc workspace: ") + cudaGetErrorString(e));
       R.ws_bytes = local_bytes(L);
     }
+    if (R.lkk_bytes < lkk_bytes(L.nb)) {
+      for (auto& b : R.lkk) {
+        cudaFree(b);
+        b = nullptr;
+      }
+      R.lkk_bytes = 0;
+      for (auto& b : R.lkk) {
+        cudaError_t e = alloc_or_fail((void**)&b, lkk_bytes(L.nb));
+        if (e != cudaSuccess) return fail(c, EXAGEO_ENOMEM, std::string("cudaMalloc L_kk buffer: ") + cudaGetErrorString(e));
+      }
+      R.lkk_bytes = lkk_bytes(L.nb);
+    }
     if (c->world > 1) {
-      const size_t rb = (size_t)L.ld(0) * L.nb * sizeof(double);
-      if (R.recv_bytes < rb) {
-        for (auto& p : R.recv) {
-          cudaFree(p);
-          p = nullptr;
+      for (int pp = 0; pp < L.P; ++pp) {
+        const size_t rb = slice_bytes(L, pp);
+        if (R.recv_bytes[pp] >= rb) continue;
+        for (auto& b : R.recv) {
+          cudaFree(b[pp]);
+          b[pp] = nullptr;
         }
-        R.recv_bytes = 0;
-        for (auto& p : R.recv) {
-          cudaError_t e = cudaMalloc(&p, rb);
-          if (e != cudaSuccess) {
-            cudaGetLastError();
+        R.recv_bytes[pp] = 0;
+        for (auto& b : R.recv) {
+          cudaError_t e = alloc_or_fail((void**)&b[pp], rb);
+          if (e != cudaSuccess)
             return fail(c, EXAGEO_ENOMEM, std::string("cudaMalloc receive buffer: ") + cudaGetErrorString(e));
-          }
         }
-        R.recv_bytes = rb;
+        R.recv_bytes[pp] = rb;
       }
     }
   }
+  return EXAGEO_OK;
+}
+
+// P > 1: the local panel offsets of rank state R (host table + device copy), from ld().
+exageo_status set_offsets(exageo_ctx* c, RankState& R) {
+  Layout& L = R.L;
+  if (L.P == 1) {
+    L.offs_h = L.offs_d = nullptr;
+    return EXAGEO_OK;
+  }
+  std::vector<int64_t> o(L.owned() + 1, 0);
+  for (int m = 0; m < L.owned(); ++m) o[m + 1] = o[m] + (int64_t)L.nb * L.ld(L.owned_panel(m));
+  if (o != R.offs_h || R.offs_d == nullptr) {
+    if (R.offs_cap < o.size()) {
+      cudaFree(R.offs_d);
+      R.offs_d = nullptr;
+      CUDA_TRY(c, cudaMalloc(&R.offs_d, sizeof(int64_t) * o.size()));
+      R.offs_cap = o.size();
+    }
+    CUDA_TRY(c, cudaMemcpy(R.offs_d, o.data(), sizeof(int64_t) * o.size(), cudaMemcpyHostToDevice));
+    R.offs_h = o;
+  }
+  L.offs_h = R.offs_h.data();
+  L.offs_d = R.offs_d;
   return EXAGEO_OK;
 }
 
@@ -216,7 +267,9 @@ exageo_status prepare_generate(exageo_ctx* c, const exageo_theta* t, int64_t n, 
   c->G = make_layout(n, nb, 0, 1, c->ind);
   for (size_t i = 0; i < c->rs.size(); ++i) {
     const int rank = c->virt ? (int)i : c->rank;
-    c->rs[i].L = make_layout(n, nb, rank, c->world, c->ind);
+    c->rs[i].L = make_layout(n, nb, rank, c->world, c->ind, c->P);
+    exageo_status st = set_offsets(c, c->rs[i]);
+    if (st != EXAGEO_OK) return st;
   }
   return ensure_buffers(c);
 }
@@ -226,6 +279,8 @@ exageo_status launch_generate(exageo_ctx* c, const MaternConsts& mc, const doubl
   c->kernels += launch_matern_table(mc, c->mtab, c->stream);
   for (auto& R : c->rs) {
     CUDA_TRY(c, cudaMemsetAsync(R.info, 0, sizeof(int), c->stream));
+    if (R.L.P > 1)  // only the diagonal ranks write log-det slots (the others' stay zero)
+      CUDA_TRY(c, cudaMemsetAsync(R.slots, 0, sizeof(double) * (size_t)R.L.owned() * (R.L.nb / PB), c->stream));
     launch_gen_panels(R.L, R.ws, mc, x, y, z, c->mtab, c->stream);
     c->kernels += 1;
   }
@@ -241,20 +296,28 @@ exageo_status do_generate(exageo_ctx* c, const exageo_theta* t, int64_t n, const
 }
 
 // ---------------------------------------------------------------------------- factorization
-// Factor owned panel k (left-looking over PB-wide column blocks) on stream s.
-void factor_panel(exageo_ctx* c, RankState& R, int k, cudaStream_t s) {
+// W_s = L_ss^{-1} of 64-block sb of panel k (written by F(k) on the diagonal rank, broadcast with
+// L_kk down the process column for the other ranks' TRSM)
+double* w_block(RankState& R, int k, int sb) {
+  return R.lkk[k & 1] + (size_t)R.L.nb * R.L.nb + (size_t)sb * PB * PB;
+}
+
+// Factor local panel k on its diagonal rank (left-looking over PB-wide column blocks) on s:
+// the diagonal tile is the top of the local panel, every row below (the rank's other tile rows
+// of column k and the z row block, if stored here) gets the panel update and the TRSM.
+exageo_status factor_panel(exageo_ctx* c, RankState& R, int k, cudaStream_t s) {
   const Layout& L = R.L;
   const int nsub = L.nb / PB;
   double* Pk = R.ws + L.off(k);
   const int64_t ldk = L.ld(k);
-  const int m = (k - L.rank) / L.world;  // local panel index
+  const int m = (k - L.q) / L.Q;  // local panel index
   for (int sb = 0; sb < nsub; ++sb) {
     const int64_t c0 = (int64_t)sb * PB;
     if ((int64_t)k * L.nb + c0 >= L.n) {
       // the rest of the (last) panel is identity padding (R12): generated as I with zero
       // rows/columns around it and never touched by an update, it already is its own factor
       // (L = I, log L_ii = 0) -- skip its POTRF/TRSM/GEMM launches
-      cudaMemsetAsync(R.slots + (int64_t)m * nsub + sb, 0, sizeof(double) * (nsub - sb), s);
+      CUDA_TRY(c, cudaMemsetAsync(R.slots + (int64_t)m * nsub + sb, 0, sizeof(double) * (nsub - sb), s));
       break;
     }
     // at small n the panel chain is the critical path: its kernels use programmatic
@@ -266,12 +329,37 @@ void factor_panel(exageo_ctx* c, RankState& R, int k, cudaStream_t s) {
                         pdl);
       c->kernels += 1;
     }
-    launch_potrf_block(Pk + c0 * ldk + c0, ldk, R.W, R.slots + (int64_t)m * nsub + sb, R.info,
-                       (int64_t)k * L.nb + c0, s, pdl && !first);
+    double* W = w_block(R, k, sb);
+    launch_potrf_block(Pk + c0 * ldk + c0, ldk, W, R.slots + (int64_t)m * nsub + sb, R.info, (int64_t)k * L.nb + c0,
+                       s, pdl && !first);
     double* below = Pk + c0 * ldk + c0 + PB;
-    launch_gemm_panel(ldk - c0 - PB, PB, PB, below, ldk, R.W, PB, below, ldk, false, R.info, s, pdl);
+    launch_gemm_panel(ldk - c0 - PB, PB, PB, below, ldk, W, PB, below, ldk, false, R.info, s, pdl);
     c->kernels += 2;
   }
+  return EXAGEO_OK;
+}
+
+// P > 1: the other ranks of panel k's process column apply F(k)'s column operations to their
+// tile rows with the received L_kk and W_s (lkk[k % 2]): for each 64-block s, the left-looking
+// update A_s -= A_{<s} L_kk[s, <s]^T, then A_s <- A_s W_s^T (the TRSM of Fig. 2 by the inverse).
+exageo_status trsm_panel(exageo_ctx* c, RankState& R, int k, cudaStream_t s) {
+  const Layout& L = R.L;
+  const int nsub = L.nb / PB;
+  double* Pk = R.ws + L.off(k);
+  const int64_t ldk = L.ld(k);
+  const double* Lkk = R.lkk[k & 1];
+  if (ldk <= 0) return EXAGEO_OK;
+  for (int sb = 0; sb < nsub; ++sb) {
+    const int64_t c0 = (int64_t)sb * PB;
+    if ((int64_t)k * L.nb + c0 >= L.n) break;  // identity padding: no-op (R12)
+    if (sb > 0) {
+      launch_gemm_panel(ldk, PB, (int)c0, Pk, ldk, Lkk + c0, L.nb, Pk + c0 * ldk, ldk, true, R.info, s);
+      c->kernels += 1;
+    }
+    launch_gemm_panel(ldk, PB, PB, Pk + c0 * ldk, ldk, w_block(R, k, sb), PB, Pk + c0 * ldk, ldk, false, R.info, s);
+    c->kernels += 1;
+  }
+  return EXAGEO_OK;
 }
 
 RankState* local_state(exageo_ctx* c, int rank) {
@@ -279,72 +367,168 @@ RankState* local_state(exageo_ctx* c, int rank) {
   return rank == c->rank ? &c->rs[0] : nullptr;
 }
 
-const double* panel_src(const RankState& R, int k) {
-  return R.L.owns(k) ? R.ws + R.L.off(k) : R.recv[k & 1];
+// Operands of panel k on rank state R: slice pp = the local panel k of rank (pp, k mod Q) --
+// R's own storage when R is that rank, else the received copy.
+void panel_slices(RankState& R, int k, const double** sl, int64_t* sld) {
+  const Layout& L = R.L;
+  for (int pp = 0; pp < L.P; ++pp) {
+    sl[pp] = (L.owns(k) && pp == L.p) ? R.ws + L.off(k) : R.recv[k & 1][pp];
+    sld[pp] = L.ld_of(pp, k);
+  }
 }
 
-// algorithmic flops of updating panels J0, J0 + world, ... (npan) by one panel:
-// 2 nb per (row, column) pair of the true lower triangle, plus the z row
+// algorithmic flops of updating local panels J0, J0 + Q, ... (npan) by one panel: 2 nb per
+// (row, column) pair of the true lower triangle stored on this rank, plus the z row
 double update_flops(const Layout& L, int k, int J0, int npan) {
   double f = 0.0;
-  const int64_t rend = std::min<int64_t>((int64_t)L.sb_end(k) * L.nb, L.n);
+  const int E = L.sb_end(k);
   for (int i = 0; i < npan; ++i) {
-    const int64_t c0 = (int64_t)(J0 + i * L.world) * L.nb;
+    const int J = J0 + i * L.Q;
+    const int64_t c0 = (int64_t)J * L.nb;
     const int64_t c1 = (c0 + L.nb) < L.n ? (c0 + L.nb) : L.n;
-    for (int64_t cc = c0; cc < c1; ++cc) f += 2.0 * L.nb * (double)(rend - cc + 1);
+    if (c1 <= c0) continue;
+    for (int I = J; I < E; ++I) {
+      if (I % L.P != L.p) continue;
+      const int64_t r0 = (int64_t)I * L.nb, r1 = (r0 + L.nb) < L.n ? (r0 + L.nb) : L.n;
+      if (r1 <= r0) continue;
+      if (I > J) {
+        f += 2.0 * L.nb * (double)(r1 - r0) * (double)(c1 - c0);
+      } else {  // diagonal tile: pairs r >= c
+        for (int64_t cc = c0; cc < c1; ++cc) f += 2.0 * L.nb * (double)(r1 - cc);
+      }
+    }
+    if (L.has_z()) f += 2.0 * L.nb * (double)(c1 - c0);
   }
   return f;
 }
 
-// Make panel j (factored by its owner) available to every rank: NCCL broadcast, or
-// device copies between virtual ranks. Buffer j % 2 of a receiver was last read by
-// U1(j-2) / U2(j-2); those events gate the overwrite.
-exageo_status broadcast_panel(exageo_ctx* c, int j) {
+ncclComm_t row_comm(const exageo_ctx* c) { return c->P == 1 ? c->comm : c->comm_row; }
+
+// Make panel j (factored on its process column) available to every rank:
+//   (a) P > 1: the diagonal rank broadcasts [L_jj | W_s] down process column j mod Q; the other
+//       ranks of that column apply the column operations of F(j) to their tile rows (trsm_panel);
+//   (b) each rank of process column j mod Q broadcasts its local panel j along its process row;
+//   (c) P > 1: every rank re-broadcasts the slice of its process row down its process column,
+//       so each rank holds all P slices (the rows of its tile rows and of its tile columns).
+// NCCL on the row / column communicators, or device copies between virtual ranks. Buffers of
+// parity j % 2 were last read by U1(j-2) / U2(j-2) (and L_kk by trsm(j-2)): those events gate
+// the overwrite. Records ev_recv[j % 2] on every rank's s_comm.
+exageo_status exchange_panel(exageo_ctx* c, int j) {
   if (c->world == 1 && !c->comm) return EXAGEO_OK;
-  const int o = j % c->world;
-  const size_t bytes = (size_t)c->G.ld(j) * c->G.nb * sizeof(double);
+  const Layout& G = c->G;
+  const int P = c->P, Q = c->Q, qj = j % Q, pj = j % P;
+  const size_t nbd = (size_t)G.nb;
+  const size_t lkk_count = nbd * nbd + 64 * nbd;
   if (!c->virt) {
     RankState& R = c->rs[0];
-    double* buf;
-    if (R.L.owns(j)) {
-      CUDA_TRY(c, cudaStreamWaitEvent(R.s_comm, R.ev_F, 0));
-      buf = R.ws + R.L.off(j);
-    } else {
-      if (j >= 2) {
-        CUDA_TRY(c, cudaStreamWaitEvent(R.s_comm, R.ev_U2[j & 1], 0));
-        CUDA_TRY(c, cudaStreamWaitEvent(R.s_comm, R.ev_U1[j & 1], 0));
-      }
-      buf = R.recv[j & 1];
+    const Layout& L = R.L;
+    const bool incol = L.owns(j);
+    if (j >= 2) {  // release the parity-(j % 2) buffers
+      CUDA_TRY(c, cudaStreamWaitEvent(R.s_comm, R.ev_U2[j & 1], 0));
+      CUDA_TRY(c, cudaStreamWaitEvent(R.s_comm, R.ev_U1[j & 1], 0));
     }
-    NCCL_TRY(c, nccl::Broadcast(buf, buf, bytes / sizeof(double), ncclDouble, o, c->comm, R.s_comm));
+    if (P > 1 && incol) {  // (a)
+      double* buf = R.lkk[j & 1];
+      if (L.diag(j)) {
+        CUDA_TRY(c, cudaStreamWaitEvent(R.s_comm, R.ev_F, 0));
+        CUDA_TRY(c, cudaMemcpy2DAsync(buf, nbd * sizeof(double), R.ws + L.off(j), (size_t)L.ld(j) * sizeof(double),
+                                      nbd * sizeof(double), nbd, cudaMemcpyDeviceToDevice, R.s_comm));
+      }
+      NCCL_TRY(c, nccl::Broadcast(buf, buf, lkk_count, ncclDouble, pj, c->comm_col, R.s_comm));
+      if (!L.diag(j)) {
+        CUDA_TRY(c, cudaEventRecord(R.ev_lkk, R.s_comm));
+        CUDA_TRY(c, cudaStreamWaitEvent(R.s_la, R.ev_lkk, 0));
+        exageo_status st = trsm_panel(c, R, j, R.s_la);
+        if (st != EXAGEO_OK) return st;
+        CUDA_TRY(c, cudaEventRecord(R.ev_F, R.s_la));
+      }
+    }
+    double* own = incol ? R.ws + L.off(j) : R.recv[j & 1][L.p];
+    if (incol) CUDA_TRY(c, cudaStreamWaitEvent(R.s_comm, R.ev_F, 0));
+    if (Q > 1 || P == 1)  // (b); with world 1 and a communicator: exercises the NCCL path
+      NCCL_TRY(c, nccl::Broadcast(own, own, (size_t)L.ld(j) * nbd, ncclDouble, qj, row_comm(c), R.s_comm));
+    if (P > 1) {  // (c)
+      NCCL_TRY(c, nccl::GroupStart());
+      for (int pp = 0; pp < P; ++pp) {
+        double* buf = pp == L.p ? own : R.recv[j & 1][pp];
+        NCCL_TRY(c, nccl::Broadcast(buf, buf, (size_t)L.ld_of(pp, j) * nbd, ncclDouble, pp, c->comm_col, R.s_comm));
+      }
+      NCCL_TRY(c, nccl::GroupEnd());
+    }
     CUDA_TRY(c, cudaEventRecord(R.ev_recv[j & 1], R.s_comm));
     return EXAGEO_OK;
   }
-  RankState& Ro = c->rs[o];
-  const double* src = Ro.ws + Ro.L.off(j);
-  for (int r = 0; r < c->world; ++r) {
-    if (r == o) continue;
-    RankState& R = c->rs[r];
-    CUDA_TRY(c, cudaStreamWaitEvent(R.s_comm, Ro.ev_F, 0));
+  // virtual ranks: the same data movement as device copies, ordered by events
+  auto rid = [&](int pp, int qq) { return pp * Q + qq; };
+  for (auto& R : c->rs)
     if (j >= 2) {
       CUDA_TRY(c, cudaStreamWaitEvent(R.s_comm, R.ev_U2[j & 1], 0));
       CUDA_TRY(c, cudaStreamWaitEvent(R.s_comm, R.ev_U1[j & 1], 0));
     }
-    CUDA_TRY(c, cudaMemcpyAsync(R.recv[j & 1], src, bytes, cudaMemcpyDeviceToDevice, R.s_comm));
-    CUDA_TRY(c, cudaEventRecord(R.ev_recv[j & 1], R.s_comm));
+  if (P > 1) {  // (a)
+    RankState& D = c->rs[rid(pj, qj)];
+    CUDA_TRY(c, cudaStreamWaitEvent(D.s_comm, D.ev_F, 0));
+    CUDA_TRY(c, cudaMemcpy2DAsync(D.lkk[j & 1], nbd * sizeof(double), D.ws + D.L.off(j),
+                                  (size_t)D.L.ld(j) * sizeof(double), nbd * sizeof(double), nbd,
+                                  cudaMemcpyDeviceToDevice, D.s_comm));
+    CUDA_TRY(c, cudaEventRecord(D.ev_lkk, D.s_comm));
+    for (int pp = 0; pp < P; ++pp) {
+      if (pp == pj) continue;
+      RankState& R = c->rs[rid(pp, qj)];
+      CUDA_TRY(c, cudaStreamWaitEvent(R.s_comm, D.ev_lkk, 0));
+      CUDA_TRY(c, cudaMemcpyAsync(R.lkk[j & 1], D.lkk[j & 1], lkk_count * sizeof(double), cudaMemcpyDeviceToDevice,
+                                  R.s_comm));
+      CUDA_TRY(c, cudaEventRecord(R.ev_lkk, R.s_comm));
+      CUDA_TRY(c, cudaStreamWaitEvent(D.s_comm, R.ev_lkk, 0));  // D's buffer is free again after this copy
+      CUDA_TRY(c, cudaStreamWaitEvent(R.s_la, R.ev_lkk, 0));
+      exageo_status st = trsm_panel(c, R, j, R.s_la);
+      if (st != EXAGEO_OK) return st;
+      CUDA_TRY(c, cudaEventRecord(R.ev_F, R.s_la));
+    }
   }
+  // (b) row copies: rank (p, q != qj) receives the local panel j of rank (p, qj)
+  for (auto& R : c->rs) {
+    const Layout& L = R.L;
+    if (L.owns(j)) continue;
+    RankState& S = c->rs[rid(L.p, qj)];
+    CUDA_TRY(c, cudaStreamWaitEvent(R.s_comm, S.ev_F, 0));
+    CUDA_TRY(c, cudaMemcpyAsync(R.recv[j & 1][L.p], S.ws + S.L.off(j), (size_t)L.ld(j) * nbd * sizeof(double),
+                                cudaMemcpyDeviceToDevice, R.s_comm));
+    CUDA_TRY(c, cudaEventRecord(R.ev_row, R.s_comm));
+  }
+  // (c) column copies: rank (p, q) receives slice pp from rank (pp, q)
+  if (P > 1) {
+    for (auto& R : c->rs) {
+      const Layout& L = R.L;
+      for (int pp = 0; pp < P; ++pp) {
+        if (pp == L.p) continue;
+        RankState& S = c->rs[rid(pp, L.q)];
+        const double* src = S.L.owns(j) ? S.ws + S.L.off(j) : S.recv[j & 1][pp];
+        CUDA_TRY(c, cudaStreamWaitEvent(R.s_comm, S.L.owns(j) ? S.ev_F : S.ev_row, 0));
+        CUDA_TRY(c, cudaMemcpyAsync(R.recv[j & 1][pp], src, (size_t)L.ld_of(pp, j) * nbd * sizeof(double),
+                                    cudaMemcpyDeviceToDevice, R.s_comm));
+      }
+    }
+    // a source's slice buffer may be refilled (step j + 2) only after its column peers copied it
+    for (auto& R : c->rs) CUDA_TRY(c, cudaEventRecord(R.ev_row, R.s_comm));
+    for (auto& S : c->rs)
+      for (int pp = 0; pp < P; ++pp)
+        if (pp != S.L.p) CUDA_TRY(c, cudaStreamWaitEvent(S.s_comm, c->rs[rid(pp, S.L.q)].ev_row, 0));
+  }
+  for (auto& R : c->rs) CUDA_TRY(c, cudaEventRecord(R.ev_recv[j & 1], R.s_comm));
   return EXAGEO_OK;
 }
 
 // Right-looking tile Cholesky with depth-1 lookahead (the paper's "updates of the
 // trailing submatrix may be triggered before the current panel factorization is
 // complete"), as prioritised CUDA streams instead of a runtime DAG:
-//   s_la  (high priority): on the owner of panel k+1, U1(k) = update of panel k+1 by
-//                          panel k, then F(k+1)
-//   s_main (low priority): U2(k) = update of the rank's other panels > k by panel k
-//   s_comm:                broadcast of panel k+1 once factored
+//   s_la  (high priority): on the ranks of panel k+1's process column, U1(k) = update of
+//                          local panel k+1 by panel k, then F(k+1) on its diagonal rank
+//                          (trsm_panel on the others, in exchange_panel)
+//   s_main (low priority): U2(k) = update of the rank's other local panels > k by panel k
+//   s_comm:                exchange of panel k+1 once factored
 // Dependencies: U1(k) after U2(k-1) and panel k; U2(k) after panel k. F(k+1) and the
-// broadcast overlap U2(k).
+// exchange overlap U2(k).
 exageo_status do_factor(exageo_ctx* c) {
   if (!c->have_matrix) return fail(c, EXAGEO_EINVAL, "no generated matrix in the workspace");
   const Layout& G = c->G;
@@ -354,17 +538,21 @@ exageo_status do_factor(exageo_ctx* c) {
     R.n_u2 = 0;
     R.u2_flops = 0.0;
   }
-  if (RankState* R0 = local_state(c, 0)) {
-    factor_panel(c, *R0, 0, R0->s_la);
-    CUDA_TRY(c, cudaEventRecord(R0->ev_F, R0->s_la));
-  }
-  exageo_status st = broadcast_panel(c, 0);
-  if (st != EXAGEO_OK) return st;
+  exageo_status st;
+  for (auto& R : c->rs)
+    if (R.L.diag(0)) {
+      if ((st = factor_panel(c, R, 0, R.s_la)) != EXAGEO_OK) return st;
+      CUDA_TRY(c, cudaEventRecord(R.ev_F, R.s_la));
+    }
+  if ((st = exchange_panel(c, 0)) != EXAGEO_OK) return st;
   for (int k = 0; k + 1 < G.T; ++k) {
     for (auto& R : c->rs) {
       const Layout& L = R.L;
-      const double* Pk = panel_src(R, k);
-      cudaEvent_t avail = L.owns(k) ? R.ev_F : R.ev_recv[k & 1];
+      const double* sl[kMaxP];
+      int64_t sld[kMaxP];
+      panel_slices(R, k, sl, sld);
+      // panel k's operands: the rank's own factored panel (1-D owner) or the exchange
+      cudaEvent_t avail = (L.P == 1 && L.owns(k)) ? R.ev_F : R.ev_recv[k & 1];
       const bool owns_next = L.owns(k + 1);
       // U2(k) needs panel k: wait now, before ev_F is re-recorded for F(k+1) below
       CUDA_TRY(c, cudaStreamWaitEvent(R.s_main, avail, 0));
@@ -372,19 +560,22 @@ exageo_status do_factor(exageo_ctx* c) {
         CUDA_TRY(c, cudaStreamWaitEvent(R.s_la, avail, 0));
         if (k > 0) CUDA_TRY(c, cudaStreamWaitEvent(R.s_la, R.ev_U2[(k - 1) & 1], 0));
         if (k + 1 < L.sb_end(k)) {  // (IND: panel k+1 opens a new super tile: no update)
-          launch_syrk_panels(L, R.ws, Pk, k, k + 1, 1, R.info, R.s_la);  // U1(k)
+          if (L.P == 1) launch_syrk_panels(L, R.ws, sl[0], k, k + 1, 1, R.info, R.s_la);  // U1(k)
+          else launch_syrk_panels_2d(L, R.ws, sl, sld, k, k + 1, 1, R.info, R.s_la);
           c->kernels += 1;
         }
         CUDA_TRY(c, cudaEventRecord(R.ev_U1[k & 1], R.s_la));
-        factor_panel(c, R, k + 1, R.s_la);  // F(k+1)
-        CUDA_TRY(c, cudaEventRecord(R.ev_F, R.s_la));
+        if (L.diag(k + 1)) {
+          if ((st = factor_panel(c, R, k + 1, R.s_la)) != EXAGEO_OK) return st;  // F(k+1)
+          CUDA_TRY(c, cudaEventRecord(R.ev_F, R.s_la));
+        }
       } else {
         CUDA_TRY(c, cudaEventRecord(R.ev_U1[k & 1], R.s_la));  // nothing read on s_la this step
       }
-      // panels updated by panel k: up to the end of k's diagonal super tile (T when exact)
+      // local panels updated by panel k: up to the end of k's diagonal super tile (T when exact)
       const int Jend = L.sb_end(k);
       const int J0 = L.first_owned_from(owns_next ? k + 2 : k + 1);
-      const int npan = J0 < Jend ? (Jend - 1 - J0) / L.world + 1 : 0;
+      const int npan = J0 < Jend ? (Jend - 1 - J0) / L.Q + 1 : 0;
       if (npan > 0) {
         if ((int)R.u2b.size() <= R.n_u2) {
           cudaEvent_t b, e;
@@ -394,7 +585,8 @@ exageo_status do_factor(exageo_ctx* c) {
           R.u2e.push_back(e);
         }
         CUDA_TRY(c, record_timing(c, R.u2b[R.n_u2], R.s_main));
-        launch_syrk_panels(L, R.ws, Pk, k, J0, npan, R.info, R.s_main);  // U2(k)
+        if (L.P == 1) launch_syrk_panels(L, R.ws, sl[0], k, J0, npan, R.info, R.s_main);  // U2(k)
+        else launch_syrk_panels_2d(L, R.ws, sl, sld, k, J0, npan, R.info, R.s_main);
         CUDA_TRY(c, record_timing(c, R.u2e[R.n_u2], R.s_main));
         ++R.n_u2;
         R.u2_flops += update_flops(L, k, J0, npan);
@@ -402,8 +594,7 @@ exageo_status do_factor(exageo_ctx* c) {
       }
       CUDA_TRY(c, cudaEventRecord(R.ev_U2[k & 1], R.s_main));
     }
-    st = broadcast_panel(c, k + 1);
-    if (st != EXAGEO_OK) return st;
+    if ((st = exchange_panel(c, k + 1)) != EXAGEO_OK) return st;
   }
   for (auto& R : c->rs) {
     CUDA_TRY(c, cudaEventRecord(R.ev_join[0], R.s_la));
@@ -497,9 +688,13 @@ std::vector<const void*> graph_key(const exageo_ctx* c, const double* x, const d
   std::vector<const void*> k = {(const void*)(intptr_t)c->G.n, (const void*)(intptr_t)c->G.nb, x, y, z,
                                 c->parts, c->out3, c->h_res, c->mtab, (const void*)(intptr_t)kind};
   for (const auto& R : c->rs) {
-    for (const void* p : {(const void*)R.ws, (const void*)R.slots, (const void*)R.recv[0], (const void*)R.recv[1],
-                          (const void*)R.W, (const void*)R.scratch, (const void*)R.info})
+    for (const void* p : {(const void*)R.ws, (const void*)R.slots, (const void*)R.lkk[0], (const void*)R.lkk[1],
+                          (const void*)R.offs_d, (const void*)R.scratch, (const void*)R.info})
       k.push_back(p);
+    for (int pp = 0; pp < kMaxP; ++pp) {
+      k.push_back(R.recv[0][pp]);
+      k.push_back(R.recv[1][pp]);
+    }
   }
   return k;
 }
@@ -695,13 +890,16 @@ namespace {
 
 void destroy_rank(RankState& R) {
   if (R.ws && !R.ws_external) cudaFree(R.ws);
-  for (auto p : R.recv) cudaFree(p);
-  cudaFree(R.W);
+  for (auto& b : R.recv)
+    for (auto p : b) cudaFree(p);
+  for (auto p : R.lkk) cudaFree(p);
+  cudaFree(R.offs_d);
   cudaFree(R.slots);
   cudaFree(R.scratch);
   cudaFree(R.info);
   cudaFree(R.part);
-  for (cudaEvent_t ev : {R.ev_F, R.ev_U2[0], R.ev_U2[1], R.ev_U1[0], R.ev_U1[1], R.ev_recv[0], R.ev_recv[1],
+  for (cudaEvent_t ev : {R.ev_F, R.ev_U2[0], R.ev_U2[1], R.ev_U1[0], R.ev_U1[1], R.ev_recv[0], R.ev_recv[1], R.ev_lkk,
+                         R.ev_row,
                          R.ev_join[0], R.ev_join[1], R.ev_join[2]})
     if (ev) cudaEventDestroy(ev);
   for (cudaEvent_t ev : R.u2b) cudaEventDestroy(ev);
@@ -718,9 +916,9 @@ cudaError_t init_rank(RankState& R) {
   if ((e = cudaStreamCreateWithPriority(&R.s_main, cudaStreamNonBlocking, lo)) != cudaSuccess) return e;
   if ((e = cudaStreamCreateWithPriority(&R.s_comm, cudaStreamNonBlocking, hi)) != cudaSuccess) return e;
   for (cudaEvent_t* ev : {&R.ev_F, &R.ev_U2[0], &R.ev_U2[1], &R.ev_U1[0], &R.ev_U1[1], &R.ev_recv[0], &R.ev_recv[1],
+                          &R.ev_lkk, &R.ev_row,
                           &R.ev_join[0], &R.ev_join[1], &R.ev_join[2]})
     if ((e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming)) != cudaSuccess) return e;
-  if ((e = cudaMalloc(&R.W, sizeof(double) * PB * PB)) != cudaSuccess) return e;
   if ((e = cudaMalloc(&R.scratch, sizeof(double) * kQuadBlocks)) != cudaSuccess) return e;
   if ((e = cudaMalloc(&R.info, sizeof(int))) != cudaSuccess) return e;
   return cudaMemset(R.info, 0, sizeof(int));
@@ -770,6 +968,12 @@ exageo_status exageo_create(exageo_ctx** out, const exageo_opts* opts) {
   if (o.world < 0 || o.virtual_ranks < 0 || (o.world > 1 && o.virtual_ranks > 1) ||
       (o.world > 1 && (o.rank < 0 || o.rank >= o.world || !o.nccl_id)))
     return fail(nullptr, EXAGEO_EINVAL, "bad distribution options (world/rank/nccl_id/virtual_ranks)");
+  {
+    const int ranks = o.virtual_ranks > 1 ? o.virtual_ranks : (o.world > 1 ? o.world : 1);
+    const int P = o.grid_rows > 1 ? o.grid_rows : 1;
+    if (o.grid_rows < 0 || P > kMaxP || ranks % P != 0)
+      return fail(nullptr, EXAGEO_EINVAL, "grid_rows must divide the number of ranks and be <= 8");
+  }
   int ndev = 0;
   cudaError_t e = cudaGetDeviceCount(&ndev);
   if (e != cudaSuccess || ndev == 0) {
@@ -787,6 +991,8 @@ exageo_status exageo_create(exageo_ctx** out, const exageo_opts* opts) {
   c->virt = o.virtual_ranks > 1;
   c->world = c->virt ? o.virtual_ranks : (o.world > 1 ? o.world : 1);
   c->rank = (!c->virt && o.world > 1) ? o.rank : 0;
+  c->P = o.grid_rows > 1 ? o.grid_rows : 1;
+  c->Q = c->world / c->P;
   auto bail = [&](cudaError_t err, const char* what) {
     g_create_err = std::string(what) + ": " + cudaGetErrorString(err);
     exageo_destroy(c);
@@ -829,6 +1035,16 @@ exageo_status exageo_create(exageo_ctx** out, const exageo_opts* opts) {
       exageo_destroy(c);
       return EXAGEO_ENCCL;
     }
+    if (c->P > 1) {  // process-row (color p, key q) and process-column (color q, key p) communicators
+      const int p = c->rank / c->Q, q = c->rank % c->Q;
+      r = nccl::CommSplit(c->comm, p, q, &c->comm_row, nullptr);
+      if (r == ncclSuccess) r = nccl::CommSplit(c->comm, q, p, &c->comm_col, nullptr);
+      if (r != ncclSuccess) {
+        g_create_err = std::string("ncclCommSplit: ") + nccl::GetErrorString(r);
+        exageo_destroy(c);
+        return EXAGEO_ENCCL;
+      }
+    }
   }
   *out = c;
   return EXAGEO_OK;
@@ -838,6 +1054,8 @@ void exageo_destroy(exageo_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
+  if (c->comm_row) nccl::CommDestroy(c->comm_row);
+  if (c->comm_col) nccl::CommDestroy(c->comm_col);
   if (c->comm) nccl::CommDestroy(c->comm);
   destroy_graph(c);
   if (c->h_res) cudaFreeHost(c->h_res);
@@ -948,7 +1166,9 @@ exageo_status exageo_simulate(exageo_ctx* c, const exageo_theta* t, int64_t n, c
   if (piv >= 0) return fail(c, EXAGEO_ENOTPD, "covariance not positive definite at pivot " + std::to_string(piv));
   // Alg. 1 l.7: z = L e -- per-panel partial products, summed over all panels (and ranks)
   const Layout& G = c->G;
-  const size_t need = sizeof(double) * (size_t)G.T * (size_t)G.N;
+  size_t slices_all = 0;
+  for (auto& R : c->rs) slices_all += (size_t)R.L.owned();
+  const size_t need = sizeof(double) * (slices_all > 0 ? slices_all : 1) * (size_t)G.N;
   RankState& R0 = c->rs[0];
   if (R0.part_cap < need) {
     cudaFree(R0.part);
@@ -1013,20 +1233,64 @@ exageo_status exageo_predict(exageo_ctx* c, const exageo_theta* t, int64_t n, co
   if (st != EXAGEO_OK) return st;
   if (piv >= 0) return fail(c, EXAGEO_ENOTPD, "covariance not positive definite at pivot " + std::to_string(piv));
   // backward solve L^T w = y, panel by panel from the last; each w_j is made available to
-  // every rank (NCCL broadcast from the panel's owner; virtual ranks share w)
+  // every rank (NCCL broadcast from the panel's diagonal rank; virtual ranks share w)
   const Layout& G = c->G;
-  for (int j = G.T - 1; j >= 0; --j) {
-    const int o = j % c->world;
-    if (RankState* R = local_state(c, o)) {
-      const double* P = R->ws + R->L.off(j);
-      const int64_t rows = G.N - (int64_t)(j + 1) * G.nb;
-      launch_backsolve_panel(P, G.ld(j), G.nb, (int64_t)(j + 1) * G.nb, rows, w, w + (int64_t)j * G.nb, ptr,
-                             c->stream);
-      c->kernels += rows > 0 ? 2 : 1;
+  if (c->P == 1) {
+    for (int j = G.T - 1; j >= 0; --j) {
+      const int o = j % c->world;
+      if (RankState* R = local_state(c, o)) {
+        const double* P = R->ws + R->L.off(j);
+        const int64_t rows = G.N - (int64_t)(j + 1) * G.nb;
+        launch_backsolve_panel(P, G.ld(j), G.nb, (int64_t)(j + 1) * G.nb, rows, w, w + (int64_t)j * G.nb, ptr,
+                               c->stream);
+        c->kernels += rows > 0 ? 2 : 1;
+      }
+      if (c->comm)
+        NCCL_TRY(c, nccl::Broadcast(w + (int64_t)j * G.nb, w + (int64_t)j * G.nb, G.nb, ncclDouble, o, c->comm,
+                                    c->stream));
     }
-    if (c->comm)
-      NCCL_TRY(c, nccl::Broadcast(w + (int64_t)j * G.nb, w + (int64_t)j * G.nb, G.nb, ncclDouble, o, c->comm,
-                                  c->stream));
+  } else {
+    // 2-D grid: y = L^{-1} z (the z rows, on one process row) replicated first; per panel j the
+    // ranks of its process column form partial sums over their tile rows below the diagonal,
+    // reduced onto the diagonal rank, which solves with L_jj and broadcasts w_j
+    double* yv = nullptr;
+    const size_t nvec = (size_t)G.N + (size_t)(kMaxP + 1) * G.nb;
+    CUDA_TRY(c, cudaMalloc(&yv, sizeof(double) * nvec));
+    Free g2{yv};
+    double* vecs = yv + G.N;  // P partial vectors (virtual) or {own partial, reduced sum} (NCCL)
+    CUDA_TRY(c, cudaMemsetAsync(yv, 0, sizeof(double) * (size_t)G.N, c->stream));
+    for (auto& R : c->rs) launch_read_zrow(R.L, R.ws, yv, c->stream);
+    c->kernels += (int64_t)c->rs.size();
+    if (c->comm) NCCL_TRY(c, nccl::AllReduce(yv, yv, (size_t)G.N, ncclDouble, ncclSum, c->comm, c->stream));
+    for (int j = G.T - 1; j >= 0; --j) {
+      double* wj = w + (int64_t)j * G.nb;
+      RankState* D = nullptr;
+      for (auto& R : c->rs) {
+        const Layout& L = R.L;
+        if (!L.owns(j)) continue;
+        if (L.diag(j)) D = &R;
+        const int64_t lr0 = L.diag(j) ? G.nb : 0;
+        const int64_t rows = L.lrows(j) - lr0;
+        double* out = c->virt ? vecs + (size_t)L.p * G.nb : vecs;
+        launch_backsolve_partial(L, j, R.ws + L.off(j), L.ld(j), lr0, rows, w, ptr, out, c->stream);
+        c->kernels += 2;
+      }
+      if (c->virt) {
+        launch_tile_solve(D->ws + D->L.off(j), D->L.ld(j), G.nb, yv + (int64_t)j * G.nb, vecs, c->P, wj, c->stream);
+        c->kernels += 1;
+      } else {
+        RankState& R = c->rs[0];
+        if (R.L.owns(j)) {
+          NCCL_TRY(c, nccl::Reduce(vecs, vecs + G.nb, G.nb, ncclDouble, ncclSum, j % c->P, c->comm_col, c->stream));
+          if (D) {
+            launch_tile_solve(D->ws + D->L.off(j), D->L.ld(j), G.nb, yv + (int64_t)j * G.nb, vecs + G.nb, 1, wj,
+                              c->stream);
+            c->kernels += 1;
+          }
+        }
+        NCCL_TRY(c, nccl::Broadcast(wj, wj, G.nb, ncclDouble, R.L.owner(j), c->comm, c->stream));
+      }
+    }
   }
   // Alg. 3 l.8 / Eq. (5): z1 = Sigma12 w with Sigma12 generated on the fly
   launch_krige(make_consts(*t, c), m, dxn, dyn, n, dx, dy, w, pkr, dzn, c->mtab, c->stream);
@@ -1044,6 +1308,8 @@ exageo_status exageo_predict_var(exageo_ctx* c, const exageo_theta* t, int64_t n
   if (!c) return fail(nullptr, EXAGEO_EINVAL, "NULL ctx");
   if (!var) return fail(c, EXAGEO_EINVAL, "NULL var");
   if (c->world != 1 || c->virt) return fail(c, EXAGEO_EINVAL, "the kriging variance needs a single-rank context");
+  if ((c->nb_opt > 0 ? c->nb_opt : auto_nb(n, 1)) > 1024)
+    return fail(c, EXAGEO_EINVAL, "the kriging variance supports tile sizes nb <= 1024 (one thread per tile row)");
   // mean (Eq. 5) -- leaves L of Sigma22 in the workspace
   exageo_status st = exageo_predict(c, t, n, x, y, z, m, xnew, ynew, znew);
   if (st != EXAGEO_OK) return st;

@@ -15,13 +15,22 @@ namespace exageo {
 // streams of the lookahead schedule and their events. In NCCL mode a process holds
 // one RankState; in virtual mode one process holds `world` of them on one device.
 struct RankState {
-  Layout L;                    // rank-local layout (rank, world)
+  Layout L;                    // rank-local layout (rank, world, process grid)
   double* ws = nullptr;        // owned panels
   size_t ws_bytes = 0;
   bool ws_external = false;
-  double* recv[2] = {nullptr, nullptr};  // copies of broadcast panels (world > 1)
-  size_t recv_bytes = 0;
-  double* W = nullptr;         // PB x PB inverse of the current diagonal block
+  std::vector<int64_t> offs_h; // P > 1: local panel offsets (host; L.offs_h points here)
+  int64_t* offs_d = nullptr;   // P > 1: the same on the device (L.offs_d)
+  size_t offs_cap = 0;
+  // received slices of panel k (world > 1), by k % 2 and source process row: slice pp is the
+  // local panel k of rank (pp, k mod Q); the rank's own slice when it stores panel k is its
+  // own storage
+  double* recv[2][kMaxP] = {};
+  size_t recv_bytes[kMaxP] = {};
+  // by k % 2: [L_kk (nb x nb, ld nb) | W_s = L_ss^{-1} of its nb/64 diagonal 64-blocks (64 x 64
+  // each)], written by F(k) on the diagonal rank and broadcast down its process column (P > 1)
+  double* lkk[2] = {nullptr, nullptr};
+  size_t lkk_bytes = 0;
   double* slots = nullptr;     // log-det partials: (nb / PB) per owned panel
   int64_t slots_cap = 0;
   double* scratch = nullptr;   // kQuadBlocks doubles
@@ -33,6 +42,8 @@ struct RankState {
   cudaEvent_t ev_U2[2] = {nullptr, nullptr};     // U2(k) done, by k % 2
   cudaEvent_t ev_U1[2] = {nullptr, nullptr};     // U1(k) done, by k % 2
   cudaEvent_t ev_recv[2] = {nullptr, nullptr};   // panel j received, by j % 2
+  cudaEvent_t ev_lkk = nullptr;                  // L_kk and W received (P > 1)
+  cudaEvent_t ev_row = nullptr;                  // row broadcast of the current panel done (virtual)
   cudaEvent_t ev_join[3] = {nullptr, nullptr, nullptr};
   std::vector<cudaEvent_t> u2b, u2e;             // timing of the bulk trailing update
   int n_u2 = 0;
@@ -53,8 +64,11 @@ struct exageo_ctx {
   double radius = 6371.0;
   int world = 1;       // ranks of the distribution (NCCL processes or virtual ranks)
   int rank = 0;        // this process's rank (NCCL mode), 0 otherwise
+  int P = 1, Q = 1;    // process grid (world = P Q)
   bool virt = false;   // virtual ranks: all `world` ranks in this process on one device
   ncclComm_t comm = nullptr;
+  ncclComm_t comm_row = nullptr;  // ranks of this process row (Q of them; key q), P > 1 or Q > 1
+  ncclComm_t comm_col = nullptr;  // ranks of this process column (P of them; key p)
   std::vector<exageo::RankState> rs;
   double* parts = nullptr;    // 2 * world doubles: per-rank {sum log L_ii, sum y^2}
   double* out3 = nullptr;     // {loglik, logdet, quad}

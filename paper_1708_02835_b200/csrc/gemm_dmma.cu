@@ -19,7 +19,8 @@ cudaError_t gemm_init() {
   cudaError_t e;
   if ((e = set_smem<PanelCfg, true, DenseMap>()) != cudaSuccess) return e;
   if ((e = set_smem<PanelCfg, false, DenseMap>()) != cudaSuccess) return e;
-  return set_smem<TrailCfg, true, SyrkMap>();
+  if ((e = set_smem<TrailCfg, true, SyrkMap>()) != cudaSuccess) return e;
+  return set_smem<TrailCfg, true, Syrk2DMap>();
 }
 
 void launch_gemm_panel(int64_t M, int N, int K, const double* A, int64_t lda, const double* B, int64_t ldb,
@@ -68,6 +69,23 @@ void launch_syrk_panels(const Layout& L, double* ws, const double* Pk, int k, in
   map.row_end = (int64_t)L.sb_end(k) * L.nb;  // N unless IND
   map.group = L.world == 1 ? syrk_group(L.nb) : 1;  // super panels: panel k's rows read once per group
   launch<TrailCfg, true, SyrkMap, true>(map, info, s);
+}
+
+void launch_syrk_panels_2d(const Layout& L, double* ws, const double* const* slices, const int64_t* slds, int k,
+                           int J0, int npan, const int* info, cudaStream_t s) {
+  if (npan <= 0) return;
+  Syrk2DMap map;
+  map.L = L;
+  map.ws = ws;
+  for (int i = 0; i < kMaxP; ++i) {
+    map.slice[i] = i < L.P ? slices[i] : nullptr;
+    map.sld[i] = i < L.P ? slds[i] : 0;
+  }
+  map.k = k;
+  map.J0 = J0;
+  map.npan = npan;
+  map.Eb = L.sb_end(k);
+  launch<TrailCfg, true, Syrk2DMap, true>(map, info, s);
 }
 
 }  // namespace exageo

@@ -182,6 +182,68 @@ struct SyrkMap {
   }
 };
 
+// Trailing update on a 2-D process grid (P > 1, internal.h): this rank's local panels
+// J = J0, J0 + Q, ... (npan of them) by panel k, whose rows arrive as P slices -- slice pp
+// is the local panel k of rank (pp, k mod Q): the tile rows I = pp (mod P), I >= k, plus the
+// z row block on the process row that holds it. The A operand of local panel J is this
+// rank's own slice p at the same local row shifted by (i0(J) - i0(k)) tiles (the z block
+// follows the square rows in both, so the shift is uniform); the B operand is tile J of
+// slice J mod P. Rows: the square rows of the tiles < Eb (T, or the end of the diagonal
+// super tile for IND) and the z block. CTA tiles BM x BN run panel by panel, row block by
+// row block (A rows reused across the nb / BN column tiles, tile J of B L2-resident for the
+// panel); sub-tiles strictly above the diagonal (only in the diagonal tile, on the rank of
+// process row J mod P) are skipped.
+struct Syrk2DMap {
+  Layout L;
+  double* ws;
+  const double* slice[kMaxP];
+  int64_t sld[kMaxP];
+  int k, J0, npan, Eb;
+
+  __host__ __device__ int64_t rows_sq(int J) const {
+    const int t = L.i0_of(L.p, Eb) - L.i0(J);
+    return t > 0 ? (int64_t)t * L.nb : 0;
+  }
+  __host__ __device__ int64_t mrows(int J) const { return rows_sq(J) + (L.has_z() ? ZR : 0); }
+
+  template <int BM, int BN>
+  __host__ __device__ __forceinline__ bool operator()(int64_t bid, GemmTile& t) const {
+    const int ct = L.nb / BN;
+    int64_t rem = bid;
+    int J = J0;
+    for (int m = 0; m < npan; ++m) {
+      J = J0 + m * L.Q;
+      const int64_t cnt = mrows(J) / BM * ct;
+      if (rem < cnt) break;
+      rem -= cnt;
+    }
+    const int64_t mt = rem / ct;
+    const int nt = (int)(rem % ct);
+    const int64_t rsq = rows_sq(J);
+    const int64_t lr = mt * BM < rsq ? mt * BM : L.lrows(J) + (mt * BM - rsq);
+    const int64_t shift = (int64_t)(L.i0(J) - L.i0(k)) * L.nb;
+    const int pJ = J % L.P;
+    const int64_t tB = (int64_t)((J - pJ) / L.P - L.i0_of(pJ, k)) * L.nb;
+    t.A = slice[L.p] + shift + lr;
+    t.lda = sld[L.p];
+    t.B = slice[pJ] + tB + (int64_t)nt * BN;
+    t.ldb = sld[pJ];
+    t.ldc = L.ld(J);
+    t.C = ws + L.off(J) + (int64_t)nt * BN * t.ldc + lr;
+    t.K = L.nb;
+    t.m_valid = BM;
+    t.n_valid = BN;
+    // strictly above the diagonal: only inside the diagonal tile (local rows [0, nb) of a
+    // panel whose diagonal tile is on this process row)
+    return !(pJ == L.p && lr < L.nb && lr + BM <= (int64_t)nt * BN);
+  }
+  __host__ int64_t blocks(int BM, int BN) const {
+    int64_t b = 0;
+    for (int m = 0; m < npan; ++m) b += mrows(J0 + m * L.Q) / BM * (L.nb / BN);
+    return b;
+  }
+};
+
 template <int BM_, int BN_, int BK_, int WARPS_M_, int WARPS_N_, int STAGES_, int MINB_>
 struct Cfg {
   static constexpr int BM = BM_, BN = BN_, BK = BK_, WARPS_M = WARPS_M_, WARPS_N = WARPS_N_, STAGES = STAGES_,

@@ -9,11 +9,15 @@
 //   (the forward solve of Alg. 2 l.4 fused as an augmented row).
 //   Rows/cols n..N-1 are identity padding (exact for log|Sigma| and z^T Sigma^-1 z).
 //
-// Distribution: panels are dealt 1-D block-cyclically over `world`
-// ranks, panel j on rank j % world. A rank stores only its own panels, back to
-// back in increasing j; global element (r, c) of an owned panel j = c / nb lives at
-//     ws + off(j) + (c - j*nb) * ld_j + (r - j*nb).
-// world = 1 is the single-GPU case (every panel owned, off(j) = sum_{t<j} nb ld_t).
+// Distribution: 2-D block-cyclic over a P x Q process grid, the layout of
+// ScaLAPACK the paper builds on: tile (I, J) lives on rank (I mod P, J mod Q),
+// rank id = p Q + q. A rank stores, for each of its tile columns J (J = q mod Q), its tile
+// rows I >= J (I = p mod P) stacked into one column-major "local panel" of lrows(J) rows,
+// followed by the z row block when its process row holds tile row T (T mod P == p); the
+// local panels lie back to back in increasing J. Local row lr < lrows(J) of panel J is global
+// row grow(J, lr); local panel J starts at ws + off(J) with leading dimension ld(J).
+// P = 1 is the 1-D column-cyclic layout (panel j on rank j % world, every tile row local:
+// ld(j) = N - j nb + ZR, closed-form offsets); world = 1 is the single-GPU case.
 #pragma once
 #include <cstddef>
 #include <cstdint>
@@ -24,15 +28,20 @@ namespace exageo {
 constexpr int ZR = 128;  // height of the z row block appended to every panel
 constexpr int PB = 64;   // inner panel block (POTRF block size)
 constexpr int kQuadBlocks = 148;  // CTAs of the local dot-product reduction
+constexpr int kMaxP = 8;          // process-grid rows supported by the trailing-update map
 
 struct Layout {
   int64_t n = 0;   // true problem size
   int nb = 0;      // tile size
-  int T = 0;       // number of panels
+  int T = 0;       // number of panels (tile columns)
   int64_t N = 0;   // padded size T*nb
-  int rank = 0;    // this rank
-  int world = 1;   // number of ranks (panel j lives on rank j % world)
+  int rank = 0;    // this rank = p Q + q
+  int world = 1;   // number of ranks = P Q
+  int P = 1, Q = 1, p = 0, q = 0;  // process grid and this rank's coordinates
   int ind = 0;     // IND approximation: diagonal super tiles of `ind` tiles; 0 = exact
+  // P > 1: offsets (doubles) of the local panels, owned() + 1 entries (host and device copies)
+  const int64_t* offs_h = nullptr;
+  const int64_t* offs_d = nullptr;
 
   // one past the last panel of the diagonal super tile holding panel k (T when exact)
   __host__ __device__ int sb_end(int k) const {
@@ -47,25 +56,65 @@ struct Layout {
     return r / w == c / w;
   }
 
-  __host__ __device__ int64_t ld(int j) const { return N - (int64_t)j * nb + ZR; }
-  __host__ __device__ bool owns(int j) const { return j % world == rank; }
-  __host__ __device__ int owner(int j) const { return j % world; }
-  // number of panels this rank owns
-  __host__ __device__ int owned() const { return T > rank ? (T - rank + world - 1) / world : 0; }
-  // j of the m-th owned panel
-  __host__ __device__ int owned_panel(int m) const { return rank + m * world; }
-  // first owned panel >= j
+  // ---- tile rows of process row pp ----
+  // local tile rows of process row pp (tiles I = pp mod P, I < T)
+  __host__ __device__ int Tp_of(int pp) const { return T > pp ? (T - pp + P - 1) / P : 0; }
+  // index of the first local tile row of process row pp that is >= J (= the count of those < J)
+  __host__ __device__ int i0_of(int pp, int J) const { return J <= pp ? 0 : (J - pp + P - 1) / P; }
+  __host__ __device__ bool has_z_of(int pp) const { return T % P == pp; }
+  __host__ __device__ int64_t lrows_of(int pp, int J) const {
+    const int t = Tp_of(pp) - i0_of(pp, J);
+    return t > 0 ? (int64_t)t * nb : 0;
+  }
+  __host__ __device__ int64_t ld_of(int pp, int J) const {
+    return P == 1 ? N - (int64_t)J * nb + ZR : lrows_of(pp, J) + (has_z_of(pp) ? ZR : 0);
+  }
+  // ---- this rank ----
+  __host__ __device__ int Tp() const { return Tp_of(p); }
+  __host__ __device__ int i0(int J) const { return P == 1 ? J : i0_of(p, J); }
+  __host__ __device__ bool has_z() const { return has_z_of(p); }
+  __host__ __device__ int64_t lrows(int J) const { return P == 1 ? N - (int64_t)J * nb : lrows_of(p, J); }
+  __host__ __device__ int64_t ld(int J) const { return ld_of(p, J); }
+  // global row of local row lr < lrows(J) of local panel J
+  __host__ __device__ int64_t grow(int J, int64_t lr) const {
+    if (P == 1) return (int64_t)J * nb + lr;
+    const int64_t t = lr / nb;
+    return ((int64_t)p + ((int64_t)i0(J) + t) * P) * nb + lr % nb;
+  }
+  // local row of global row r (r >= N: the z row block) in local panel J; -1 if not stored here
+  __host__ __device__ int64_t lrow(int J, int64_t r) const {
+    if (r >= N) return has_z() ? lrows(J) + (r - N) : -1;
+    if (r < (int64_t)J * nb) return -1;
+    const int I = (int)(r / nb);
+    if (I % P != p) return -1;
+    return (int64_t)((I - p) / P - i0(J)) * nb + r % nb;
+  }
+  // tile column j is stored on this rank's process column
+  __host__ __device__ bool owns(int j) const { return j % Q == q; }
+  // the rank holding the diagonal tile (j, j): it factors panel j
+  __host__ __device__ int owner(int j) const { return (j % P) * Q + j % Q; }
+  __host__ __device__ bool diag(int j) const { return j % Q == q && j % P == p; }
+  // number of tile columns this rank stores
+  __host__ __device__ int owned() const { return T > q ? (T - q + Q - 1) / Q : 0; }
+  // j of the m-th owned tile column
+  __host__ __device__ int owned_panel(int m) const { return q + m * Q; }
+  // first owned tile column >= j
   __host__ __device__ int first_owned_from(int j) const {
-    const int d = ((rank - j) % world + world) % world;
+    const int d = ((q - j) % Q + Q) % Q;
     return j + d;
   }
-  // local offset (doubles) of the m-th owned panel:
-  //   nb * sum_{i<m} ld(rank + i world) = nb [m (N + ZR - rank nb) - world nb m (m-1)/2]
+  // local offset (doubles) of the m-th owned panel; P = 1:
+  //   nb * sum_{i<m} ld(q + i Q) = nb [m (N + ZR - q nb) - Q nb m (m-1)/2]
   __host__ __device__ int64_t off_m(int64_t m) const {
-    return (int64_t)nb * (m * (N + ZR - (int64_t)rank * nb) - (int64_t)world * nb * (m * (m - 1) / 2));
+    if (P == 1) return (int64_t)nb * (m * (N + ZR - (int64_t)q * nb) - (int64_t)Q * nb * (m * (m - 1) / 2));
+#ifdef __CUDA_ARCH__
+    return offs_d[m];
+#else
+    return offs_h[m];
+#endif
   }
   // local offset of owned panel j
-  __host__ __device__ int64_t off(int j) const { return off_m((j - rank) / world); }
+  __host__ __device__ int64_t off(int j) const { return off_m((j - q) / Q); }
   // local storage (doubles)
   __host__ __device__ int64_t total() const { return off_m(owned()); }
 };
@@ -116,6 +165,10 @@ void launch_gemm_panel(int64_t M, int N, int K, const double* A, int64_t lda, co
 // A_rc -= sum_t L_rt L_ct for every lower element and the z row of those panels.
 void launch_syrk_panels(const Layout& L, double* ws, const double* Pk, int k, int J0, int npan, const int* info,
                         cudaStream_t s);
+// The same on a 2-D process grid (P > 1): panel k arrives as P slices (slices[pp] with
+// leading dimension slds[pp]: the local panel k of rank (pp, k mod Q)), gemm_dmma.cuh Syrk2DMap.
+void launch_syrk_panels_2d(const Layout& L, double* ws, const double* const* slices, const int64_t* slds, int k,
+                           int J0, int npan, const int* info, cudaStream_t s);
 // Factor the PB x PB diagonal block at `a` (ld) in place, write W = L^{-1} (PB x PB,
 // ld PB) and slot = sum log L_ii; info = first bad global pivot + 1.
 void launch_potrf_block(double* a, int64_t lda, double* W, double* logdet_slot, int* info, int64_t pivot_base,
@@ -145,6 +198,13 @@ void launch_trmv_sum(int64_t n, int64_t N, const double* part, int nparts, doubl
 int trsv_chunks(int64_t rows);
 void launch_backsolve_panel(const double* P, int64_t ld, int nb, int64_t row_after, int64_t rows,
                             const double* w, double* wj, double* part, cudaStream_t s);
+// 2-D layouts: out (nb) = sum over local rows lr0 .. lr0 + rows - 1 of local panel j (global
+// row L.grow(j, lr)) of L_rc w_r; part: trsv_chunks(rows) * nb scratch.
+void launch_backsolve_partial(const Layout& L, int j, const double* P, int64_t ld, int64_t lr0, int64_t rows,
+                              const double* w, double* part, double* out, cudaStream_t s);
+// L_jj^T w_j = y_j - sum_s parts[s] with the diagonal tile at the top of P (ld), y_j given.
+void launch_tile_solve(const double* P, int64_t ld, int nb, const double* yj, const double* parts, int nparts,
+                       double* wj, cudaStream_t s);
 // Kriging variance (trsv.cu): multi-RHS forward solve pieces. diag_solve: S (nb x cols, ld
 // lds) <- L_jj^{-1} S with the panel's diagonal tile; transpose: Bt = S^T (cols x rows);
 // column_var: var_c = theta1 - sum_{k<n} V_kc^2.

@@ -247,10 +247,11 @@ __device__ __forceinline__ double gen_entry(const Layout& L, const MaternConsts&
 
 constexpr int kGenCols = 8;  // columns per CTA: one (x, y) row load and index test serve 8 entries
 
-// One CTA per (owned panel j = rank + world * blockIdx.y, columns kGenCols * blockIdx.x ..)
-// -> walks the rows of those columns, two rows per thread and step, coalesced double2
-// stores down each column. Rows below the diagonal tile inside n (the bulk) take the
-// check-free path.
+// One CTA per (owned panel j = q + Q * blockIdx.y, columns kGenCols * blockIdx.x ..) -> walks
+// the local rows of those columns, two rows per thread and step, coalesced double2 stores
+// down each column. Local rows of tile rows strictly below the diagonal tile inside n (the
+// bulk) take the check-free path. Pairs of local rows (lr even) never straddle a tile, so
+// they are consecutive global rows (2-D layouts: internal.h grow()).
 template <int KIND>
 __global__ void __launch_bounds__(256) gen_panels_kernel(Layout L, double* __restrict__ ws, MaternConsts mc,
                                                          const double* __restrict__ x, const double* __restrict__ y,
@@ -259,7 +260,7 @@ __global__ void __launch_bounds__(256) gen_panels_kernel(Layout L, double* __res
   const int cc0 = blockIdx.x * kGenCols;
   const int64_t jb = (int64_t)j * L.nb;
   const int64_t ld = L.ld(j);
-  const int64_t R = L.N - jb;  // square rows of this panel
+  const int64_t R = L.lrows(j);  // square rows of this local panel (the z row block follows)
   double* col0 = ws + L.off(j) + (int64_t)cc0 * ld;
   __shared__ double xc[kGenCols], yc[kGenCols];
   if (threadIdx.x < kGenCols) {
@@ -270,8 +271,8 @@ __global__ void __launch_bounds__(256) gen_panels_kernel(Layout L, double* __res
   __syncthreads();
   const bool cols_in = jb + cc0 + kGenCols <= L.n;
   for (int64_t rr = 2 * (int64_t)threadIdx.x; rr < ld; rr += 2 * blockDim.x) {
-    const int64_t r0 = jb + rr;
-    if (cols_in && rr >= L.nb && r0 + 1 < L.n && L.in_super_tile(r0, jb)) {
+    const int64_t r0 = rr < R ? L.grow(j, rr) : L.N;  // global row of the pair (z block: N)
+    if (cols_in && rr < R && r0 >= jb + L.nb && r0 + 1 < L.n && L.in_super_tile(r0, jb)) {
       const double x0 = x[r0], y0 = y[r0], x1 = x[r0 + 1], y1 = y[r0 + 1];
 #pragma unroll 1
       for (int k = 0; k < kGenCols; ++k) {  // rolled: one inlined copy of the evaluator
@@ -288,7 +289,7 @@ __global__ void __launch_bounds__(256) gen_panels_kernel(Layout L, double* __res
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int64_t lr = rr + e;
-          if (lr < R) v[e] = gen_entry<KIND>(L, mc, x, y, jb + lr, c, xck, yck, tab);
+          if (lr < R) v[e] = gen_entry<KIND>(L, mc, x, y, r0 + e, c, xck, yck, tab);
           else v[e] = (lr == R && c < L.n && z != nullptr) ? z[c] : 0.0;  // z row block
         }
         *reinterpret_cast<double2*>(col0 + k * ld + rr) = make_double2(v[0], v[1]);

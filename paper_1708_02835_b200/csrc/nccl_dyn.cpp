@@ -14,6 +14,10 @@ ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
 ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
 ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
 ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+ncclResult_t (*Reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, int, ncclComm_t, cudaStream_t) = nullptr;
+ncclResult_t (*CommSplit)(ncclComm_t, int, int, ncclComm_t*, ncclConfig_t*) = nullptr;
+ncclResult_t (*GroupStart)() = nullptr;
+ncclResult_t (*GroupEnd)() = nullptr;
 const char* (*GetErrorString)(ncclResult_t) = nullptr;
 
 namespace {
@@ -45,7 +49,9 @@ bool load(std::string* err) {
   }
   bool ok = sym(h, "ncclGetUniqueId", GetUniqueId) && sym(h, "ncclCommInitRank", CommInitRank) &&
             sym(h, "ncclCommDestroy", CommDestroy) && sym(h, "ncclBroadcast", Broadcast) &&
-            sym(h, "ncclAllReduce", AllReduce) && sym(h, "ncclGetErrorString", GetErrorString);
+            sym(h, "ncclAllReduce", AllReduce) && sym(h, "ncclReduce", Reduce) && sym(h, "ncclCommSplit", CommSplit) &&
+            sym(h, "ncclGroupStart", GroupStart) && sym(h, "ncclGroupEnd", GroupEnd) &&
+            sym(h, "ncclGetErrorString", GetErrorString);
   if (!ok) {
     if (err) *err = g_err;
     return false;

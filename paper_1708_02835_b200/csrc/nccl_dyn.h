@@ -18,6 +18,10 @@ extern ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int);
 extern ncclResult_t (*CommDestroy)(ncclComm_t);
 extern ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
 extern ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t);
+extern ncclResult_t (*Reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, int, ncclComm_t, cudaStream_t);
+extern ncclResult_t (*CommSplit)(ncclComm_t, int, int, ncclComm_t*, ncclConfig_t*);
+extern ncclResult_t (*GroupStart)();
+extern ncclResult_t (*GroupEnd)();
 extern const char* (*GetErrorString)(ncclResult_t);
 
 }  // namespace nccl

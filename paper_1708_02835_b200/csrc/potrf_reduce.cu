@@ -377,19 +377,21 @@ __device__ double block_sum(double v, double* red) {
   return r;  // valid in thread 0
 }
 
-// y_c of owned column c (z row of its panel)
+// y_c of owned column c (z row of its local panel; only ranks whose process row holds the z
+// row block call this)
 __device__ __forceinline__ double zrow_value(const Layout& L, const double* ws, int64_t c) {
   const int j = (int)(c / L.nb);
   const int64_t jb = (int64_t)j * L.nb;
-  return ws[L.off(j) + (c - jb) * L.ld(j) + (L.N - jb)];
+  return ws[L.off(j) + (c - jb) * L.ld(j) + L.lrows(j)];
 }
 
 // Stage 1: kQuadBlocks CTAs; CTA b sums y_c^2 over a contiguous range of this rank's
-// columns (the owned panels' columns, in order, restricted to c < n).
+// columns (the owned panels' columns, in order, restricted to c < n); zero on ranks without
+// the z row block.
 __global__ void __launch_bounds__(512) quad_partial_kernel(Layout L, const double* __restrict__ ws,
                                                            double* __restrict__ part) {
   __shared__ double red[32];
-  const int64_t cols = (int64_t)L.owned() * L.nb;
+  const int64_t cols = L.has_z() ? (int64_t)L.owned() * L.nb : 0;
   const int64_t per = (cols + gridDim.x - 1) / gridDim.x;
   const int64_t lo = (int64_t)blockIdx.x * per;
   const int64_t hi = (lo + per) < cols ? (lo + per) : cols;
@@ -437,17 +439,22 @@ __global__ void combine_kernel(const double* __restrict__ parts, int nparts, int
   out3[2] = b;
 }
 
-// One CTA per owned column.
+// One CTA per owned column: its stored rows (global r >= c, r < n) into dense dst.
 __global__ void read_lower_kernel(Layout L, const double* __restrict__ ws, double* __restrict__ dst, int64_t ld) {
   const int64_t c = (int64_t)L.owned_panel((int)(blockIdx.x / L.nb)) * L.nb + blockIdx.x % L.nb;
   if (c >= L.n) return;
   const int j = (int)(c / L.nb);
   const int64_t jb = (int64_t)j * L.nb;
-  const double* col = ws + L.off(j) + (c - jb) * L.ld(j) - jb;  // index by global row
-  for (int64_t r = c + threadIdx.x; r < L.n; r += blockDim.x) dst[c * ld + r] = col[r];
+  const double* col = ws + L.off(j) + (c - jb) * L.ld(j);
+  const int64_t R = L.lrows(j);
+  for (int64_t lr = threadIdx.x; lr < R; lr += blockDim.x) {
+    const int64_t r = L.grow(j, lr);
+    if (r >= c && r < L.n) dst[c * ld + r] = col[lr];
+  }
 }
 
 __global__ void read_zrow_kernel(Layout L, const double* __restrict__ ws, double* __restrict__ dst) {
+  if (!L.has_z()) return;
   const int64_t cols = (int64_t)L.owned() * L.nb;
   for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < cols;
        idx += (int64_t)gridDim.x * blockDim.x) {
@@ -462,28 +469,31 @@ __global__ void read_entries_kernel(Layout L, const double* __restrict__ ws, int
     const int64_t r = rc[i], c = rc[count + i];
     const int j = (int)(c / L.nb);
     if (!L.owns(j)) continue;
+    const int64_t lr = L.lrow(j, r);
+    if (lr < 0) continue;
     const int64_t jb = (int64_t)j * L.nb;
-    out[i] = ws[L.off(j) + (c - jb) * L.ld(j) + (r - jb)];
+    out[i] = ws[L.off(j) + (c - jb) * L.ld(j) + lr];
   }
 }
 
-// TRMV stage 1: part[m][r] = sum_{c in owned panel m, c <= r, c < n} L_rc e_c  (grid: row blocks x owned panels).
+// TRMV stage 1: part[m][r] = sum_{c in owned panel m, c <= r, c < n} L_rc e_c for the global
+// rows r stored here (grid: local row blocks x owned panels); the other rows of part stay as
+// the caller zeroed them.
 __global__ void __launch_bounds__(256) trmv_partial_kernel(Layout L, const double* __restrict__ ws,
                                                            const double* __restrict__ e, double* __restrict__ part) {
   const int m = blockIdx.y;
   const int j = L.owned_panel(m);
   const int64_t jb = (int64_t)j * L.nb;
-  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= L.N) return;
+  const int64_t lr = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (lr >= L.lrows(j)) return;
+  const int64_t r = L.grow(j, lr);
+  const double* Pp = ws + L.off(j) + lr;
+  const int64_t ld = L.ld(j);
+  const int64_t cend = (r - jb + 1) < L.nb ? (r - jb + 1) : L.nb;
   double acc = 0.0;
-  if (r >= jb) {
-    const double* P = ws + L.off(j) + (r - jb);
-    const int64_t ld = L.ld(j);
-    const int64_t cend = (r - jb + 1) < L.nb ? (r - jb + 1) : L.nb;
-    for (int64_t cc = 0; cc < cend; ++cc) {
-      const int64_t c = jb + cc;
-      if (c < L.n) acc += P[cc * ld] * e[c];
-    }
+  for (int64_t cc = 0; cc < cend; ++cc) {
+    const int64_t c = jb + cc;
+    if (c < L.n) acc += Pp[cc * ld] * e[c];
   }
   part[(int64_t)m * L.N + r] = acc;
 }
@@ -557,7 +567,8 @@ void launch_read_entries(const Layout& L, const double* ws, int64_t count, const
 
 void launch_trmv_partial(const Layout& L, const double* ws, const double* e, double* part, cudaStream_t s) {
   if (L.owned() == 0) return;
-  dim3 g1((unsigned)((L.N + 255) / 256), (unsigned)L.owned());
+  cudaMemsetAsync(part, 0, sizeof(double) * (size_t)L.owned() * (size_t)L.N, s);
+  dim3 g1((unsigned)((L.lrows(L.owned_panel(0)) + 255) / 256), (unsigned)L.owned());
   trmv_partial_kernel<<<g1, 256, 0, s>>>(L, ws, e, part);
 }
 

@@ -19,13 +19,14 @@ namespace {
 constexpr int kColsPerCta = 8;  // columns of the panel per CTA in gemv_t
 constexpr int kRowChunk = 4096;
 
-__global__ void __launch_bounds__(256) gemv_t_kernel(const double* __restrict__ P, int64_t ld, int nb,
-                                                     int64_t row0, int64_t rows, const double* __restrict__ w,
+__global__ void __launch_bounds__(256) gemv_t_kernel(Layout L, int j, const double* __restrict__ P, int64_t ld,
+                                                     int64_t lr0, int64_t rows, const double* __restrict__ w,
                                                      double* __restrict__ part) {
-  // P: panel (column-major, ld), local row index lr corresponds to global row (row0 + lr - nb)
-  // when lr >= nb; here rows are local rows nb .. nb + rows - 1 of the panel, w indexed by
-  // the same global row.
+  // P: local panel j (column-major, ld); local rows lr0 .. lr0 + rows - 1 (square rows below
+  // the diagonal tile), the local row lr being global row L.grow(j, lr); w is indexed by
+  // global row.
   __shared__ double red[8][kColsPerCta];
+  const int nb = L.nb;
   const int c0 = blockIdx.x * kColsPerCta;
   const int64_t r_lo = (int64_t)blockIdx.y * kRowChunk;
   const int64_t r_hi = (r_lo + kRowChunk) < rows ? (r_lo + kRowChunk) : rows;
@@ -34,9 +35,9 @@ __global__ void __launch_bounds__(256) gemv_t_kernel(const double* __restrict__ 
   for (int q = 0; q < kColsPerCta; ++q) acc[q] = 0.0;
 #pragma unroll 4  // several rows' loads in flight per thread (the loop is HBM-latency bound)
   for (int64_t r = r_lo + threadIdx.x; r < r_hi; r += blockDim.x) {
-    const double wr = w[row0 + r];
+    const double wr = w[L.grow(j, lr0 + r)];
 #pragma unroll
-    for (int q = 0; q < kColsPerCta; ++q) acc[q] += P[(int64_t)(c0 + q) * ld + nb + r] * wr;
+    for (int q = 0; q < kColsPerCta; ++q) acc[q] += P[(int64_t)(c0 + q) * ld + lr0 + r] * wr;
   }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
@@ -53,35 +54,50 @@ __global__ void __launch_bounds__(256) gemv_t_kernel(const double* __restrict__ 
   }
 }
 
-// One CTA of nb threads (nb <= 1024): thread c owns column c of the diagonal tile.
+// out[c] = sum_s part[s][c], fixed order (one partial vector per rank for the 2-D solve).
+__global__ void sum_parts_kernel(const double* __restrict__ part, int nparts, int nb, double* __restrict__ out) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= nb) return;
+  double v = 0.0;
+  for (int s = 0; s < nparts; ++s) v += part[(int64_t)s * nb + c];
+  out[c] = v;
+}
+
+// One CTA of min(nb, 1024) threads: thread c owns columns c, c + blockDim.x, ... of the
+// diagonal tile. rhs_c = y_c - sum_s part[s][c]; y from yv (nb entries) when given, else
+// from the panel's z row (local row zrow).
 __global__ void tile_solve_kernel(const double* __restrict__ P, int64_t ld, int nb, int64_t zrow,
-                                  const double* __restrict__ part, int nparts, double* __restrict__ wj) {
+                                  const double* __restrict__ yv, const double* __restrict__ part, int nparts,
+                                  double* __restrict__ wj) {
   extern __shared__ double sh[];
   double* rhs = sh;            // nb
   double* blk = sh + nb;       // 64 x 65 diagonal block (column-major)
-  const int c = threadIdx.x;
-  double v = P[(int64_t)c * ld + zrow];  // y_c (z row of the panel)
-  for (int s = 0; s < nparts; ++s) v -= part[(int64_t)s * nb + c];
-  rhs[c] = v;
+  const int nt = blockDim.x;
+  for (int c = threadIdx.x; c < nb; c += nt) {
+    double v = yv ? yv[c] : P[(int64_t)c * ld + zrow];  // y_c
+    for (int s = 0; s < nparts; ++s) v -= part[(int64_t)s * nb + c];
+    rhs[c] = v;
+  }
   __syncthreads();
   for (int b = nb / 64 - 1; b >= 0; --b) {
     const int b0 = b * 64;
     // load the 64 x 64 diagonal block L[b0.., b0..]
-    for (int idx = c; idx < 64 * 64; idx += blockDim.x) {
+    for (int idx = threadIdx.x; idx < 64 * 64; idx += nt) {
       const int r = idx % 64, cc = idx / 64;
       blk[cc * 65 + r] = P[(int64_t)(b0 + cc) * ld + b0 + r];
     }
     __syncthreads();
     // backward substitution: w_k = (rhs_k - sum_{r > k} L_rk w_r) / L_kk, right-looking
     for (int k = 63; k >= 0; --k) {
-      if (c == 0) rhs[b0 + k] /= blk[k * 65 + k];
+      if (threadIdx.x == 0) rhs[b0 + k] /= blk[k * 65 + k];
       __syncthreads();
       const double wk = rhs[b0 + k];
+      const int c = threadIdx.x;
       if (c < k) rhs[b0 + c] -= blk[c * 65 + k] * wk;  // L_{k, c} = row k of column c
       __syncthreads();
     }
     // rhs_c -= sum_{r in block b} L_rc w_r for the columns c < b0 (rows of block b, column c)
-    if (c < b0) {
+    for (int c = threadIdx.x; c < b0; c += nt) {
       double acc = 0.0;
       const double* col = P + (int64_t)c * ld + b0;
       for (int r = 0; r < 64; ++r) acc += col[r] * rhs[b0 + r];
@@ -89,7 +105,7 @@ __global__ void tile_solve_kernel(const double* __restrict__ P, int64_t ld, int 
     }
     __syncthreads();
   }
-  wj[c] = rhs[c];
+  for (int c = threadIdx.x; c < nb; c += nt) wj[c] = rhs[c];
 }
 
 // ---- multi-right-hand-side forward solve L V = S for the kriging variance (exageo_predict_var)
@@ -180,13 +196,35 @@ int trsv_chunks(int64_t rows) { return rows > 0 ? (int)((rows + kRowChunk - 1) /
 
 void launch_backsolve_panel(const double* P, int64_t ld, int nb, int64_t row_after, int64_t rows,
                             const double* w, double* wj, double* part, cudaStream_t s) {
+  Layout L;  // 1-D panel: local row lr of panel j = row_after / nb - 1 is global row j nb + lr
+  L.nb = nb;
+  const int j = (int)(row_after / nb) - 1;
   const int nparts = trsv_chunks(rows);
   if (nparts > 0) {
     dim3 grid(nb / kColsPerCta, nparts);
-    gemv_t_kernel<<<grid, 256, 0, s>>>(P, ld, nb, row_after, rows, w, part);
+    gemv_t_kernel<<<grid, 256, 0, s>>>(L, j, P, ld, nb, rows, w, part);
   }
   const int64_t zrow = ld - ZR;  // local row of the z row
-  tile_solve_kernel<<<1, nb, (nb + 64 * 65) * sizeof(double), s>>>(P, ld, nb, zrow, part, nparts, wj);
+  const int nt = nb < 1024 ? nb : 1024;
+  tile_solve_kernel<<<1, nt, (nb + 64 * 65) * sizeof(double), s>>>(P, ld, nb, zrow, nullptr, part, nparts, wj);
+}
+
+void launch_backsolve_partial(const Layout& L, int j, const double* P, int64_t ld, int64_t lr0, int64_t rows,
+                              const double* w, double* part, double* out, cudaStream_t s) {
+  const int nparts = trsv_chunks(rows);
+  if (nparts > 0) {
+    dim3 grid(L.nb / kColsPerCta, nparts);
+    gemv_t_kernel<<<grid, 256, 0, s>>>(L, j, P, ld, lr0, rows, w, part);
+    sum_parts_kernel<<<(L.nb + 255) / 256, 256, 0, s>>>(part, nparts, L.nb, out);
+  } else {
+    cudaMemsetAsync(out, 0, sizeof(double) * L.nb, s);
+  }
+}
+
+void launch_tile_solve(const double* P, int64_t ld, int nb, const double* yj, const double* parts, int nparts,
+                       double* wj, cudaStream_t s) {
+  const int nt = nb < 1024 ? nb : 1024;
+  tile_solve_kernel<<<1, nt, (nb + 64 * 65) * sizeof(double), s>>>(P, ld, nb, 0, yj, parts, nparts, wj);
 }
 
 }  // namespace exageo

@@ -292,3 +292,71 @@ def test_virtual_ranks_not_pd_and_simulate():
     zo = oracle.simulate(x, y, (1.0, 0.1, 1.0), e)
     assert np.abs(z - zo).max() <= 1e-11 * np.abs(zo).max()
     c.close()
+
+
+# ---- 2-D block-cyclic P x Q process grids on one GPU (virtual ranks) --------
+GRIDS = [(1, 2), (2, 1), (2, 2), (2, 4), (4, 2), (3, 2)]  # (P, Q)
+
+
+@pytest.mark.parametrize("P,Q", GRIDS, ids=[f"{p}x{q}" for p, q in GRIDS])
+@pytest.mark.parametrize("n,nb", [(1000, 128), (2600, 256), (700, 128)])
+def test_grid_virtual_ranks_match_single_and_oracle(P, Q, n, nb):
+    x, y = ex.gen_locations(n, 21)
+    theta = (1.0, 0.1, 0.8)
+    z = oracle.simulate(x, y, (1.0, 0.1, 0.5), si.normals(n, 22))
+    single = ex.Context(device=0, nb=nb)
+    r1 = single.loglik(x, y, z, theta)
+    single.stage_generate_dev(dev(x), dev(y), dev(z), theta)
+    single.stage_factor()
+    L1, y1 = single.read_lower(n), single.read_zrow(n)
+    single.close()
+    c = ex.Context(device=0, nb=nb, virtual_ranks=P * Q, grid_rows=P)
+    r = c.loglik(x, y, z, theta)
+    assert_ll(r.loglik, oracle.loglik(x, y, z, theta), n, what=(P, Q, n, nb))
+    # same tile kernels in the same order per tile: only the final partial sums are grouped
+    # by rank
+    assert r.loglik == pytest.approx(r1.loglik, rel=1e-13)
+    assert r.logdet == pytest.approx(r1.logdet, rel=1e-13) and r.quad == pytest.approx(r1.quad, rel=1e-13)
+    # the factor and y read back from the block-cyclic tiles equal the single-GPU ones bitwise
+    c.stage_generate_dev(dev(x), dev(y), dev(z), theta)
+    c.stage_factor()
+    assert np.array_equal(c.read_lower(n), L1)
+    assert np.array_equal(c.read_zrow(n), y1)
+    c.close()
+
+
+@pytest.mark.parametrize("P,Q", [(2, 2), (2, 1), (4, 2)], ids=["2x2", "2x1", "4x2"])
+def test_grid_simulate_predict_not_pd(P, Q):
+    n, nb, theta = 900, 128, (1.0, 0.1, 1.0)
+    x, y = ex.gen_locations(n, 9)
+    e = si.normals(n, 10)
+    c = ex.Context(device=0, nb=nb, virtual_ranks=P * Q, grid_rows=P)
+    z = c.simulate(x, y, e, theta)
+    zo = oracle.simulate(x, y, theta, e)
+    assert np.abs(z - zo).max() <= 1e-11 * np.abs(zo).max()
+    xn, yn = ex.gen_locations(37, 11)
+    xn, yn = xn * 0.97 + 0.011, yn * 0.97 + 0.013
+    got = c.predict(x, y, z, xn, yn, theta)
+    ref = oracle.predict(x, y, z, xn, yn, theta)
+    assert np.abs(got - ref).max() <= 1e-9 * np.abs(ref).max()
+    xd = np.concatenate([x[:300], x[:1]])
+    yd = np.concatenate([y[:300], y[:1]])
+    with pytest.raises(ex.NotPositiveDefinite) as ei:
+        c.loglik(xd, yd, np.ones(301), theta)
+    assert ei.value.pivot == 300
+    c.close()
+
+
+def test_grid_ind_matches_single():
+    n, nb = 1500, 128
+    x, y = ex.gen_locations(n, 3)
+    z = si.normals(n, 4)
+    a = ex.Context(device=0, nb=nb, ind_tiles=3).loglik(x, y, z, (1.0, 0.1, 1.0))
+    b = ex.Context(device=0, nb=nb, ind_tiles=3, virtual_ranks=4, grid_rows=2).loglik(x, y, z, (1.0, 0.1, 1.0))
+    assert b.loglik == pytest.approx(a.loglik, rel=1e-13)
+
+
+def test_grid_rows_validation():
+    with pytest.raises(ex.ExageoError) as ei:
+        ex.Context(device=0, virtual_ranks=6, grid_rows=4)
+    assert ei.value.status == ex.EINVAL

@@ -21,6 +21,8 @@ int check(int T, int nb, int world, int rank, int k, int J0, int npan, int64_t r
   L.n = L.N - 3;
   L.rank = rank;
   L.world = world;
+  L.Q = world;
+  L.q = rank;
   static double ws_dummy[1], pk_dummy[1];
   SyrkMap m;
   m.L = L;
@@ -102,6 +104,8 @@ int check_offsets(int T, int nb, int world) {
     L.N = (int64_t)T * nb;
     L.rank = r;
     L.world = world;
+    L.Q = world;
+    L.q = r;
     int64_t expect_off = 0;
     for (int j = r; j < T; j += world) {
       if (L.off(j) != expect_off) {
@@ -141,6 +145,8 @@ int main() {
             L.T = T;
             L.rank = rank;
             L.world = world;
+            L.Q = world;
+            L.q = rank;
             // U1(k): panel k+1 on its owner; U2(k): owned panels from k+1 (or k+2)
             if (L.owns(k + 1)) {
               bad += check<64, 64>(T, nb, world, rank, k, k + 1, 1);
@@ -164,6 +170,8 @@ int main() {
         L.T = 20;
         L.rank = rank;
         L.world = world;
+        L.Q = world;
+        L.q = rank;
         L.ind = 3;
         const int e = L.sb_end(k);
         const int J0 = L.first_owned_from(L.owns(k + 1) ? k + 2 : k + 1);
