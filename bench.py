@@ -197,6 +197,17 @@ def run_reference(args):
 
 
 # ----------------------------------------------------------------------------- distributed helpers
+def grid_shape(spec: str, world: int):
+    """P x Q process grid for `world` ranks: "PxQ" (P Q = world), or "auto": the squarest
+    grid with P <= Q (1x1, 1x2, 2x2, 2x4 for 1/2/4/8 GPUs -- SURVEY §8(d) cfg 4)."""
+    if spec and spec != "auto":
+        P, Q = (int(v) for v in spec.lower().split("x"))
+        if P * Q != world:
+            raise SystemExit(f"--grid {spec}: P*Q must equal the number of ranks ({world})")
+        return P, Q
+    P = max(p for p in range(1, int(world**0.5) + 1) if world % p == 0)
+    return P, world // P
+
 def dist_env():
     """(rank, world, local_rank) from the torchrun environment (defaults: single process)."""
     return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
@@ -299,9 +310,11 @@ def run_gpu(args):
         torch.cuda.synchronize()
 
     stream = torch.cuda.Stream(device=local)
-    # one exact evaluation distributed over all ranks (1-D block-cyclic panels, NCCL
-    # panel broadcasts): strong scaling at fixed n
-    ctx = ex.Context(device=local, stream=stream, world=world, rank=rank, nccl_id=nccl_id)
+    # one exact evaluation distributed over all ranks (2-D block-cyclic tiles on a P x Q
+    # process grid, NCCL slice broadcasts along process rows and columns): strong scaling at
+    # fixed n (weak scaling: tools/scaling_sweep.sh scales n with the GPU count)
+    P, Q = grid_shape(args.grid, world)
+    ctx = ex.Context(device=local, stream=stream, world=world, rank=rank, nccl_id=nccl_id, grid_rows=P)
     n = args.n
     # inputs: jittered grid (Sec. 7.1) and z = L(theta) e (Alg. 1), identical on every rank -- untimed
     x, y = ex.gen_locations(n, SEED)
@@ -392,8 +405,8 @@ def run_gpu(args):
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"loglik n={n} theta={THETA} jittered grid, z=L e (BASELINE configs[2])",
                        "n": n, "nb": infos[-1]["nb"], "tiles": infos[-1]["ntiles"],
-                       "parallelism": f"1-D block-cyclic panels over {world} GPUs (NCCL)" if world > 1
-                       else "single GPU",
+                       "parallelism": f"2-D block-cyclic {P}x{Q} process grid over {world} GPUs (NCCL)"
+                       if world > 1 else "single GPU", "grid": f"{P}x{Q}",
                        "l2": "inputs (40.6 GB tiles) >> L2; no flush needed"},
             "loglik": r.loglik,
             "phase_ms": {"gen": statistics.mean(i["ms_gen"] for i in infos), "chol_and_solve": chol_ms,
@@ -431,6 +444,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--n", type=int, default=100_000)
+    ap.add_argument("--grid", default="auto", help="process grid PxQ for N > 1 GPUs (default: squarest, P <= Q)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-sample", type=int, default=5000)
     ap.add_argument("--ref-sample", type=int, default=5000, help="oracle sample n of --impl reference "

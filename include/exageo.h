@@ -138,6 +138,15 @@ void exageo_destroy(exageo_ctx* ctx);
  * (lower block-column panels plus the z row block). */
 size_t exageo_workspace_bytes(int64_t n, int nb);
 
+/* Bytes of device workspace one rank of a distributed context needs: its local panels of the
+ * 2-D block-cyclic layout -- the tile rows I = p mod P, I >= J, of its tile
+ * columns J = q mod Q, plus the z row block on the process row that holds it -- for n
+ * locations, tile size nb (0 = automatic as on a context with `world` ranks), `world` ranks
+ * on a grid_rows x (world / grid_rows) grid (0 = 1 x world) and rank = p Q + q. Host-only (no
+ * device needed); the ranks' values sum to exageo_workspace_bytes(n, nb) plus 2 KB per rank.
+ * Returns 0 on invalid arguments. */
+size_t exageo_rank_workspace_bytes(int64_t n, int nb, int world, int grid_rows, int rank);
+
 /* Hand the context a caller-owned device buffer (e.g. a torch tensor) to use
  * as tile workspace; it must stay alive while the context uses it. ptr = NULL
  * returns to library-managed allocation. */

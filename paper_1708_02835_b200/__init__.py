@@ -64,6 +64,8 @@ SIGNATURES = [
     ("exageo_create", ctypes.c_int, [ctypes.POINTER(_C), ctypes.POINTER(Opts)]),
     ("exageo_destroy", None, [_C]),
     ("exageo_workspace_bytes", ctypes.c_size_t, [ctypes.c_int64, ctypes.c_int]),
+    ("exageo_rank_workspace_bytes", ctypes.c_size_t, [ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                                      ctypes.c_int]),
     ("exageo_set_workspace", ctypes.c_int, [_C, ctypes.c_void_p, ctypes.c_size_t]),
     ("exageo_gen_locations", ctypes.c_int, [ctypes.c_int64, ctypes.c_uint64, _f64p, _f64p]),
     ("exageo_matern_cov", ctypes.c_int, [_C, ctypes.POINTER(Theta), ctypes.c_int64, _f64p, _f64p, ctypes.c_int64,
@@ -155,6 +157,11 @@ def gen_locations(n: int, seed: int):
 
 def workspace_bytes(n: int, nb: int = 0) -> int:
     return int(load_library().exageo_workspace_bytes(int(n), int(nb)))
+
+
+def rank_workspace_bytes(n: int, nb: int, world: int, grid_rows: int, rank: int) -> int:
+    """Device workspace of one rank of a grid_rows x (world / grid_rows) process grid (host-only)."""
+    return int(load_library().exageo_rank_workspace_bytes(int(n), int(nb), int(world), int(grid_rows), int(rank)))
 
 
 @dataclass

@@ -1079,6 +1079,18 @@ size_t exageo_workspace_bytes(int64_t n, int nb) {
   return local_bytes(make_layout(n, nb));
 }
 
+size_t exageo_rank_workspace_bytes(int64_t n, int nb, int world, int grid_rows, int rank) {
+  const int P = grid_rows > 1 ? grid_rows : 1;
+  if (n < 1 || world < 1 || rank < 0 || rank >= world || P > kMaxP || world % P != 0) return 0;
+  if (nb <= 0) nb = auto_nb(n, world);
+  if (nb % 128 != 0) return 0;
+  Layout L = make_layout(n, nb, rank, world, 0, P);
+  std::vector<int64_t> o(L.owned() + 1, 0);
+  for (int m = 0; m < L.owned(); ++m) o[m + 1] = o[m] + (int64_t)L.nb * L.ld(L.owned_panel(m));
+  L.offs_h = o.data();
+  return local_bytes(L);
+}
+
 exageo_status exageo_set_workspace(exageo_ctx* c, void* ptr, size_t bytes) {
   if (!c) return EXAGEO_EINVAL;
   if (c->virt) return fail(c, EXAGEO_EINVAL, "external workspace is not supported with virtual ranks");
