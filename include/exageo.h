@@ -149,8 +149,17 @@ size_t exageo_rank_workspace_bytes(int64_t n, int nb, int world, int grid_rows, 
 
 /* Hand the context a caller-owned device buffer (e.g. a torch tensor) to use
  * as tile workspace; it must stay alive while the context uses it. ptr = NULL
- * returns to library-managed allocation. */
+ * returns to library-managed allocation. ptr must be 256-byte aligned (the kernels
+ * store double2 and load 16-byte cp.async chunks), else EXAGEO_EINVAL. */
 exageo_status exageo_set_workspace(exageo_ctx* ctx, void* ptr, size_t bytes);
+
+/* Order the context's stream after all work submitted so far to `stream` (a cudaStream_t
+ * of the context's device, e.g. torch's current stream): records an event on `stream` and
+ * makes the context stream wait on it (no host synchronisation). The *_dev entry points
+ * read caller-owned device buffers on the context stream; call this first whenever those
+ * buffers were written on another stream. stream == NULL means the legacy default stream.
+ * EXAGEO_ECUDA on a CUDA failure. */
+exageo_status exageo_stream_wait(exageo_ctx* ctx, void* stream);
 
 /* Jittered-grid locations (Sec. 7.1; R1-R3):
  *   s_q = ((r - 0.5 + X_rl)/g, (l - 0.5 + Y_rl)/g), g = ceil(sqrt n),
@@ -283,7 +292,9 @@ exageo_status exageo_stage_finish(exageo_ctx* ctx, double* out3, int64_t* npd_pi
  * (Sigma after generate, L after factor) to host dense column-major
  * dst[i + j*ld], 0 <= j <= i < n; the strict upper triangle of dst is not
  * written. Synchronises. The read_* functions return the columns held by this
- * process (all of them unless world > 1 with NCCL; other columns read as 0). */
+ * process (all of them unless world > 1 with NCCL; other columns read as 0).
+ * read_lower stages a dense n x n copy on the device and the host, so it is limited
+ * to n <= 32768 (EXAGEO_EINVAL above; use exageo_read_entries for sampled entries). */
 exageo_status exageo_read_lower(exageo_ctx* ctx, double* dst, int64_t ld);
 /* Copy the current z row (z after generate, y = L^{-1} z after factor) to the
  * host array dst (n doubles). Synchronises. */

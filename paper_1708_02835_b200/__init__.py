@@ -67,6 +67,7 @@ SIGNATURES = [
     ("exageo_rank_workspace_bytes", ctypes.c_size_t, [ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                                       ctypes.c_int]),
     ("exageo_set_workspace", ctypes.c_int, [_C, ctypes.c_void_p, ctypes.c_size_t]),
+    ("exageo_stream_wait", ctypes.c_int, [_C, ctypes.c_void_p]),
     ("exageo_gen_locations", ctypes.c_int, [ctypes.c_int64, ctypes.c_uint64, _f64p, _f64p]),
     ("exageo_matern_cov", ctypes.c_int, [_C, ctypes.POINTER(Theta), ctypes.c_int64, _f64p, _f64p, ctypes.c_int64,
                                          _f64p, _f64p, _f64p, ctypes.c_int64]),
@@ -228,6 +229,7 @@ class Context:
         if st != OK:
             raise ExageoError(st, self._lib.exageo_last_error(None).decode())
         self._workspace = None
+        self.device = int(device)
 
     # -- plumbing ---------------------------------------------------------
     def close(self):
@@ -286,11 +288,28 @@ class Context:
         self._check(st, info.npd_pivot)
         return Result(info.loglik, info.logdet, info.quad, info.as_dict())
 
+    def _dev_inputs(self, *tensors):
+        """Check device inputs (contiguous float64 on this context's device, equal lengths) and
+        order the context stream after torch's current stream, which may still be writing them."""
+        import torch
+
+        n = None
+        for a in tensors:
+            if a is None:
+                continue
+            if not (a.is_cuda and a.dtype == torch.float64 and a.is_contiguous()):
+                raise ValueError("device entry points need contiguous CUDA float64 tensors")
+            if a.device.index != self.device:
+                raise ValueError(f"tensor on cuda:{a.device.index}, context on cuda:{self.device}")
+            if n is not None and a.numel() != n:
+                raise ValueError("x, y and z must have the same length")
+            n = a.numel()
+        self._check(self._lib.exageo_stream_wait(self._ctx, ctypes.c_void_p(torch.cuda.current_stream(self.device)
+                                                                             .cuda_stream)))
+
     def loglik_dev(self, x, y, z, theta) -> Result:
         """Eq. (1) with torch CUDA float64 tensors already resident on the device."""
-        for a in (x, y, z):
-            if not (a.is_cuda and str(a.dtype) == "torch.float64" and a.is_contiguous()):
-                raise ValueError("loglik_dev needs contiguous CUDA float64 tensors")
+        self._dev_inputs(x, y, z)
         t = _theta(theta)
         out = ctypes.c_double()
         info = LoglikInfo()
@@ -350,6 +369,7 @@ class Context:
 
     # -- stage-level access (tests) -------------------------------------------
     def stage_generate_dev(self, x, y, z, theta):
+        self._dev_inputs(x, y, z)
         t = _theta(theta)
         zp = ctypes.c_void_p(z.data_ptr()) if z is not None else None
         self._check(self._lib.exageo_stage_generate_dev(self._ctx, ctypes.byref(t), x.numel(),

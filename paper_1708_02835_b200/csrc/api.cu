@@ -1012,6 +1012,8 @@ exageo_status exageo_create(exageo_ctx** out, const exageo_opts* opts) {
     if ((e = cudaEventCreate(&ev)) != cudaSuccess) return bail(e, "cudaEventCreate");
   if ((e = cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming)) != cudaSuccess)
     return bail(e, "cudaEventCreate");
+  if ((e = cudaEventCreateWithFlags(&c->ev_wait, cudaEventDisableTiming)) != cudaSuccess)
+    return bail(e, "cudaEventCreate");
   c->rs.resize(c->virt ? c->world : 1);
   for (auto& R : c->rs)
     if ((e = init_rank(R)) != cudaSuccess) return bail(e, "rank state");
@@ -1069,6 +1071,7 @@ void exageo_destroy(exageo_ctx* c) {
   for (auto& ev : c->ev)
     if (ev) cudaEventDestroy(ev);
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->ev_wait) cudaEventDestroy(c->ev_wait);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }
@@ -1094,6 +1097,8 @@ size_t exageo_rank_workspace_bytes(int64_t n, int nb, int world, int grid_rows, 
 exageo_status exageo_set_workspace(exageo_ctx* c, void* ptr, size_t bytes) {
   if (!c) return EXAGEO_EINVAL;
   if (c->virt) return fail(c, EXAGEO_EINVAL, "external workspace is not supported with virtual ranks");
+  // the generator stores double2 and the DMMA kernels load 16-byte cp.async chunks
+  if ((uintptr_t)ptr % 256 != 0) return fail(c, EXAGEO_EINVAL, "workspace pointer must be 256-byte aligned");
   CUDA_TRY(c, cudaSetDevice(c->device));
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   RankState& R = c->rs[0];
@@ -1102,6 +1107,15 @@ exageo_status exageo_set_workspace(exageo_ctx* c, void* ptr, size_t bytes) {
   R.ws_bytes = ptr ? bytes : 0;
   R.ws_external = ptr != nullptr;
   c->have_matrix = false;
+  return EXAGEO_OK;
+}
+
+exageo_status exageo_stream_wait(exageo_ctx* c, void* stream) {
+  if (!c) return fail(nullptr, EXAGEO_EINVAL, "NULL ctx");
+  if ((cudaStream_t)stream == c->stream) return EXAGEO_OK;
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  CUDA_TRY(c, cudaEventRecord(c->ev_wait, (cudaStream_t)stream));
+  CUDA_TRY(c, cudaStreamWaitEvent(c->stream, c->ev_wait, 0));
   return EXAGEO_OK;
 }
 
@@ -1120,14 +1134,18 @@ exageo_status exageo_matern_cov(exageo_ctx* c, const exageo_theta* t, int64_t m,
   const size_t bytes = sizeof(double) * (2 * (size_t)m + 2 * (size_t)n + (size_t)m * (size_t)n);
   CUDA_TRY(c, cudaMalloc(&d, bytes));
   double *dx1 = d, *dy1 = d + m, *dx2 = d + 2 * m, *dy2 = d + 2 * m + n, *dC = d + 2 * m + 2 * n;
-  cudaMemcpyAsync(dx1, x1, sizeof(double) * m, cudaMemcpyHostToDevice, c->stream);
-  cudaMemcpyAsync(dy1, y1, sizeof(double) * m, cudaMemcpyHostToDevice, c->stream);
-  cudaMemcpyAsync(dx2, x2, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream);
-  cudaMemcpyAsync(dy2, y2, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream);
-  launch_matern_dense(make_consts(*t, c), m, dx1, dy1, n, dx2, dy2, dC, m, c->mtab, c->stream);
-  c->kernels += 1;
-  cudaError_t e = cudaMemcpy2DAsync(C, sizeof(double) * ldc, dC, sizeof(double) * m, sizeof(double) * m, n,
-                                    cudaMemcpyDeviceToHost, c->stream);
+  cudaError_t e = cudaMemcpyAsync(dx1, x1, sizeof(double) * m, cudaMemcpyHostToDevice, c->stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(dy1, y1, sizeof(double) * m, cudaMemcpyHostToDevice, c->stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(dx2, x2, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(dy2, y2, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream);
+  if (e == cudaSuccess) {
+    launch_matern_dense(make_consts(*t, c), m, dx1, dy1, n, dx2, dy2, dC, m, c->mtab, c->stream);
+    c->kernels += 1;
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess)
+    e = cudaMemcpy2DAsync(C, sizeof(double) * ldc, dC, sizeof(double) * m, sizeof(double) * m, n,
+                          cudaMemcpyDeviceToHost, c->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
   cudaFree(d);
   if (e != cudaSuccess) return fail(c, EXAGEO_ECUDA, std::string("matern_cov: ") + cudaGetErrorString(e));
@@ -1394,11 +1412,17 @@ exageo_status exageo_stage_finish(exageo_ctx* c, double* out3, int64_t* pivot) {
   return do_finish(c, out3, pivot);
 }
 
+static const int64_t kReadLowerMaxN = 32768;
+
 exageo_status exageo_read_lower(exageo_ctx* c, double* dst, int64_t ld) {
   if (!c) return fail(nullptr, EXAGEO_EINVAL, "NULL ctx");
   if (!c->have_matrix || !dst || ld < c->G.n) return fail(c, EXAGEO_EINVAL, "no matrix or bad ld");
-  CUDA_TRY(c, cudaSetDevice(c->device));
   const int64_t n = c->G.n;
+  // a dense n x n staging copy on the device and the host: a debugging/test entry, bounded
+  if (n > kReadLowerMaxN)
+    return fail(c, EXAGEO_EINVAL, "read_lower stages a dense n x n copy; n > " + std::to_string(kReadLowerMaxN) +
+                                      " (use exageo_read_entries)");
+  CUDA_TRY(c, cudaSetDevice(c->device));
   double* d = nullptr;
   CUDA_TRY(c, cudaMalloc(&d, sizeof(double) * (size_t)n * (size_t)n));
   cudaError_t e = cudaMemsetAsync(d, 0, sizeof(double) * (size_t)n * (size_t)n, c->stream);

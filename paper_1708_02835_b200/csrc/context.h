@@ -81,6 +81,7 @@ struct exageo_ctx {
   bool have_matrix = false;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   cudaEvent_t ev_fork = nullptr;
+  cudaEvent_t ev_wait = nullptr;  // exageo_stream_wait
   int64_t kernels = 0;
   std::string err;
   // CUDA-graph replay of a whole evaluation (exageo_opts.graphs; api.cu loglik_graph)

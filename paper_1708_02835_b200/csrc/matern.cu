@@ -7,6 +7,10 @@
 //     K_mu and K_mu+1 by Temme's power series (x <= 2) or by Steed's
 //     continued fraction CF2 (x > 2, scaled by e^x), then recur upward
 //     K_{a+1} = K_{a-1} + (2a/x) K_a, which is stable for K.
+//     Sources: N. M. Temme, "On the numerical evaluation of the modified Bessel function of
+//     the third kind", J. Comput. Phys. 19 (1975) 324-337 (series and CF2); the same
+//     algorithm as Numerical Recipes 3rd ed. Sec. 6.6 (bessik), whose variable names
+//     (gam1/gam2, p, q, delh, a1) the two routines below keep.
 // Per-theta constants (prefactor, Temme's gamma_1/gamma_2, 1/Gamma(1 +- mu))
 // are computed once on the host in long double (exageo::matern_consts).
 //

@@ -58,18 +58,23 @@ def main():
             dt = time.time() - t0
             cases.append({"theta": list(th), "loglik": ll, "logdet": ld, "quad": q, "oracle_seconds": dt})
             print(f"n={n} theta={th} l={ll!r} ({dt:.0f} s)", flush=True)
-        out = {
-            "n": n, "seed": SEED, "theta_true": list(THETA_TRUE),
-            "locations": "oracle.gen_locations(n, seed) (jittered grid, DESIGN R1-R3)",
-            "z": f"z_n{n}.npy = oracle.simulate(x, y, theta_true, synth_inputs.normals(n, seed))",
-            "simulate_seconds": t_sim, "cases": cases,
-            "oracle_threads": oracle.num_threads(), "cpu_model": cpu_model(), "host": platform.node(),
-            "source": "tools/make_golden_large.py (oracle.simulate + oracle.loglik only)",
-        }
-        path = os.path.join(ROOT, "tests", "golden", f"loglik_n{n}.json")
-        with open(path, "w") as f:
-            json.dump(out, f, indent=1)
-        print(json.dumps(out), flush=True)
+            write(n, t_sim, cases)  # after every case: a long run keeps what it finished
+
+
+def write(n, t_sim, cases):
+    out = {
+        "n": n, "seed": SEED, "theta_true": list(THETA_TRUE),
+        "locations": "oracle.gen_locations(n, seed) (jittered grid, DESIGN R1-R3)",
+        "z": f"z_n{n}.npy = oracle.simulate(x, y, theta_true, synth_inputs.normals(n, seed))",
+        "simulate_seconds": t_sim, "cases": cases,
+        "oracle_threads": oracle.num_threads(), "cpu_model": cpu_model(), "host": platform.node(),
+        "source": "tools/make_golden_large.py (oracle.simulate + oracle.loglik only)",
+    }
+    path = os.path.join(ROOT, "tests", "golden", f"loglik_n{n}.json")
+    with open(path + ".tmp", "w") as f:
+        json.dump(out, f, indent=1)
+    os.replace(path + ".tmp", path)
+    print(json.dumps(out), flush=True)
 
 
 if __name__ == "__main__":
