@@ -91,6 +91,11 @@ typedef struct {
                            Q = ranks / P. 0 or 1 = 1 x ranks (panel j on rank j % ranks); must
                            divide world (or virtual_ranks); P <= 8. NCCL row and column
                            communicators are split from the world communicator.             */
+  int tile_tasks;       /* single-rank contexts (no IND): run the factorization as ONE persistent
+                           kernel that executes the 64 x 64 tile-task DAG on the device (the
+                           paper's dynamic runtime, moved onto the GPU; dag.cu) instead
+                           of stream-launched panel kernels. 0 = automatic (n <= 4096),
+                           1 = always when eligible, -1 = never                              */
 } exageo_opts;
 
 /* Per-evaluation details of exageo_loglik*. */

@@ -35,7 +35,8 @@ class Opts(ctypes.Structure):
     _fields_ = [("device", ctypes.c_int), ("nb", ctypes.c_int), ("stream", ctypes.c_void_p),
                 ("world", ctypes.c_int), ("rank", ctypes.c_int), ("nccl_id", ctypes.c_void_p),
                 ("virtual_ranks", ctypes.c_int), ("ind_tiles", ctypes.c_int), ("distance", ctypes.c_int),
-                ("radius", ctypes.c_double), ("graphs", ctypes.c_int), ("grid_rows", ctypes.c_int)]
+                ("radius", ctypes.c_double), ("graphs", ctypes.c_int), ("grid_rows", ctypes.c_int),
+                ("tile_tasks", ctypes.c_int)]
 
 
 class MleOpts(ctypes.Structure):
@@ -210,11 +211,14 @@ class Context:
     ranks as a P x (ranks / P) process grid with tile (I, J) on rank (I mod P, J mod Q) (the
     2-D block-cyclic distribution; 0/1 = 1 x ranks); ind_tiles > 0 selects the IND
     approximation with diagonal super tiles of ind_tiles tiles; graphs selects
-    CUDA-graph replay of whole evaluations (0 automatic for n <= 32768, 1 always, -1 never)."""
+    CUDA-graph replay of whole evaluations (0 automatic for n <= 32768, 1 always, -1 never);
+    tile_tasks selects the persistent tile-task kernel for the factorization of single-rank
+    contexts (0 automatic for n <= 4096, 1 always, -1 never)."""
 
     def __init__(self, device: int = 0, nb: int = 0, stream=None, world: int = 1, rank: int = 0,
                  nccl_id: bytes | None = None, virtual_ranks: int = 0, ind_tiles: int = 0,
-                 distance: str = "euclidean", radius: float = 6371.0, graphs: int = 0, grid_rows: int = 0):
+                 distance: str = "euclidean", radius: float = 6371.0, graphs: int = 0, grid_rows: int = 0,
+                 tile_tasks: int = 0):
         self._lib = load_library()
         self._ctx = ctypes.c_void_p()
         sp = None
@@ -224,7 +228,7 @@ class Context:
         idp = ctypes.cast(self._id_buf, ctypes.c_void_p) if self._id_buf is not None else None
         metric = {"euclidean": 0, "great_circle": 1, "gcd": 1}[distance]
         o = Opts(int(device), int(nb), sp, int(world), int(rank), idp, int(virtual_ranks), int(ind_tiles), metric,
-                 float(radius), int(graphs), int(grid_rows))
+                 float(radius), int(graphs), int(grid_rows), int(tile_tasks))
         st = self._lib.exageo_create(ctypes.byref(self._ctx), ctypes.byref(o))
         if st != OK:
             raise ExageoError(st, self._lib.exageo_last_error(None).decode())

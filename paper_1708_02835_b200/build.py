@@ -22,7 +22,7 @@ CSRC = os.path.join(HERE, "csrc")
 OUT_DIR = os.path.join(HERE, "_lib")
 LIB = os.path.join(OUT_DIR, "libexageo.so")
 INCLUDE = os.path.join(ROOT, "include")
-SOURCES = ["api.cu", "matern.cu", "gemm_dmma.cu", "potrf_reduce.cu", "trsv.cu", "locations.cpp", "mle.cpp",
+SOURCES = ["api.cu", "matern.cu", "gemm_dmma.cu", "potrf_reduce.cu", "dag.cu", "trsv.cu", "locations.cpp", "mle.cpp",
            "nccl_dyn.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

@@ -258,6 +258,58 @@ exageo_status set_offsets(exageo_ctx* c, RankState& R) {
   return EXAGEO_OK;
 }
 
+// ---------------------------------------------------------------------------- tile-task executor
+// The whole factorization as one persistent kernel over the 64 x 64 tile DAG (dag.cu): used
+// where the stream schedule is bound by its critical path and launch count (small n).
+constexpr int64_t kTileTasksAutoN = 4096;
+
+bool tile_tasks_eligible(const exageo_ctx* c, int64_t n) {
+  if (c->tile_tasks < 0 || c->world > 1 || c->virt || c->ind > 0) return false;
+  return c->tile_tasks > 0 || n <= kTileTasksAutoN;
+}
+
+// Plan (host list schedule, cached by nt and the CTA count) and buffers for the current layout.
+exageo_status prepare_tile_tasks(exageo_ctx* c) {
+  const Layout& G = c->G;
+  const int nt = (int)((G.n + PB - 1) / PB);
+  int nsm = 0;
+  CUDA_TRY(c, cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device));
+  if (c->dag_nt != nt || c->dag_nproc != nsm) {
+    std::vector<int4> order;
+    dag_plan(nt, nsm, order);
+    if ((int64_t)order.size() > c->dag_cap_tasks) {
+      cudaFree(c->dag_tasks);
+      c->dag_tasks = nullptr;
+      c->dag_cap_tasks = 0;
+      CUDA_TRY(c, cudaMalloc(&c->dag_tasks, sizeof(int4) * order.size()));
+      c->dag_cap_tasks = (int64_t)order.size();
+    }
+    CUDA_TRY(c, cudaMemcpy(c->dag_tasks, order.data(), sizeof(int4) * order.size(), cudaMemcpyHostToDevice));
+    const int64_t ntr = (int64_t)order.size() + 3 * (int64_t)nt;  // + the chain CTA's records
+    if (!c->dag_trace_path.empty() && c->dag_trace_cap < ntr) {
+      cudaFree(c->dag_trace);
+      c->dag_trace = nullptr;
+      c->dag_trace_cap = 0;
+      CUDA_TRY(c, cudaMalloc(&c->dag_trace, sizeof(unsigned long long) * 4 * ntr));
+      c->dag_trace_cap = ntr;
+    }
+    c->dag_ntasks = (int)order.size();
+    c->dag_nt = nt;
+    c->dag_nproc = nsm;
+  }
+  if (c->dag_cap_nt < nt) {
+    cudaFree(c->dag_sync);
+    cudaFree(c->dag_W);
+    c->dag_sync = nullptr;
+    c->dag_W = nullptr;
+    c->dag_cap_nt = 0;
+    CUDA_TRY(c, cudaMalloc(&c->dag_sync, sizeof(int) * (size_t)dag_sync_ints(nt)));
+    CUDA_TRY(c, cudaMalloc(&c->dag_W, sizeof(double) * (size_t)nt * PB * PB));
+    c->dag_cap_nt = nt;
+  }
+  return EXAGEO_OK;
+}
+
 // ---------------------------------------------------------------------------- generation
 // Validate, set the layouts for n and make sure every buffer exists (no launches).
 exageo_status prepare_generate(exageo_ctx* c, const exageo_theta* t, int64_t n, const double* x, const double* y) {
@@ -271,7 +323,10 @@ exageo_status prepare_generate(exageo_ctx* c, const exageo_theta* t, int64_t n, 
     exageo_status st = set_offsets(c, c->rs[i]);
     if (st != EXAGEO_OK) return st;
   }
-  return ensure_buffers(c);
+  exageo_status st = ensure_buffers(c);
+  if (st != EXAGEO_OK) return st;
+  // the tile-task plan and buffers exist before any launch (and outside graph capture)
+  return tile_tasks_eligible(c, n) ? prepare_tile_tasks(c) : EXAGEO_OK;
 }
 
 exageo_status launch_generate(exageo_ctx* c, const MaternConsts& mc, const double* x, const double* y,
@@ -285,6 +340,7 @@ exageo_status launch_generate(exageo_ctx* c, const MaternConsts& mc, const doubl
     c->kernels += 1;
   }
   c->have_matrix = true;
+  c->dag_finished = false;
   return check_launch(c);
 }
 
@@ -337,6 +393,51 @@ exageo_status factor_panel(exageo_ctx* c, RankState& R, int k, cudaStream_t s) {
     c->kernels += 2;
   }
   return EXAGEO_OK;
+}
+
+// Text trace of the last executor run: one line per ticket "t type i j k cta grab ready done"
+// (times in ns from the first grab).
+void dump_tile_task_trace(exageo_ctx* c) {
+  const int ntr = c->dag_ntasks + 3 * c->dag_nt;
+  std::vector<unsigned long long> tr((size_t)4 * ntr);
+  std::vector<int4> tk(ntr);
+  if (cudaDeviceSynchronize() != cudaSuccess ||
+      cudaMemcpy(tr.data(), c->dag_trace, sizeof(unsigned long long) * tr.size(), cudaMemcpyDeviceToHost) != cudaSuccess ||
+      cudaMemcpy(tk.data(), c->dag_tasks, sizeof(int4) * c->dag_ntasks, cudaMemcpyDeviceToHost) != cudaSuccess)
+    return;
+  for (int k = 0; k < c->dag_nt; ++k) {  // chain CTA: POTRF(k), TRSM(k+1, k), SYRK(k+1, k+1, k)
+    tk[c->dag_ntasks + 3 * k] = make_int4(0, k, k, k);
+    tk[c->dag_ntasks + 3 * k + 1] = make_int4(1, k + 1, k, k);
+    tk[c->dag_ntasks + 3 * k + 2] = make_int4(2, k + 1, k + 1, k);
+  }
+  FILE* f = fopen(c->dag_trace_path.c_str(), "w");
+  if (!f) return;
+  unsigned long long t0 = ~0ull;
+  for (int t = 0; t < ntr; ++t)
+    if (tr[4 * t + 1] && tr[4 * t + 1] < t0) t0 = tr[4 * t + 1];
+  fprintf(f, "# ticket type i j k cta grab_ns ready_ns done_ns (n=%lld nt=%d)\n", (long long)c->G.n, c->dag_nt);
+  for (int t = 0; t < ntr; ++t)
+    fprintf(f, "%d %d %d %d %d %llu %lld %lld %lld\n", t, tk[t].x, tk[t].y, tk[t].z, tk[t].w, tr[4 * t],
+            (long long)(tr[4 * t + 1] - t0), (long long)(tr[4 * t + 2] - t0), (long long)(tr[4 * t + 3] - t0));
+  fclose(f);
+}
+
+exageo_status factor_tile_tasks(exageo_ctx* c) {
+  if (c->dag_nt != (int)((c->G.n + PB - 1) / PB) || c->dag_cap_nt < c->dag_nt)
+    return fail(c, EXAGEO_EINVAL, "tile-task plan missing (prepare_generate)");
+  RankState& R = c->rs[0];
+  const Layout& L = R.L;
+  CUDA_TRY(c, cudaMemsetAsync(c->dag_sync, 0, sizeof(int) * (size_t)dag_sync_ints(c->dag_nt), c->stream));
+  // log-det slots of 64-blocks beyond n (identity padding) stay zero
+  CUDA_TRY(c, cudaMemsetAsync(R.slots, 0, sizeof(double) * (size_t)L.owned() * (L.nb / PB), c->stream));
+  R.n_u2 = 0;
+  R.u2_flops = 0.0;
+  const int nctas = 1 + std::min(c->dag_nproc - 1, std::max(c->dag_ntasks, 1));  // chain CTA + pool
+  launch_dag_factor(L, R.ws, c->dag_tasks, c->dag_ntasks, c->dag_nt, c->dag_sync, c->dag_W, R.slots, R.info,
+                    c->out3, c->dag_trace, nctas, c->stream);
+  c->kernels += 1;
+  c->dag_finished = true;
+  return check_launch(c);
 }
 
 // P > 1: the other ranks of panel k's process column apply F(k)'s column operations to their
@@ -532,6 +633,8 @@ exageo_status exchange_panel(exageo_ctx* c, int j) {
 exageo_status do_factor(exageo_ctx* c) {
   if (!c->have_matrix) return fail(c, EXAGEO_EINVAL, "no generated matrix in the workspace");
   const Layout& G = c->G;
+  if (tile_tasks_eligible(c, G.n)) return factor_tile_tasks(c);
+  c->dag_finished = false;
   CUDA_TRY(c, cudaEventRecord(c->ev_fork, c->stream));
   for (auto& R : c->rs) {
     for (cudaStream_t s : {R.s_la, R.s_main, R.s_comm}) CUDA_TRY(c, cudaStreamWaitEvent(s, c->ev_fork, 0));
@@ -627,6 +730,7 @@ exageo_status first_pivot(exageo_ctx* c, int64_t* pivot) {
 
 // Launch the log-det / dot reductions and the combination into c->out3 (no host sync).
 exageo_status launch_finish(exageo_ctx* c) {
+  if (c->dag_finished) return EXAGEO_OK;  // the tile-task kernel wrote out3 itself
   for (size_t i = 0; i < c->rs.size(); ++i) {
     RankState& R = c->rs[i];
     launch_local_partials(R.L, R.ws, R.slots, R.L.owned() * (R.L.nb / PB), R.scratch, c->parts + 2 * i, c->stream);
@@ -686,7 +790,8 @@ void destroy_graph(exageo_ctx* c) {
 std::vector<const void*> graph_key(const exageo_ctx* c, const double* x, const double* y, const double* z,
                                    int kind) {
   std::vector<const void*> k = {(const void*)(intptr_t)c->G.n, (const void*)(intptr_t)c->G.nb, x, y, z,
-                                c->parts, c->out3, c->h_res, c->mtab, (const void*)(intptr_t)kind};
+                                c->parts, c->out3, c->h_res, c->mtab, (const void*)(intptr_t)kind,
+                                c->dag_tasks, c->dag_sync, c->dag_W, (const void*)(intptr_t)c->dag_ntasks};
   for (const auto& R : c->rs) {
     for (const void* p : {(const void*)R.ws, (const void*)R.slots, (const void*)R.lkk[0], (const void*)R.lkk[1],
                           (const void*)R.offs_d, (const void*)R.scratch, (const void*)R.info})
@@ -986,6 +1091,8 @@ exageo_status exageo_create(exageo_ctx** out, const exageo_opts* opts) {
   c->nb_opt = o.nb;
   c->ind = o.ind_tiles > 0 ? o.ind_tiles : 0;
   c->graphs = o.graphs > 0 ? 1 : (o.graphs < 0 ? -1 : 0);
+  c->tile_tasks = o.tile_tasks > 0 ? 1 : (o.tile_tasks < 0 ? -1 : 0);
+  if (const char* tp = getenv("EXAGEO_TILE_TASK_TRACE")) c->dag_trace_path = tp;
   c->metric = o.distance;
   c->radius = o.radius > 0 ? o.radius : 6371.0;
   c->virt = o.virtual_ranks > 1;
@@ -1001,6 +1108,7 @@ exageo_status exageo_create(exageo_ctx** out, const exageo_opts* opts) {
   if ((e = cudaSetDevice(o.device)) != cudaSuccess) return bail(e, "cudaSetDevice");
   if ((e = gemm_init()) != cudaSuccess) return bail(e, "gemm_init");
   if ((e = potrf_init()) != cudaSuccess) return bail(e, "potrf_init");
+  if ((e = dag_init()) != cudaSuccess) return bail(e, "dag_init");
   if (o.stream) {
     c->stream = (cudaStream_t)o.stream;
   } else {
@@ -1068,6 +1176,11 @@ void exageo_destroy(exageo_ctx* c) {
   cudaFree(c->pivbuf);
   cudaFree(c->vec);
   cudaFree(c->zsum);
+  if (c->dag_trace && !c->dag_trace_path.empty()) dump_tile_task_trace(c);
+  cudaFree(c->dag_tasks);
+  cudaFree(c->dag_sync);
+  cudaFree(c->dag_W);
+  cudaFree(c->dag_trace);
   for (auto& ev : c->ev)
     if (ev) cudaEventDestroy(ev);
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);

@@ -82,6 +82,21 @@ struct exageo_ctx {
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   cudaEvent_t ev_fork = nullptr;
   cudaEvent_t ev_wait = nullptr;  // exageo_stream_wait
+  // tile-task executor (dag.cu; exageo_opts.tile_tasks): the whole factorization of a
+  // single-rank context as one persistent kernel running the 64 x 64 tile DAG
+  int tile_tasks = 0;          // 0 automatic (n <= kTileTasksAutoN), 1 always when eligible, -1 never
+  int dag_nt = 0, dag_ntasks = 0, dag_nproc = 0;  // plan of the uploaded task list
+  int4* dag_tasks = nullptr;
+  int* dag_sync = nullptr;     // ticket + tile / z version counters
+  double* dag_W = nullptr;     // W_k = L_kk^{-1}, 64 x 64 per tile column
+  int dag_cap_nt = 0;          // nt the sync / W buffers are sized for
+  int64_t dag_cap_tasks = 0;
+  bool dag_finished = false;   // the last factorization ran on the executor (out3 written by it)
+  // tracing (env EXAGEO_TILE_TASK_TRACE=<file>): per ticket {cta, grabbed, ready, done} of the
+  // last evaluation, written as text when the context is destroyed
+  std::string dag_trace_path;
+  unsigned long long* dag_trace = nullptr;
+  int64_t dag_trace_cap = 0;
   int64_t kernels = 0;
   std::string err;
   // CUDA-graph replay of a whole evaluation (exageo_opts.graphs; api.cu loglik_graph)

@@ -1,0 +1,667 @@
+// dag.cu -- the tile-task executor: the whole tiled Cholesky of a single-rank context with
+// the forward solve fused (Alg. 2 l.3-4; the tile algorithm of Fig. 2)
+// as ONE persistent kernel that runs the task DAG on the device.
+//
+// The paper hands the tile tasks (POTRF / TRSM / SYRK / GEMM, Fig. 2) to a dynamic runtime
+// (StarPU through Chameleon) that starts each task once its inputs are final. At
+// small n the stream-launched schedule (api.cu do_factor) is bound by that DAG's critical
+// path plus a launch per task; here the runtime lives inside the GPU instead:
+//   * tasks on 64 x 64 tiles (64 = the K2 block): POTRF(k) (K2 body: L_kk, W_k = L_kk^{-1},
+//     sum log L_ii, pivot check), TRSM(i,k) A_ik <- A_ik W_k^T, GEMM(i,j,k) A_ij -= L_ik L_jk^T
+//     (SYRK when i == j), and the augmented z row: ZTRSM(k) y_k <- z_k W_k^T,
+//     ZGEMM(j,k) z_j -= y_k L_jk^T -- the same operations as the stream path;
+//   * one CTA per SM loops: take the next task from a global ticket counter, wait until its
+//     inputs are final (per-tile version counters in global memory, acquire loads), run it
+//     with all 256 threads, publish (fence + release store);
+//   * the ticket order is a list schedule computed on the host (dag_plan): the tasks sorted
+//     by their start time in a simulated greedy schedule on the SM count with the bottom
+//     level (longest path to the end) as priority, so the critical chain
+//     POTRF(k) -> TRSM(k+1,k) -> SYRK(k+1,k+1,k) -> POTRF(k+1) is taken as soon as it can run.
+//     Start times respect every dependency, so the order is topological: a task's inputs are
+//     always held by CTAs already running (no deadlock for any grid size).
+// Every tile version counter st(i,j) counts the operations applied to tile (i, j) in the
+// fixed order k = 0, 1, ...; updates are never reordered, so results are deterministic.
+// The data stays in the standard panel layout (internal.h), so predict, simulate and the
+// read-back entries work on the result unchanged. Tile rows at or beyond n (pure identity
+// padding, zero left of the diagonal) are never touched, as in the stream path.
+#include <algorithm>
+#include <cstring>
+#include <queue>
+#include <vector>
+
+#include "internal.h"
+
+namespace exageo {
+
+namespace {
+
+#include "potrf64.cuh"
+
+constexpr int LDS = PB + 4;  // shared leading dimension of staged tiles (4 mod 16 doubles)
+constexpr int kTileSmem = 2 * PB * LDS;
+constexpr int kDagSmemDoubles = kPotrfSmemDoubles + 2 * PB * LDS;  // K2 region + X, Y (chain CTA)
+static_assert(kPotrfSmemDoubles >= kTileSmem, "pool tiles fit in the K2 region");
+constexpr int kSyncHead = 32;  // ints before the tile counters (the ticket is sync[0])
+constexpr int kPad = 32;       // one 128-byte line per version counter (pollers of different
+                               // tiles never share a line with each other or the ticket)
+
+enum TaskType : int { kPotrf = 0, kTrsm = 1, kGemm = 2, kZTrsm = 3, kZGemm = 4 };
+
+struct DagArgs {
+  Layout L;
+  double* ws;
+  const int4* tasks;  // {type, i, j, k} in ticket order
+  int ntasks;
+  int nt;             // tile columns inside n: ceil(n / 64)
+  int* sync;          // [0] ticket; [kSyncHead ..] st(i, j) at i * nt + j; then z(j)
+  double* W;          // nt blocks of 64 x 64: W_k = L_kk^{-1}
+  double* slots;      // log-det partials, one per 64-block column (panel p, sub-block sb)
+  int* info;
+  double* out3;   // {loglik, logdet, quad}, written by the last CTA to leave (Alg. 2 l.5-7)
+  int64_t n;
+  unsigned long long* trace;  // optional: per ticket {cta, grabbed, inputs ready, done} (ns)
+};
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void cp_async16(double* s, const double* g) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(s);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+// Tile (i, j) (64-row / 64-column units) of the single-rank panel layout and its ld.
+__device__ __forceinline__ double* tile_ptr(const DagArgs& a, int i, int j, int64_t& ld) {
+  const int nsub = a.L.nb / PB, p = j / nsub, cb = (j % nsub) * PB;
+  ld = a.L.ld(p);
+  return a.ws + a.L.off(p) + (int64_t)cb * ld + ((int64_t)i * PB - (int64_t)p * a.L.nb);
+}
+// z row segment of column block j (entry t at ptr[t * ld]).
+__device__ __forceinline__ double* zseg_ptr(const DagArgs& a, int j, int64_t& ld) {
+  const int nsub = a.L.nb / PB, p = j / nsub, cb = (j % nsub) * PB;
+  ld = a.L.ld(p);
+  return a.ws + a.L.off(p) + (int64_t)cb * ld + a.L.lrows(p);
+}
+
+// ---- 64 x 64 x 64 DMMA tile products on 256 threads -----------------------------------------
+// Warp w owns rows r0 = 32 (w & 1) .. +31 and columns c0 = 16 (w >> 1) .. +15 of the result as
+// 4 x 2 m8n8k4 fragments; operands in shared memory, column-major with ld LDS.
+struct Frag {
+  double v[4][2][2];
+};
+__device__ __forceinline__ int frag_r0() { return 32 * ((threadIdx.x >> 5) & 1); }
+__device__ __forceinline__ int frag_c0() { return 16 * (threadIdx.x >> 6); }
+
+// dst (shared, ld LDS) <- 64 x 64 tile at src (global, ld) by cp.async (L2 only); committed
+// as one group, not waited for.
+__device__ __forceinline__ void stage_tile(double* dst, const double* src, int64_t ld) {
+  const int tid = threadIdx.x;
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    const int idx = tid + 256 * u, r2 = idx & 31, c = idx >> 5;
+    cp_async16(dst + c * LDS + 2 * r2, src + (int64_t)c * ld + 2 * r2);
+  }
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+__device__ __forceinline__ void frag_load(Frag& f, const double* C, int64_t ldc) {
+  const int lane = threadIdx.x & 31, fr = lane >> 2, fk = lane & 3, r0 = frag_r0(), c0 = frag_c0();
+#pragma unroll
+  for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) f.v[mt][nt][e] = __ldcg(C + (int64_t)(c0 + 8 * nt + 2 * fk + e) * ldc + r0 + 8 * mt + fr);
+}
+__device__ __forceinline__ void frag_load_s(Frag& f, const double* Cs) {  // from shared, ld LDS
+  const int lane = threadIdx.x & 31, fr = lane >> 2, fk = lane & 3, r0 = frag_r0(), c0 = frag_c0();
+#pragma unroll
+  for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) f.v[mt][nt][e] = Cs[(c0 + 8 * nt + 2 * fk + e) * LDS + r0 + 8 * mt + fr];
+}
+__device__ __forceinline__ void frag_zero(Frag& f) {
+#pragma unroll
+  for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) f.v[mt][nt][0] = f.v[mt][nt][1] = 0.0;
+}
+// C (global or shared) <- f; skip_upper: leave warp tiles strictly above the diagonal alone
+__device__ __forceinline__ void frag_store(const Frag& f, double* C, int64_t ldc) {
+  const int lane = threadIdx.x & 31, fr = lane >> 2, fk = lane & 3, r0 = frag_r0(), c0 = frag_c0();
+#pragma unroll
+  for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) C[(int64_t)(c0 + 8 * nt + 2 * fk + e) * ldc + r0 + 8 * mt + fr] = f.v[mt][nt][e];
+}
+// f += sgn * A[:, 0:kend] B[:, 0:kend]^T (A, B shared, ld LDS)
+__device__ __forceinline__ void frag_mma(Frag& f, const double* As, const double* Bs, double sgn, int kend) {
+  const int lane = threadIdx.x & 31, fr = lane >> 2, fk = lane & 3, r0 = frag_r0(), c0 = frag_c0();
+#pragma unroll 4
+  for (int kk = 0; kk < kend; kk += 4) {
+    const double* as = As + (kk + fk) * LDS + r0 + fr;
+    const double* bs = Bs + (kk + fk) * LDS + c0 + fr;
+    double af[4], bf[2];
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt) af[mt] = sgn * as[8 * mt];
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) bf[nt] = bs[8 * nt];
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) dmma64(f.v[mt][nt], af[mt], bf[nt]);
+  }
+}
+// warp tile strictly above the diagonal of a diagonal tile (never read: K2 reads the lower
+// triangle and the diagonal 16 x 16 blocks only)
+__device__ __forceinline__ bool frag_upper() { return frag_r0() + 32 <= frag_c0(); }
+
+// TRSM by the inverse, in place: A (global, ld) <- A W^T, W lower triangular in shared
+// memory (ld LDS): result column c only needs t <= c. Leaves the result in X too (shared).
+__device__ __forceinline__ void tile_trsm(double* A, int64_t ld, const double* Ws, double* X) {
+  stage_tile(X, A, ld);
+  Frag f;
+  frag_zero(f);
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+  __syncthreads();
+  frag_mma(f, X, Ws, 1.0, frag_c0() + 16);
+  __syncthreads();  // every warp has read X
+  frag_store(f, A, ld);
+  frag_store(f, X, LDS);
+}
+// C (global, ld) -= A B^T with A, B in shared memory; diagonal tile (A == B): skip the warp
+// tiles above the diagonal.
+__device__ __forceinline__ void tile_update(double* C, int64_t ldc, const double* As, const double* Bs, bool diag) {
+  if (diag && frag_upper()) return;
+  Frag f;
+  frag_load(f, C, ldc);
+  frag_mma(f, As, Bs, -1.0, PB);
+  frag_store(f, C, ldc);
+}
+
+// y_k <- z_k W_k^T: y_c = sum_{t <= c} z_t W_ct (W lower triangular); 256 threads, four per
+// column c over interleaved t, combined in a fixed order.
+__device__ __forceinline__ void z_trsm(double* zp, int64_t ldz, const double* Wk, double* sm) {
+  const int tid = threadIdx.x, c = tid & 63, part = tid >> 6;
+  if (tid < PB) sm[tid] = __ldcg(zp + (int64_t)tid * ldz);
+  __syncthreads();
+  double acc = 0.0;
+  for (int t = part; t <= c; t += 4) acc = fma(sm[t], __ldcg(Wk + t * PB + c), acc);
+  sm[PB + part * PB + c] = acc;
+  __syncthreads();
+  if (tid < PB) zp[(int64_t)tid * ldz] = (sm[PB + tid] + sm[2 * PB + tid]) + (sm[3 * PB + tid] + sm[4 * PB + tid]);
+}
+
+// z_j -= y_k L_jk^T: z_j[c] -= sum_t y_t L_jk(c, t).
+__device__ __forceinline__ void z_gemm(double* zj, int64_t ldzj, const double* yk, int64_t ldyk, const double* Ljk,
+                                       int64_t ld, double* sm) {
+  const int tid = threadIdx.x, c = tid & 63, part = tid >> 6;
+  if (tid < PB) sm[tid] = __ldcg(yk + (int64_t)tid * ldyk);
+  __syncthreads();
+  double acc = 0.0;
+#pragma unroll 4
+  for (int t = 16 * part; t < 16 * part + 16; ++t) acc = fma(sm[t], __ldcg(Ljk + (int64_t)t * ld + c), acc);
+  sm[PB + part * PB + c] = acc;
+  __syncthreads();
+  if (tid < PB) {
+    const double s = (sm[PB + tid] + sm[2 * PB + tid]) + (sm[3 * PB + tid] + sm[4 * PB + tid]);
+    zj[(int64_t)tid * ldzj] = __ldcg(zj + (int64_t)tid * ldzj) - s;
+  }
+}
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// thread 0: wait until *f >= v (relaxed polls with a short back-off, then an acquire fence);
+// false if a pivot failed meanwhile (info set)
+__device__ __forceinline__ bool wait_ge(const int* f, int v, const int* info) {
+  if (*(volatile const int*)f < v) {
+    int spins = 0;
+    while (*(volatile const int*)f < v) {
+      if (*(volatile const int*)info != 0) return false;
+      if (++spins > 4) __nanosleep(40);
+    }
+  }
+  __threadfence();
+  return true;
+}
+
+// Warp-level stage of a 64 x 64 tile (one warp issues all 512 16-byte copies; committed).
+__device__ __forceinline__ void stage_tile_warp(double* dst, const double* src, int64_t ld) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll 4
+  for (int u = 0; u < 64; ++u) {
+    const int idx = lane + 32 * u, r2 = idx & 31, c = idx >> 5;
+    cp_async16(dst + c * LDS + 2 * r2, src + (int64_t)c * ld + 2 * r2);
+  }
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+
+// Prefetch hook of the chain CTA (runs on warp 7 inside POTRF(k), potrf64_body): polls the
+// version counters of A_{k+1,k} and A_{k+1,k+1} without blocking -- the counter values
+// loaded at strip K are looked at in strip K + 1 -- and issues the cp.async of each tile
+// into X / Y once the pool has finished it. Bits of *issued: 1 X, 2 Y.
+struct ChainPrefetch {
+  const int* f1;
+  const int* f2;
+  int need;
+  double* X;
+  const double* A1;
+  int64_t ld1;
+  double* Y;
+  const double* A2;
+  int64_t ld2;
+  int* issued;  // shared: written at K = 4 for the rest of the CTA
+  int* st;      // registers of warp 7: {issued bits, counter 1, counter 2} (lane 0 loads)
+  __device__ __forceinline__ void operator()(int K) const {
+    const int lane = threadIdx.x & 31;
+    int done = st[0];
+    if (K > 0 && done != 3) {
+      const int c1 = __shfl_sync(0xffffffffu, st[1], 0), c2 = __shfl_sync(0xffffffffu, st[2], 0);
+      if (!(done & 1) && c1 >= need) {
+        stage_tile_warp(X, A1, ld1);
+        done |= 1;
+      }
+      if (!(done & 2) && c2 >= need) {
+        stage_tile_warp(Y, A2, ld2);
+        done |= 2;
+      }
+      st[0] = done;
+    }
+    if (K < 4 && done != 3 && lane == 0) {  // loads for the next look (in flight until then)
+      st[1] = *(volatile const int*)f1;
+      st[2] = *(volatile const int*)f2;
+    }
+    if (K == 4 && lane == 0) *issued = done;
+  }
+};
+
+// The critical chain on CTA 0: for k = 0, 1, ...: POTRF(k) (K2 body: L_kk, W_k and the pivots
+// stay in shared memory), TRSM(k+1, k) with W_k from shared memory, SYRK(k+1, k+1, k) with
+// L_{k+1,k} from shared memory, its result written straight into the K2 body's input block:
+// POTRF(k+1) starts from shared memory. The two tiles a step reads from the pool (A_{k+1,k},
+// A_{k+1,k+1}) are prefetched by cp.async while POTRF(k) runs (ChainPrefetch). Results the
+// pool needs (L_kk / W_k, L_{k+1,k}) are published by a warp with little work in the phase
+// that follows, so the release fence stays off the chain; the SYRK result is consumed by
+// this CTA only (POTRF(k+1) publishes the tile's next version).
+// Trace records (optional): ntasks + 3k + {0, 1, 2} for POTRF / TRSM / SYRK of step k.
+__device__ void chain_cta(const DagArgs& a, int* st, double* sm) {
+  __shared__ int s_ok, s_issued;
+  double* X = sm + kPotrfSmemDoubles;  // A_{k+1,k}, then L_{k+1,k}
+  double* Y = X + PB * LDS;            // A_{k+1,k+1}
+  const double* Ws = sm + PB * LDA2;   // K2 body's W = L_kk^{-1} (ld LDA2 = LDS)
+  const int nsub = a.L.nb / PB;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  auto stf = [&](int i, int j) { return st + (i * a.nt + j) * kPad; };
+  auto release_by = [&](int w, int* f, int v) {  // after a barrier: one lane of warp w publishes
+    if (warp == w && lane == 0) {
+      __threadfence();
+      st_release(f, v);
+    }
+  };
+  auto rec = [&](int slot, unsigned long long t0, unsigned long long t1) {
+    if (a.trace && threadIdx.x == 0) {
+      unsigned long long* r = a.trace + 4 * (a.ntasks + slot);
+      r[0] = blockIdx.x;
+      r[1] = t0;
+      r[2] = t1;
+      r[3] = gtimer();
+    }
+  };
+  for (int k = 0; k < a.nt; ++k) {
+    const bool last = k + 1 == a.nt;
+    int64_t ld, ldb = 0, ldd = 0;
+    double* Akk = tile_ptr(a, k, k, ld);
+    double* Ab = last ? nullptr : tile_ptr(a, k + 1, k, ldb);
+    double* Ad = last ? nullptr : tile_ptr(a, k + 1, k + 1, ldd);
+    if (threadIdx.x == 0) s_issued = last ? 3 : 0;
+    __syncthreads();
+    const unsigned long long t0 = a.trace ? gtimer() : 0;
+    // POTRF(k): st(k, k) == k already (the pool's updates were waited for before SYRK(k, k, k-1))
+    int hst[3] = {last ? 3 : 0, 0, 0};
+    ChainPrefetch hook{last ? nullptr : stf(k + 1, k), last ? nullptr : stf(k + 1, k + 1), k, X, Ab, ldb, Y, Ad, ldd,
+                       &s_issued, hst};
+    double* Wk = a.W + (size_t)k * PB * PB;
+    double* slot = a.slots + (k / nsub) * nsub + k % nsub;
+    const bool ok = k == 0 ? potrf64_body<false>(Akk, ld, Wk, slot, a.info, (int64_t)k * PB, sm, hook)
+                           : potrf64_body<true>(Akk, ld, Wk, slot, a.info, (int64_t)k * PB, sm, hook);
+    if (!ok) {
+      asm volatile("cp.async.wait_all;\n" ::: "memory");
+      return;
+    }
+    release_by(0, stf(k, k), k + 1);  // body ended with a barrier: L_kk, W_k stored
+    rec(3 * k, t0, t0);
+    if (last) break;
+    // TRSM(k+1, k): L_{k+1,k} = A_{k+1,k} W_k^T
+    const unsigned long long t2 = a.trace ? gtimer() : 0;
+    const int issued = s_issued;
+    if (warp == 7) asm volatile("cp.async.wait_all;\n" ::: "memory");
+    if (!(issued & 1)) {
+      if (threadIdx.x == 0) s_ok = wait_ge(stf(k + 1, k), k, a.info);
+      __syncthreads();
+      if (!s_ok) return;
+      stage_tile(X, Ab, ldb);
+      asm volatile("cp.async.wait_all;\n" ::: "memory");
+    }
+    __syncthreads();
+    const unsigned long long t3 = a.trace ? gtimer() : 0;
+    Frag f;
+    frag_zero(f);
+    frag_mma(f, X, Ws, 1.0, frag_c0() + 16);
+    __syncthreads();  // every warp has read X
+    frag_store(f, Ab, ldb);
+    frag_store(f, X, LDS);
+    __syncthreads();
+    release_by(4, stf(k + 1, k), k + 1);  // warp 4 has no SYRK block
+    rec(3 * k + 1, t2, t3);
+    // SYRK(k+1, k+1, k): A_{k+1,k+1} -= L_{k+1,k} L_{k+1,k}^T into the body's input block As
+    const unsigned long long t4 = a.trace ? gtimer() : 0;
+    if (!(issued & 2)) {
+      if (threadIdx.x == 0) s_ok = wait_ge(stf(k + 1, k + 1), k, a.info);
+      __syncthreads();
+      if (!s_ok) return;
+      stage_tile(Y, Ad, ldd);
+      asm volatile("cp.async.wait_all;\n" ::: "memory");
+      __syncthreads();
+    }
+    const unsigned long long t5 = a.trace ? gtimer() : 0;
+    if (!frag_upper()) {
+      frag_load_s(f, Y);
+      frag_mma(f, X, X, -1.0, PB);
+      frag_store(f, sm, LDA2);
+    }
+    __syncthreads();
+    rec(3 * k + 2, t4, t5);
+  }
+}
+
+// Alg. 2 l.5-7 by the last CTA to leave the kernel (a counter of finished CTAs): logdet =
+// 2 sum of the 64-block partials, quad = sum over c < n of y_c^2 from the z row, and
+// l = -quad/2 - logdet/2 - (n/2) log 2 pi, each sum in a fixed order (deterministic).
+__device__ void finish_tail(const DagArgs& a, double* red) {
+  __shared__ int s_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = atomicAdd(a.sync + 16, 1) == (int)gridDim.x - 1;
+    if (s_last) __threadfence();
+  }
+  __syncthreads();
+  if (!s_last) return;
+  const int tid = threadIdx.x, nsub = a.L.nb / PB;
+  const int nslots = a.L.owned() * nsub;
+  double s1 = 0.0, s2 = 0.0;
+  for (int i = tid; i < nslots; i += 256) s1 += __ldcg(a.slots + i);
+  for (int64_t c = tid; c < a.n; c += 256) {
+    const int p = (int)(c / a.L.nb);
+    const double y = __ldcg(a.ws + a.L.off(p) + (c - (int64_t)p * a.L.nb) * a.L.ld(p) + a.L.lrows(p));
+    s2 += y * y;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    s1 += __shfl_down_sync(0xffffffffu, s1, o);
+    s2 += __shfl_down_sync(0xffffffffu, s2, o);
+  }
+  if ((tid & 31) == 0) {
+    red[tid >> 5] = s1;
+    red[8 + (tid >> 5)] = s2;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double ld2 = 0.0, q = 0.0;
+    for (int w = 0; w < 8; ++w) {
+      ld2 += red[w];
+      q += red[8 + w];
+    }
+    const double logdet = 2.0 * ld2;
+    a.out3[0] = -0.5 * q - 0.5 * logdet - 0.5 * (double)a.n * 1.8378770664093454835606594728112;
+    a.out3[1] = logdet;
+    a.out3[2] = q;
+  }
+}
+
+__device__ void pool_cta(const DagArgs& a, int* st, int* zs, double* sm);
+
+__global__ void __launch_bounds__(256, 1) dag_factor_kernel(DagArgs a) {
+  extern __shared__ double sm[];
+  int* st = a.sync + kSyncHead;  // st(i, j) = operations applied to tile (i, j), at (i nt + j) kPad
+  int* zs = st + a.nt * a.nt * kPad;  // z(j) = operations applied to z segment j, at j kPad
+  if (blockIdx.x == 0) chain_cta(a, st, sm);
+  else pool_cta(a, st, zs, sm);
+  finish_tail(a, sm);
+}
+
+// Pool CTAs: tickets in list-schedule order (dag_plan).
+__device__ void pool_cta(const DagArgs& a, int* st, int* zs, double* sm) {
+  __shared__ int s_task, s_ok;
+  unsigned long long t_grab = 0;
+  double* As = sm;
+  double* Bs = sm + PB * LDS;
+  for (;;) {
+    if (threadIdx.x == 0) {
+      s_task = atomicAdd(a.sync, 1);
+      if (a.trace) t_grab = gtimer();
+    }
+    __syncthreads();
+    const int t = s_task;
+    if (t >= a.ntasks) return;
+    const int4 tk = a.tasks[t];
+    const int type = tk.x, i = tk.y, j = tk.z, k = tk.w;
+    if (threadIdx.x == 0) {
+      bool ok = true;
+      switch (type) {
+        case kTrsm: ok = wait_ge(st + (k * a.nt + k) * kPad, k + 1, a.info) && wait_ge(st + (i * a.nt + k) * kPad, k, a.info); break;
+        case kGemm:
+          ok = wait_ge(st + (i * a.nt + k) * kPad, k + 1, a.info) && wait_ge(st + (j * a.nt + k) * kPad, k + 1, a.info) &&
+               wait_ge(st + (i * a.nt + j) * kPad, k, a.info);
+          break;
+        case kZTrsm: ok = wait_ge(st + (k * a.nt + k) * kPad, k + 1, a.info) && wait_ge(zs + k * kPad, k, a.info); break;
+        default:
+          ok = wait_ge(zs + k * kPad, k + 1, a.info) && wait_ge(st + (j * a.nt + k) * kPad, k + 1, a.info) &&
+               wait_ge(zs + j * kPad, k, a.info);
+          break;
+      }
+      s_ok = ok;
+      if (a.trace) {
+        a.trace[4 * t] = blockIdx.x;
+        a.trace[4 * t + 1] = t_grab;
+        a.trace[4 * t + 2] = gtimer();
+      }
+    }
+    __syncthreads();
+    if (!s_ok) return;  // a pivot failed: ENOTPD, nothing later matters
+    int* flag;
+    int64_t ld, ld2;
+    switch (type) {
+      case kTrsm: {
+        double* Aik = tile_ptr(a, i, k, ld);
+        stage_tile(Bs, a.W + (size_t)k * PB * PB, PB);
+        tile_trsm(Aik, ld, Bs, As);
+        flag = st + (i * a.nt + k) * kPad;
+        break;
+      }
+      case kGemm: {
+        int64_t ldi, ldj;
+        double* Aij = tile_ptr(a, i, j, ld);
+        stage_tile(As, tile_ptr(a, i, k, ldi), ldi);
+        if (i != j) stage_tile(Bs, tile_ptr(a, j, k, ldj), ldj);
+        asm volatile("cp.async.wait_all;\n" ::: "memory");
+        __syncthreads();
+        tile_update(Aij, ld, As, i != j ? Bs : As, i == j);
+        flag = st + (i * a.nt + j) * kPad;
+        break;
+      }
+      case kZTrsm: {
+        double* zk = zseg_ptr(a, k, ld);
+        z_trsm(zk, ld, a.W + (size_t)k * PB * PB, sm);
+        flag = zs + k * kPad;
+        break;
+      }
+      default: {
+        double* zj = zseg_ptr(a, j, ld);
+        const double* yk = zseg_ptr(a, k, ld2);
+        int64_t ldl;
+        const double* Ljk = tile_ptr(a, j, k, ldl);
+        z_gemm(zj, ld, yk, ld2, Ljk, ldl, sm);
+        flag = zs + j * kPad;
+        break;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      st_release(flag, k + 1);
+      if (a.trace) a.trace[4 * t + 3] = gtimer();
+    }
+  }
+}
+
+}  // namespace
+
+// ---- host: the list schedule ------------------------------------------------------------
+// Tasks of the tile DAG for nt tile columns. The critical chain POTRF(k), TRSM(k+1, k),
+// SYRK(k+1, k+1, k) runs on CTA 0 (chain_cta); every other task goes to the ticket list,
+// ordered by its start time in a simulated greedy list schedule on the other nproc - 1 CTAs
+// (priority: bottom level = cost of the longest path to the end; the chain tasks run on
+// their own processor in the simulation). Costs are rough measured durations in
+// microseconds (K2 ~13, a 64^3 DMMA tile ~3-5, a z-row task ~3); only proportions matter.
+void dag_plan(int nt, int nproc, std::vector<int4>& order) {
+  std::vector<int4> tk;
+  std::vector<float> cost;
+  std::vector<char> chain;
+  std::vector<std::vector<int>> deps;
+  std::vector<int> potrf(nt), ztrsm(nt), trsm((size_t)nt * nt, -1), zgemm((size_t)nt * nt, -1);
+  std::vector<int> gemm_prev((size_t)nt * nt, -1);  // last GEMM applied to tile (i, j) so far
+  auto add = [&](int type, int i, int j, int k, float c, bool ch, std::vector<int> d) {
+    tk.push_back(make_int4(type, i, j, k));
+    cost.push_back(c);
+    chain.push_back(ch);
+    d.erase(std::remove(d.begin(), d.end(), -1), d.end());
+    deps.push_back(std::move(d));
+    return (int)tk.size() - 1;
+  };
+  for (int k = 0; k < nt; ++k) {
+    potrf[k] = add(kPotrf, k, k, k, 13.f, true, {gemm_prev[(size_t)k * nt + k]});
+    for (int i = k + 1; i < nt; ++i)
+      trsm[(size_t)i * nt + k] = add(kTrsm, i, k, k, i == k + 1 ? 2.f : 4.f, i == k + 1,
+                                     {potrf[k], gemm_prev[(size_t)i * nt + k]});
+    ztrsm[k] = add(kZTrsm, nt, k, k, 3.f, false, {potrf[k], k > 0 ? zgemm[(size_t)k * nt + k - 1] : -1});
+    for (int j = k + 1; j < nt; ++j)
+      for (int i = j; i < nt; ++i) {
+        const size_t ij = (size_t)i * nt + j;
+        const bool ch = i == k + 1 && j == k + 1;
+        gemm_prev[ij] = add(kGemm, i, j, k, ch ? 2.5f : 5.f, ch,
+                            {trsm[(size_t)i * nt + k], i != j ? trsm[(size_t)j * nt + k] : -1, gemm_prev[ij]});
+      }
+    for (int j = k + 1; j < nt; ++j)
+      zgemm[(size_t)j * nt + k] = add(kZGemm, nt, j, k, 3.f, false,
+                                      {ztrsm[k], trsm[(size_t)j * nt + k], k > 0 ? zgemm[(size_t)j * nt + k - 1] : -1});
+  }
+  const int N = (int)tk.size();
+  std::vector<std::vector<int>> succ(N);
+  std::vector<int> pending(N);
+  for (int t = 0; t < N; ++t) {
+    pending[t] = (int)deps[t].size();
+    for (int d : deps[t]) succ[d].push_back(t);
+  }
+  std::vector<float> bl(N);  // ids are in topological order (every dependency has a smaller id)
+  for (int t = N - 1; t >= 0; --t) {
+    float m = 0.f;
+    for (int s2 : succ[t]) m = std::max(m, bl[s2]);
+    bl[t] = cost[t] + m;
+  }
+  auto lower = [&](int x, int y) { return bl[x] < bl[y] || (bl[x] == bl[y] && x > y); };
+  std::priority_queue<int, std::vector<int>, decltype(lower)> ready(lower);
+  std::priority_queue<int, std::vector<int>, std::greater<int>> chain_ready;  // chain order = id order
+  using Ev = std::pair<float, int>;
+  std::priority_queue<Ev, std::vector<Ev>, std::greater<Ev>> running;
+  auto make_ready = [&](int t) {
+    if (chain[t]) chain_ready.push(t);
+    else ready.push(t);
+  };
+  for (int t = 0; t < N; ++t)
+    if (pending[t] == 0) make_ready(t);
+  order.clear();
+  int free_pool = nproc > 1 ? nproc - 1 : 1;
+  bool chain_busy = false;
+  float now = 0.f;
+  int done = 0;
+  while (done < N) {
+    if (!chain_busy && !chain_ready.empty()) {
+      const int t = chain_ready.top();
+      chain_ready.pop();
+      running.push({now + cost[t], t});
+      chain_busy = true;
+    }
+    while (free_pool > 0 && !ready.empty()) {
+      const int t = ready.top();
+      ready.pop();
+      order.push_back(tk[t]);
+      running.push({now + cost[t], t});
+      --free_pool;
+    }
+    if (running.empty()) break;  // cannot happen: the DAG is acyclic
+    now = running.top().first;
+    while (!running.empty() && running.top().first <= now) {
+      const int t = running.top().second;
+      running.pop();
+      ++done;
+      if (chain[t]) chain_busy = false;
+      else ++free_pool;
+      for (int s2 : succ[t])
+        if (--pending[s2] == 0) make_ready(s2);
+    }
+  }
+}
+
+int dag_sync_ints(int nt) { return kSyncHead + (nt * nt + nt) * kPad; }
+
+cudaError_t dag_init() {
+  return cudaFuncSetAttribute(dag_factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              kDagSmemDoubles * (int)sizeof(double));
+}
+
+void launch_dag_factor(const Layout& L, double* ws, const int4* tasks, int ntasks, int nt, int* sync, double* W,
+                       double* slots, int* info, double* out3, unsigned long long* trace, int nctas,
+                       cudaStream_t s) {
+  DagArgs a;
+  a.L = L;
+  a.ws = ws;
+  a.tasks = tasks;
+  a.ntasks = ntasks;
+  a.nt = nt;
+  a.sync = sync;
+  a.W = W;
+  a.slots = slots;
+  a.info = info;
+  a.out3 = out3;
+  a.n = L.n;
+  a.trace = trace;
+  // cooperative: every CTA is co-resident (the chain CTA and the pool wait on each other)
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(nctas);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = kDagSmemDoubles * sizeof(double);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, dag_factor_kernel, a);
+}
+
+const void* dag_factor_kernel_fn() { return (const void*)dag_factor_kernel; }
+
+}  // namespace exageo

@@ -23,6 +23,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include <vector>
+
 namespace exageo {
 
 constexpr int ZR = 128;  // height of the z row block appended to every panel
@@ -169,6 +171,19 @@ void launch_syrk_panels(const Layout& L, double* ws, const double* Pk, int k, in
 // leading dimension slds[pp]: the local panel k of rank (pp, k mod Q)), gemm_dmma.cuh Syrk2DMap.
 void launch_syrk_panels_2d(const Layout& L, double* ws, const double* const* slices, const int64_t* slds, int k,
                            int J0, int npan, const int* info, cudaStream_t s);
+// Tile-task executor (dag.cu): the factorization (with the fused forward solve) of a
+// single-rank layout as one persistent kernel over the 64 x 64 tile DAG. dag_plan lists the
+// tasks of nt = ceil(n / 64) tile columns in ticket order for nproc CTAs; sync holds
+// dag_sync_ints(nt) ints, zeroed before each launch; W holds nt 64 x 64 blocks. The last CTA to
+// finish writes out3 = {loglik, logdet, quad} (so no separate reduction kernels follow).
+void dag_plan(int nt, int nproc, std::vector<int4>& order);
+int dag_sync_ints(int nt);
+cudaError_t dag_init();
+void launch_dag_factor(const Layout& L, double* ws, const int4* tasks, int ntasks, int nt, int* sync, double* W,
+                       double* slots, int* info, double* out3, unsigned long long* trace, int nctas,
+                       cudaStream_t s);
+const void* dag_factor_kernel_fn();
+
 // Factor the PB x PB diagonal block at `a` (ld) in place, write W = L^{-1} (PB x PB,
 // ld PB) and slot = sum log L_ii; info = first bad global pivot + 1.
 void launch_potrf_block(double* a, int64_t lda, double* W, double* logdet_slot, int* info, int64_t pivot_base,
