@@ -94,7 +94,7 @@ typedef struct {
   int tile_tasks;       /* single-rank contexts (no IND): run the factorization as ONE persistent
                            kernel that executes the 64 x 64 tile-task DAG on the device (the
                            paper's dynamic runtime, moved onto the GPU; dag.cu) instead
-                           of stream-launched panel kernels. 0 = automatic (n <= 4096),
+                           of stream-launched panel kernels. 0 = automatic (n <= 3200),
                            1 = always when eligible, -1 = never                              */
 } exageo_opts;
 

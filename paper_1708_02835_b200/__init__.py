@@ -213,7 +213,7 @@ class Context:
     approximation with diagonal super tiles of ind_tiles tiles; graphs selects
     CUDA-graph replay of whole evaluations (0 automatic for n <= 32768, 1 always, -1 never);
     tile_tasks selects the persistent tile-task kernel for the factorization of single-rank
-    contexts (0 automatic for n <= 4096, 1 always, -1 never)."""
+    contexts (0 automatic for n <= 3200, 1 always, -1 never)."""
 
     def __init__(self, device: int = 0, nb: int = 0, stream=None, world: int = 1, rank: int = 0,
                  nccl_id: bytes | None = None, virtual_ranks: int = 0, ind_tiles: int = 0,

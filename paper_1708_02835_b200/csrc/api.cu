@@ -261,10 +261,10 @@ exageo_status set_offsets(exageo_ctx* c, RankState& R) {
 // ---------------------------------------------------------------------------- tile-task executor
 // The whole factorization as one persistent kernel over the 64 x 64 tile DAG (dag.cu): used
 // where the stream schedule is bound by its critical path and launch count (small n).
-constexpr int64_t kTileTasksAutoN = 4096;
+constexpr int64_t kTileTasksAutoN = 3200;
 
 bool tile_tasks_eligible(const exageo_ctx* c, int64_t n) {
-  if (c->tile_tasks < 0 || c->world > 1 || c->virt || c->ind > 0) return false;
+  if (c->tile_tasks < 0 || c->world > 1 || c->virt || c->ind > 0 || c->comm) return false;
   return c->tile_tasks > 0 || n <= kTileTasksAutoN;
 }
 
@@ -304,6 +304,7 @@ exageo_status prepare_tile_tasks(exageo_ctx* c) {
     c->dag_W = nullptr;
     c->dag_cap_nt = 0;
     CUDA_TRY(c, cudaMalloc(&c->dag_sync, sizeof(int) * (size_t)dag_sync_ints(nt)));
+    CUDA_TRY(c, cudaMemset(c->dag_sync, 0, sizeof(int) * (size_t)dag_sync_ints(nt)));
     CUDA_TRY(c, cudaMalloc(&c->dag_W, sizeof(double) * (size_t)nt * PB * PB));
     c->dag_cap_nt = nt;
   }
@@ -387,7 +388,7 @@ exageo_status factor_panel(exageo_ctx* c, RankState& R, int k, cudaStream_t s) {
     }
     double* W = w_block(R, k, sb);
     launch_potrf_block(Pk + c0 * ldk + c0, ldk, W, R.slots + (int64_t)m * nsub + sb, R.info, (int64_t)k * L.nb + c0,
-                       s, pdl && !first);
+                       s, pdl && !first, (int)std::min<int64_t>(PB, L.n - ((int64_t)k * L.nb + c0)));
     double* below = Pk + c0 * ldk + c0 + PB;
     launch_gemm_panel(ldk - c0 - PB, PB, PB, below, ldk, W, PB, below, ldk, false, R.info, s, pdl);
     c->kernels += 2;
@@ -427,9 +428,7 @@ exageo_status factor_tile_tasks(exageo_ctx* c) {
     return fail(c, EXAGEO_EINVAL, "tile-task plan missing (prepare_generate)");
   RankState& R = c->rs[0];
   const Layout& L = R.L;
-  CUDA_TRY(c, cudaMemsetAsync(c->dag_sync, 0, sizeof(int) * (size_t)dag_sync_ints(c->dag_nt), c->stream));
-  // log-det slots of 64-blocks beyond n (identity padding) stay zero
-  CUDA_TRY(c, cudaMemsetAsync(R.slots, 0, sizeof(double) * (size_t)L.owned() * (L.nb / PB), c->stream));
+  // the counters are zero: set at allocation, reset by the last CTA of every launch
   R.n_u2 = 0;
   R.u2_flops = 0.0;
   const int nctas = 1 + std::min(c->dag_nproc - 1, std::max(c->dag_ntasks, 1));  // chain CTA + pool

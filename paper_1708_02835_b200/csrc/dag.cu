@@ -320,14 +320,13 @@ __device__ void chain_cta(const DagArgs& a, int* st, double* sm) {
       r[3] = gtimer();
     }
   };
+  for (int i = a.nt + threadIdx.x; i < a.L.owned() * nsub; i += 256) a.slots[i] = 0.0;  // padding blocks
   for (int k = 0; k < a.nt; ++k) {
     const bool last = k + 1 == a.nt;
     int64_t ld, ldb = 0, ldd = 0;
     double* Akk = tile_ptr(a, k, k, ld);
     double* Ab = last ? nullptr : tile_ptr(a, k + 1, k, ldb);
     double* Ad = last ? nullptr : tile_ptr(a, k + 1, k + 1, ldd);
-    if (threadIdx.x == 0) s_issued = last ? 3 : 0;
-    __syncthreads();
     const unsigned long long t0 = a.trace ? gtimer() : 0;
     // POTRF(k): st(k, k) == k already (the pool's updates were waited for before SYRK(k, k, k-1))
     int hst[3] = {last ? 3 : 0, 0, 0};
@@ -335,8 +334,10 @@ __device__ void chain_cta(const DagArgs& a, int* st, double* sm) {
                        &s_issued, hst};
     double* Wk = a.W + (size_t)k * PB * PB;
     double* slot = a.slots + (k / nsub) * nsub + k % nsub;
-    const bool ok = k == 0 ? potrf64_body<false>(Akk, ld, Wk, slot, a.info, (int64_t)k * PB, sm, hook)
-                           : potrf64_body<true>(Akk, ld, Wk, slot, a.info, (int64_t)k * PB, sm, hook);
+    const int64_t ncols = a.n - (int64_t)k * PB;  // ragged last block: only its real strips
+    const int nstrips = ncols >= PB ? 4 : (int)(ncols + 15) / 16;
+    const bool ok = k == 0 ? potrf64_body<false>(Akk, ld, Wk, slot, a.info, (int64_t)k * PB, sm, hook, nstrips)
+                           : potrf64_body<true>(Akk, ld, Wk, slot, a.info, (int64_t)k * PB, sm, hook, nstrips);
     if (!ok) {
       asm volatile("cp.async.wait_all;\n" ::: "memory");
       return;
@@ -428,6 +429,14 @@ __device__ void finish_tail(const DagArgs& a, double* red) {
     a.out3[0] = -0.5 * q - 0.5 * logdet - 0.5 * (double)a.n * 1.8378770664093454835606594728112;
     a.out3[1] = logdet;
     a.out3[2] = q;
+  }
+  // every other CTA has left: zero the counters this launch used, ready for the next one
+  // (no memset node before each launch)
+  int* st = a.sync + kSyncHead;
+  for (int u = tid; u < a.nt * a.nt + a.nt; u += 256) st[u * kPad] = 0;  // tile and z counters
+  if (tid == 0) {
+    a.sync[0] = 0;
+    a.sync[16] = 0;
   }
 }
 

@@ -185,10 +185,10 @@ void launch_dag_factor(const Layout& L, double* ws, const int4* tasks, int ntask
 const void* dag_factor_kernel_fn();
 
 // Factor the PB x PB diagonal block at `a` (ld) in place, write W = L^{-1} (PB x PB,
-// ld PB) and slot = sum log L_ii; info = first bad global pivot + 1.
+// ld PB) and slot = sum log L_ii; info = first bad global pivot + 1. ncols < PB: only the
+// first ncols columns are inside n (the rest is identity padding; only their strips run).
 void launch_potrf_block(double* a, int64_t lda, double* W, double* logdet_slot, int* info, int64_t pivot_base,
-                        cudaStream_t s,
-                        bool pdl = false);
+                        cudaStream_t s, bool pdl = false, int ncols = PB);
 // out2 = {sum of this rank's log-det partials (nslots), sum of y_c^2 over this rank's columns};
 // scratch: kQuadBlocks doubles.
 void launch_local_partials(const Layout& L, const double* ws, const double* slots, int nslots, double* scratch,

@@ -224,7 +224,10 @@ __device__ __forceinline__ int factor_strip(double* As, double* dv, double* rs, 
 // blocks are read) -- the tile-task chain CTA hands the SYRK result over in shared memory.
 // hook(K), K = 0..4, runs on warp 7 (a helper warp without block work) at the start of strip
 // K's helper phase (K = 4: after the last one): the chain CTA polls and prefetches the next tiles there. Returns false
-// (uniformly) when a pivot failed (info written).
+// (uniformly) when a pivot failed (info written). nstrips (1..4): 16-column strips holding
+// columns < n; the others are identity padding (R12): not factored, L stays the generated
+// identity, W gets identity rows, log L_ii = 0 -- the ragged last block of a matrix costs
+// only its real strips.
 struct NoHook {
   __device__ __forceinline__ void operator()(int) const {}
 };
@@ -232,7 +235,7 @@ struct NoHook {
 template <bool kFromSmem = false, class Hook = NoHook>
 __device__ __forceinline__ bool potrf64_body(double* __restrict__ a, int64_t lda, double* __restrict__ W,
                                              double* __restrict__ slot, int* __restrict__ info, int64_t pivot_base,
-                                             double* smem_p, Hook hook = Hook()) {
+                                             double* smem_p, Hook hook = Hook(), int nstrips = 4) {
   PTRACE(0);
   double* As = smem_p;             // As[c * LDA2 + r]
   double* Ws = As + PB * LDA2;     // Ws[c * LDA2 + r]
@@ -263,7 +266,7 @@ __device__ __forceinline__ bool potrf64_body(double* __restrict__ a, int64_t lda
   if (warp < NFW) {
     int first = -1;
 #pragma unroll 1
-    for (int K = 0; K < 4; ++K) {
+    for (int K = 0; K < nstrips; ++K) {
       int b;
       switch (K) {
         case 0: b = factor_strip<64>(As, dv, rs, colbuf, a, lda); break;
@@ -289,6 +292,14 @@ __device__ __forceinline__ bool potrf64_body(double* __restrict__ a, int64_t lda
     for (int K = 0; K < 4; ++K) {
       const int k0 = 16 * K;
       if (warp == 7) hook(K);
+      if (K >= nstrips) {  // identity padding: W row block K = identity rows, log L_ii = 0
+        for (int idx = tid - 32 * NFW; idx < 16 * PB; idx += NH) {
+          const int r = idx & 15, c = idx >> 4;
+          W[c * PB + k0 + r] = (c == k0 + r) ? 1.0 : 0.0;
+        }
+        if (warp == NFW && lane < 16) lgv[k0 + lane] = 0.0;
+        continue;
+      }
       named_sync(1 + K, 256);  // strip K is in As
       if (warp == NFW && lane < 16) {  // column c = lane of T_K: t_r = (delta_rc - sum_{m<r} L_rm t_m) / L_rr
         const int c = lane;

@@ -26,12 +26,12 @@ namespace {
 
 __global__ void __launch_bounds__(256) potrf_block_kernel(double* __restrict__ a, int64_t lda,
                                                           double* __restrict__ W, double* __restrict__ slot,
-                                                          int* __restrict__ info, int64_t pivot_base) {
+                                                          int* __restrict__ info, int64_t pivot_base, int nstrips) {
   asm volatile("griddepcontrol.wait;\n" ::: "memory");  // programmatic dependent launch
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   if (*(volatile int*)info != 0) return;
   extern __shared__ double smem_p[];
-  potrf64_body(a, lda, W, slot, info, pivot_base, smem_p);
+  potrf64_body(a, lda, W, slot, info, pivot_base, smem_p, NoHook(), nstrips);
 }
 
 // Fixed-shape block sum (blockDim.x a multiple of 32): deterministic tree.
@@ -192,9 +192,10 @@ cudaError_t potrf_init() {
 }
 
 void launch_potrf_block(double* a, int64_t lda, double* W, double* slot, int* info, int64_t pivot_base,
-                        cudaStream_t s, bool pdl) {
+                        cudaStream_t s, bool pdl, int ncols) {
+  const int nstrips = ncols >= PB ? 4 : (ncols + 15) / 16;
   if (!pdl) {
-    potrf_block_kernel<<<1, 256, kPotrfSmem, s>>>(a, lda, W, slot, info, pivot_base);
+    potrf_block_kernel<<<1, 256, kPotrfSmem, s>>>(a, lda, W, slot, info, pivot_base, nstrips);
     return;
   }
   cudaLaunchConfig_t cfg = {};
@@ -207,7 +208,7 @@ void launch_potrf_block(double* a, int64_t lda, double* W, double* slot, int* in
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, potrf_block_kernel, a, lda, W, slot, info, pivot_base);
+  cudaLaunchKernelEx(&cfg, potrf_block_kernel, a, lda, W, slot, info, pivot_base, nstrips);
 }
 
 void launch_local_partials(const Layout& L, const double* ws, const double* slots, int nslots, double* scratch,

@@ -47,7 +47,7 @@ def test_ind_large_super_tile_is_exact():
     n, nb = 1700, 128
     x, y = ex.gen_locations(n, 5)
     z = si.normals(n, 6)
-    a = ex.Context(device=0, nb=nb).loglik(x, y, z, (1.0, 0.1, 0.7))
+    a = ex.Context(device=0, nb=nb, tile_tasks=-1).loglik(x, y, z, (1.0, 0.1, 0.7))  # same (stream) schedule
     b = ex.Context(device=0, nb=nb, ind_tiles=100).loglik(x, y, z, (1.0, 0.1, 0.7))
     assert a.loglik == b.loglik
 

@@ -23,7 +23,7 @@ def test_single_rank_nccl_equals_plain():
     x, y = ex.gen_locations(n, 1)
     e = si.normals(n, 2)
     theta = (1.0, 0.1, 0.8)
-    plain = ex.Context(device=0, nb=128)
+    plain = ex.Context(device=0, nb=128, tile_tasks=-1)  # the NCCL context's schedule
     nc = ex.Context(device=0, nb=128, world=1, rank=0, nccl_id=ex.nccl_unique_id())
     z1 = plain.simulate(x, y, e, theta)
     z2 = nc.simulate(x, y, e, theta)

@@ -256,7 +256,7 @@ def test_virtual_ranks_match_single_and_oracle(world, n, nb):
     x, y = ex.gen_locations(n, 21)
     theta = (1.0, 0.1, 0.8)
     z = oracle.simulate(x, y, (1.0, 0.1, 0.5), si.normals(n, 22))
-    single = ex.Context(device=0, nb=nb)
+    single = ex.Context(device=0, nb=nb, tile_tasks=-1)  # the distributed schedule's kernels
     r1 = single.loglik(x, y, z, theta)
     single.close()
     c = ex.Context(device=0, nb=nb, virtual_ranks=world)
@@ -269,7 +269,7 @@ def test_virtual_ranks_match_single_and_oracle(world, n, nb):
     c.stage_generate_dev(dev(x), dev(y), dev(z), theta)
     c.stage_factor()
     Lv = c.read_lower(n)
-    s2 = ex.Context(device=0, nb=nb)
+    s2 = ex.Context(device=0, nb=nb, tile_tasks=-1)
     s2.stage_generate_dev(dev(x), dev(y), dev(z), theta)
     s2.stage_factor()
     assert np.array_equal(Lv, s2.read_lower(n))
@@ -304,7 +304,7 @@ def test_grid_virtual_ranks_match_single_and_oracle(P, Q, n, nb):
     x, y = ex.gen_locations(n, 21)
     theta = (1.0, 0.1, 0.8)
     z = oracle.simulate(x, y, (1.0, 0.1, 0.5), si.normals(n, 22))
-    single = ex.Context(device=0, nb=nb)
+    single = ex.Context(device=0, nb=nb, tile_tasks=-1)  # the distributed schedule's kernels
     r1 = single.loglik(x, y, z, theta)
     single.stage_generate_dev(dev(x), dev(y), dev(z), theta)
     single.stage_factor()

@@ -63,7 +63,7 @@ def test_predict_virtual_ranks(ctx, world):
     z = si.normals(n, 10)
     rng = np.random.default_rng(1)
     xn, yn = rng.random(m), rng.random(m)
-    c1 = ex.Context(device=0, nb=128)
+    c1 = ex.Context(device=0, nb=128, tile_tasks=-1)  # the distributed schedule's kernels
     a = c1.predict(x, y, z, xn, yn, theta)
     c1.close()
     cv = ex.Context(device=0, nb=128, virtual_ranks=world)
