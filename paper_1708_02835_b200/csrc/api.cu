@@ -197,6 +197,7 @@ exageo_status ensure_buffers(exageo_ctx* c) {
       cudaFree(R.ws);
       R.ws = nullptr;
       R.ws_bytes = 0;
+      c->dag_init_key.clear();  // a new allocation may reuse the address with other contents
       cudaError_t e = alloc_or_fail((void**)&R.ws, local_bytes(L));
       if (e != cudaSuccess) return fail(c, EXAGEO_ENOMEM, std::string("cudaMalloc workspace: ") + cudaGetErrorString(e));
       R.ws_bytes = local_bytes(L);
@@ -327,29 +328,58 @@ exageo_status prepare_generate(exageo_ctx* c, const exageo_theta* t, int64_t n, 
   exageo_status st = ensure_buffers(c);
   if (st != EXAGEO_OK) return st;
   // the tile-task plan and buffers exist before any launch (and outside graph capture)
-  return tile_tasks_eligible(c, n) ? prepare_tile_tasks(c) : EXAGEO_OK;
+  if (!tile_tasks_eligible(c, n)) return EXAGEO_OK;
+  if ((st = prepare_tile_tasks(c)) != EXAGEO_OK) return st;
+  // the executor generates only the tiles inside n; the rest of the layout (identity padding,
+  // the z block's zero rows) is theta-independent: generated once per workspace and layout
+  const std::vector<const void*> key = {c->rs[0].ws, (const void*)(intptr_t)n, (const void*)(intptr_t)nb};
+  if (c->dag_init_key != key) {
+    const MaternConsts mc = make_consts(*t, c);
+    launch_matern_table(mc, c->mtab, c->stream);
+    launch_gen_panels(c->rs[0].L, c->rs[0].ws, mc, x, y, nullptr, c->mtab, c->stream);
+    if ((st = check_launch(c)) != EXAGEO_OK) return st;
+    c->dag_init_key = key;
+  }
+  return EXAGEO_OK;
 }
 
 exageo_status launch_generate(exageo_ctx* c, const MaternConsts& mc, const double* x, const double* y,
-                              const double* z) {
-  c->kernels += launch_matern_table(mc, c->mtab, c->stream);
+                              const double* z, bool defer = false) {
+  const int tab = launch_matern_table(mc, c->mtab, c->stream);
+  c->kernels += tab;
+  c->gen_launches += tab;
+  if (defer && tile_tasks_eligible(c, c->G.n)) {
+    // Alg. 2 l.2 fused into the executor (its GEN tasks, ahead of the factorization's tasks)
+    CUDA_TRY(c, cudaMemsetAsync(c->rs[0].info, 0, sizeof(int), c->stream));
+    c->dag_gen = true;
+    c->dag_mc = mc;
+    c->dag_x = x;
+    c->dag_y = y;
+    c->dag_z = z;
+    c->have_matrix = true;
+    c->dag_finished = false;
+    return check_launch(c);
+  }
+  c->dag_gen = false;
   for (auto& R : c->rs) {
     CUDA_TRY(c, cudaMemsetAsync(R.info, 0, sizeof(int), c->stream));
     if (R.L.P > 1)  // only the diagonal ranks write log-det slots (the others' stay zero)
       CUDA_TRY(c, cudaMemsetAsync(R.slots, 0, sizeof(double) * (size_t)R.L.owned() * (R.L.nb / PB), c->stream));
     launch_gen_panels(R.L, R.ws, mc, x, y, z, c->mtab, c->stream);
     c->kernels += 1;
+    c->gen_launches += 1;
   }
   c->have_matrix = true;
   c->dag_finished = false;
   return check_launch(c);
 }
 
+// defer: the caller factors next (loglik, simulate, predict), so the executor may generate
 exageo_status do_generate(exageo_ctx* c, const exageo_theta* t, int64_t n, const double* x, const double* y,
-                          const double* z) {
+                          const double* z, bool defer = false) {
   exageo_status st = prepare_generate(c, t, n, x, y);
   if (st != EXAGEO_OK) return st;
-  return launch_generate(c, make_consts(*t, c), x, y, z);
+  return launch_generate(c, make_consts(*t, c), x, y, z, defer);
 }
 
 // ---------------------------------------------------------------------------- factorization
@@ -432,9 +462,12 @@ exageo_status factor_tile_tasks(exageo_ctx* c) {
   R.n_u2 = 0;
   R.u2_flops = 0.0;
   const int nctas = 1 + std::min(c->dag_nproc - 1, std::max(c->dag_ntasks, 1));  // chain CTA + pool
+  DagGen g{c->dag_gen, c->dag_mc, c->mtab, c->dag_x, c->dag_y, c->dag_z};
   launch_dag_factor(L, R.ws, c->dag_tasks, c->dag_ntasks, c->dag_nt, c->dag_sync, c->dag_W, R.slots, R.info,
-                    c->out3, c->dag_trace, nctas, c->stream);
+                    c->out3, c->dag_trace, g, nctas, c->stream);
   c->kernels += 1;
+  if (c->dag_gen) c->gen_launches += 1;
+  c->dag_gen = false;  // one generation per launch_generate
   c->dag_finished = true;
   return check_launch(c);
 }
@@ -807,7 +840,7 @@ std::vector<const void*> graph_key(const exageo_ctx* c, const double* x, const d
 exageo_status graph_body(exageo_ctx* c, const MaternConsts& mc, const double* x, const double* y,
                          const double* z) {
   CUDA_TRY(c, record_timing(c, c->ev[0], c->stream));
-  exageo_status st = launch_generate(c, mc, x, y, z);
+  exageo_status st = launch_generate(c, mc, x, y, z, true);
   if (st != EXAGEO_OK) return st;
   CUDA_TRY(c, record_timing(c, c->ev[1], c->stream));
   if ((st = do_factor(c)) != EXAGEO_OK) return st;
@@ -840,6 +873,7 @@ exageo_status run_graph(exageo_ctx* c, const exageo_theta* t, int64_t n, const d
   if (!c->gexec || key != c->gkey) {
     destroy_graph(c);
     const int64_t k0 = c->kernels;
+    c->gen_launches = 0;
     CUDA_TRY(c, cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
     c->capturing = true;
     st = graph_body(c, mc, x, y, z);
@@ -863,9 +897,11 @@ exageo_status run_graph(exageo_ctx* c, const exageo_theta* t, int64_t n, const d
       if (ty != cudaGraphNodeTypeKernel) continue;
       cudaKernelNodeParams kp;
       CUDA_TRY(c, cudaGraphKernelNodeGetParams(nd, &kp));
-      if (kp.func == gen_panels_kernel_fn(mc.kind) || kp.func == matern_table_kernel_fn()) c->gen_nodes.push_back(nd);
+      if (kp.func == gen_panels_kernel_fn(mc.kind) || kp.func == matern_table_kernel_fn() ||
+          (kp.func == dag_factor_kernel_fn() && dag_args_generate(kp.kernelParams[0])))
+        c->gen_nodes.push_back(nd);
     }
-    if (c->gen_nodes.size() != c->rs.size() + (mc.kind == 0 ? 1 : 0)) {
+    if ((int)c->gen_nodes.size() != c->gen_launches) {
       destroy_graph(c);
       return fail(c, EXAGEO_ECUDA, "graph capture: generator nodes not found");
     }
@@ -885,11 +921,17 @@ exageo_status run_graph(exageo_ctx* c, const exageo_theta* t, int64_t n, const d
       cudaKernelNodeParams kp;
       CUDA_TRY(c, cudaGraphKernelNodeGetParams(nd, &kp));
       void* args[7];
-      const bool gen = kp.func == gen_panels_kernel_fn(mc.kind);
-      const int nargs = gen ? 7 : 2, imc = gen ? 2 : 0;
-      // gen_panels_kernel(Layout, ws, MaternConsts, x, y, z, tab); matern_table_kernel(MaternConsts, tab)
-      for (int i = 0; i < nargs; ++i) args[i] = kp.kernelParams[i];
-      args[imc] = (void*)&mc;
+      std::vector<char> dag_args;
+      if (kp.func == dag_factor_kernel_fn()) {  // dag_factor_kernel(DagArgs): theta inside the struct
+        dag_args_with_theta(kp.kernelParams[0], mc, dag_args);
+        args[0] = dag_args.data();
+      } else {
+        const bool gen = kp.func == gen_panels_kernel_fn(mc.kind);
+        const int nargs = gen ? 7 : 2, imc = gen ? 2 : 0;
+        // gen_panels_kernel(Layout, ws, MaternConsts, x, y, z, tab); matern_table_kernel(MaternConsts, tab)
+        for (int i = 0; i < nargs; ++i) args[i] = kp.kernelParams[i];
+        args[imc] = (void*)&mc;
+      }
       kp.kernelParams = args;
       CUDA_TRY(c, cudaGraphExecKernelNodeSetParams(c->gexec, nd, &kp));
     }
@@ -925,7 +967,7 @@ exageo_status loglik_device(exageo_ctx* c, const exageo_theta* t, int64_t n, con
     if (st != EXAGEO_OK && st != EXAGEO_ENOTPD) return st;
   } else {
     CUDA_TRY(c, cudaEventRecord(c->ev[0], c->stream));
-    st = do_generate(c, t, n, x, y, z);
+    st = do_generate(c, t, n, x, y, z, true);
     if (st != EXAGEO_OK) return st;
     CUDA_TRY(c, cudaEventRecord(c->ev[1], c->stream));
     st = do_factor(c);
@@ -1219,6 +1261,7 @@ exageo_status exageo_set_workspace(exageo_ctx* c, void* ptr, size_t bytes) {
   R.ws_bytes = ptr ? bytes : 0;
   R.ws_external = ptr != nullptr;
   c->have_matrix = false;
+  c->dag_init_key.clear();
   return EXAGEO_OK;
 }
 
@@ -1298,7 +1341,7 @@ exageo_status exageo_simulate(exageo_ctx* c, const exageo_theta* t, int64_t n, c
   CUDA_TRY(c, cudaMemcpyAsync(dx, x, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
   CUDA_TRY(c, cudaMemcpyAsync(dy, y, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
   CUDA_TRY(c, cudaMemcpyAsync(de, e, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
-  st = do_generate(c, t, n, dx, dy, nullptr);
+  st = do_generate(c, t, n, dx, dy, nullptr, true);
   if (st != EXAGEO_OK) return st;
   st = do_factor(c);
   if (st != EXAGEO_OK) return st;
@@ -1366,7 +1409,7 @@ exageo_status exageo_predict(exageo_ctx* c, const exageo_theta* t, int64_t n, co
   CUDA_TRY(c, cudaMemcpyAsync(dxn, xnew, sizeof(double) * m, cudaMemcpyHostToDevice, c->stream));
   CUDA_TRY(c, cudaMemcpyAsync(dyn, ynew, sizeof(double) * m, cudaMemcpyHostToDevice, c->stream));
   // Alg. 3 l.3-7: Sigma22 = L L^T with the forward solve y = L^{-1} z2 fused (z row)
-  exageo_status st = do_generate(c, t, n, dx, dy, dz);
+  exageo_status st = do_generate(c, t, n, dx, dy, dz, true);
   if (st != EXAGEO_OK) return st;
   st = do_factor(c);
   if (st != EXAGEO_OK) return st;

@@ -92,6 +92,12 @@ struct exageo_ctx {
   int dag_cap_nt = 0;          // nt the sync / W buffers are sized for
   int64_t dag_cap_tasks = 0;
   bool dag_finished = false;   // the last factorization ran on the executor (out3 written by it)
+  // fused generation: launch_generate defers Sigma's tiles inside n to the executor's GEN tasks
+  bool dag_gen = false;        // the next executor launch generates (params below)
+  exageo::MaternConsts dag_mc{};
+  const double *dag_x = nullptr, *dag_y = nullptr, *dag_z = nullptr;
+  std::vector<const void*> dag_init_key;  // (ws, n, nb) whose padding / z block was generated
+  int gen_launches = 0;        // kernels that take theta (K1T, K1, executor with GEN), counted per capture
   // tracing (env EXAGEO_TILE_TASK_TRACE=<file>): per ticket {cta, grabbed, ready, done} of the
   // last evaluation, written as text when the context is destroyed
   std::string dag_trace_path;

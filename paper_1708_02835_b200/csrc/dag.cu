@@ -20,7 +20,10 @@
 //     Start times respect every dependency, so the order is topological: a task's inputs are
 //     always held by CTAs already running (no deadlock for any grid size).
 // Every tile version counter st(i,j) counts the operations applied to tile (i, j) in the
-// fixed order k = 0, 1, ...; updates are never reordered, so results are deterministic.
+// fixed order GEN, k = 0, 1, ...: 1 after GEN, k + 2 after the update by panel k (or, at
+// k = j, after POTRF / TRSM: final); the z segments likewise. Updates are never reordered, so
+// results are deterministic. GEN tasks (Alg. 2 l.2, Eq. (2)) generate Sigma's tiles inside n
+// and the z row in the same kernel, highest priority first (the first panel's tiles).
 // The data stays in the standard panel layout (internal.h), so predict, simulate and the
 // read-back entries work on the result unchanged. Tile rows at or beyond n (pure identity
 // padding, zero left of the diagonal) are never touched, as in the stream path.
@@ -30,6 +33,7 @@
 #include <vector>
 
 #include "internal.h"
+#include "matern_eval.cuh"
 
 namespace exageo {
 
@@ -45,7 +49,7 @@ constexpr int kSyncHead = 32;  // ints before the tile counters (the ticket is s
 constexpr int kPad = 32;       // one 128-byte line per version counter (pollers of different
                                // tiles never share a line with each other or the ticket)
 
-enum TaskType : int { kPotrf = 0, kTrsm = 1, kGemm = 2, kZTrsm = 3, kZGemm = 4 };
+enum TaskType : int { kPotrf = 0, kTrsm = 1, kGemm = 2, kZTrsm = 3, kZGemm = 4, kGen = 5 };
 
 struct DagArgs {
   Layout L;
@@ -59,6 +63,7 @@ struct DagArgs {
   int* info;
   double* out3;   // {loglik, logdet, quad}, written by the last CTA to leave (Alg. 2 l.5-7)
   int64_t n;
+  DagGen gen;
   unsigned long long* trace;  // optional: per ticket {cta, grabbed, inputs ready, done} (ns)
 };
 
@@ -218,6 +223,43 @@ __device__ __forceinline__ void z_gemm(double* zj, int64_t ldzj, const double* y
   }
 }
 
+// GEN(i, j): tile (i, j) of Sigma by Eq. (2) -- identity padding outside n (R12),
+// theta1 on the diagonal (R9); thread: row 64 i + (tid & 63), 16 columns from 16 (tid >> 6).
+// The upper half of a diagonal tile gets the symmetric values (never read).
+template <int KIND>
+__device__ __forceinline__ void gen_tile_k(const DagArgs& a, double* T, int64_t ld, int i, int j, double* sm) {
+  const MaternConsts& mc = a.gen.mc;
+  const int r = threadIdx.x & 63, cb = 16 * (threadIdx.x >> 6);
+  const int64_t gr = (int64_t)i * PB + r;
+  const bool rin = gr < a.n;
+  double* xc = sm;  // the tile's 64 column sites, loaded once
+  double* yc = sm + PB;
+  if (threadIdx.x < PB) {
+    const int64_t gc = (int64_t)j * PB + threadIdx.x;
+    xc[threadIdx.x] = gc < a.n ? a.gen.x[gc] : 0.0;
+    yc[threadIdx.x] = gc < a.n ? a.gen.y[gc] : 0.0;
+  }
+  const double xr = rin ? a.gen.x[gr] : 0.0, yr = rin ? a.gen.y[gr] : 0.0;
+  __syncthreads();
+#pragma unroll(KIND == 0 ? 1 : 4)  // closed forms: independent entries in flight together
+  for (int cc = 0; cc < 16; ++cc) {
+    const int64_t gc = (int64_t)j * PB + cb + cc;
+    double v;
+    if (!rin || gc >= a.n) v = gr == gc ? 1.0 : 0.0;
+    else if (gr == gc) v = mc.theta1;
+    else v = mat::matern_eval_k<KIND>(mat::dist2d(xr, yr, xc[cb + cc], yc[cb + cc], mc), mc, a.gen.tab);
+    T[(int64_t)(cb + cc) * ld + r] = v;
+  }
+}
+__device__ __forceinline__ void gen_tile(const DagArgs& a, double* T, int64_t ld, int i, int j, double* sm) {
+  switch (a.gen.mc.kind) {
+    case 1: gen_tile_k<1>(a, T, ld, i, j, sm); break;
+    case 2: gen_tile_k<2>(a, T, ld, i, j, sm); break;
+    case 3: gen_tile_k<3>(a, T, ld, i, j, sm); break;
+    default: gen_tile_k<0>(a, T, ld, i, j, sm); break;
+  }
+}
+
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -321,6 +363,15 @@ __device__ void chain_cta(const DagArgs& a, int* st, double* sm) {
     }
   };
   for (int i = a.nt + threadIdx.x; i < a.L.owned() * nsub; i += 256) a.slots[i] = 0.0;  // padding blocks
+  {  // A_00 (after its GEN task) into the K2 body's input block; later blocks come from SYRK
+    if (threadIdx.x == 0) s_ok = wait_ge(stf(0, 0), 1, a.info);
+    __syncthreads();
+    if (!s_ok) return;
+    int64_t ld0;
+    stage_tile(sm, tile_ptr(a, 0, 0, ld0), ld0);
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+    __syncthreads();
+  }
   for (int k = 0; k < a.nt; ++k) {
     const bool last = k + 1 == a.nt;
     int64_t ld, ldb = 0, ldd = 0;
@@ -328,21 +379,21 @@ __device__ void chain_cta(const DagArgs& a, int* st, double* sm) {
     double* Ab = last ? nullptr : tile_ptr(a, k + 1, k, ldb);
     double* Ad = last ? nullptr : tile_ptr(a, k + 1, k + 1, ldd);
     const unsigned long long t0 = a.trace ? gtimer() : 0;
-    // POTRF(k): st(k, k) == k already (the pool's updates were waited for before SYRK(k, k, k-1))
+    // POTRF(k): the block is in shared memory (A_00 staged above, else the SYRK(k, k, k-1) result,
+    // whose input version k was waited for)
     int hst[3] = {last ? 3 : 0, 0, 0};
-    ChainPrefetch hook{last ? nullptr : stf(k + 1, k), last ? nullptr : stf(k + 1, k + 1), k, X, Ab, ldb, Y, Ad, ldd,
+    ChainPrefetch hook{last ? nullptr : stf(k + 1, k), last ? nullptr : stf(k + 1, k + 1), k + 1, X, Ab, ldb, Y, Ad, ldd,
                        &s_issued, hst};
     double* Wk = a.W + (size_t)k * PB * PB;
     double* slot = a.slots + (k / nsub) * nsub + k % nsub;
     const int64_t ncols = a.n - (int64_t)k * PB;  // ragged last block: only its real strips
     const int nstrips = ncols >= PB ? 4 : (int)(ncols + 15) / 16;
-    const bool ok = k == 0 ? potrf64_body<false>(Akk, ld, Wk, slot, a.info, (int64_t)k * PB, sm, hook, nstrips)
-                           : potrf64_body<true>(Akk, ld, Wk, slot, a.info, (int64_t)k * PB, sm, hook, nstrips);
+    const bool ok = potrf64_body<true>(Akk, ld, Wk, slot, a.info, (int64_t)k * PB, sm, hook, nstrips);
     if (!ok) {
       asm volatile("cp.async.wait_all;\n" ::: "memory");
       return;
     }
-    release_by(0, stf(k, k), k + 1);  // body ended with a barrier: L_kk, W_k stored
+    release_by(0, stf(k, k), k + 2);  // body ended with a barrier: L_kk, W_k stored
     rec(3 * k, t0, t0);
     if (last) break;
     // TRSM(k+1, k): L_{k+1,k} = A_{k+1,k} W_k^T
@@ -350,7 +401,7 @@ __device__ void chain_cta(const DagArgs& a, int* st, double* sm) {
     const int issued = s_issued;
     if (warp == 7) asm volatile("cp.async.wait_all;\n" ::: "memory");
     if (!(issued & 1)) {
-      if (threadIdx.x == 0) s_ok = wait_ge(stf(k + 1, k), k, a.info);
+      if (threadIdx.x == 0) s_ok = wait_ge(stf(k + 1, k), k + 1, a.info);
       __syncthreads();
       if (!s_ok) return;
       stage_tile(X, Ab, ldb);
@@ -365,12 +416,12 @@ __device__ void chain_cta(const DagArgs& a, int* st, double* sm) {
     frag_store(f, Ab, ldb);
     frag_store(f, X, LDS);
     __syncthreads();
-    release_by(4, stf(k + 1, k), k + 1);  // warp 4 has no SYRK block
+    release_by(4, stf(k + 1, k), k + 2);  // warp 4 has no SYRK block
     rec(3 * k + 1, t2, t3);
     // SYRK(k+1, k+1, k): A_{k+1,k+1} -= L_{k+1,k} L_{k+1,k}^T into the body's input block As
     const unsigned long long t4 = a.trace ? gtimer() : 0;
     if (!(issued & 2)) {
-      if (threadIdx.x == 0) s_ok = wait_ge(stf(k + 1, k + 1), k, a.info);
+      if (threadIdx.x == 0) s_ok = wait_ge(stf(k + 1, k + 1), k + 1, a.info);
       __syncthreads();
       if (!s_ok) return;
       stage_tile(Y, Ad, ldd);
@@ -470,15 +521,16 @@ __device__ void pool_cta(const DagArgs& a, int* st, int* zs, double* sm) {
     if (threadIdx.x == 0) {
       bool ok = true;
       switch (type) {
-        case kTrsm: ok = wait_ge(st + (k * a.nt + k) * kPad, k + 1, a.info) && wait_ge(st + (i * a.nt + k) * kPad, k, a.info); break;
+        case kTrsm: ok = wait_ge(st + (k * a.nt + k) * kPad, k + 2, a.info) && wait_ge(st + (i * a.nt + k) * kPad, k + 1, a.info); break;
         case kGemm:
-          ok = wait_ge(st + (i * a.nt + k) * kPad, k + 1, a.info) && wait_ge(st + (j * a.nt + k) * kPad, k + 1, a.info) &&
-               wait_ge(st + (i * a.nt + j) * kPad, k, a.info);
+          ok = wait_ge(st + (i * a.nt + k) * kPad, k + 2, a.info) && wait_ge(st + (j * a.nt + k) * kPad, k + 2, a.info) &&
+               wait_ge(st + (i * a.nt + j) * kPad, k + 1, a.info);
           break;
-        case kZTrsm: ok = wait_ge(st + (k * a.nt + k) * kPad, k + 1, a.info) && wait_ge(zs + k * kPad, k, a.info); break;
+        case kZTrsm: ok = wait_ge(st + (k * a.nt + k) * kPad, k + 2, a.info) && wait_ge(zs + k * kPad, k + 1, a.info); break;
+        case kGen: break;
         default:
-          ok = wait_ge(zs + k * kPad, k + 1, a.info) && wait_ge(st + (j * a.nt + k) * kPad, k + 1, a.info) &&
-               wait_ge(zs + j * kPad, k, a.info);
+          ok = wait_ge(zs + k * kPad, k + 2, a.info) && wait_ge(st + (j * a.nt + k) * kPad, k + 2, a.info) &&
+               wait_ge(zs + j * kPad, k + 1, a.info);
           break;
       }
       s_ok = ok;
@@ -511,6 +563,21 @@ __device__ void pool_cta(const DagArgs& a, int* st, int* zs, double* sm) {
         flag = st + (i * a.nt + j) * kPad;
         break;
       }
+      case kGen: {
+        if (i < a.nt) {
+          double* T = tile_ptr(a, i, j, ld);
+          if (a.gen.generate) gen_tile(a, T, ld, i, j, sm);
+          flag = st + (i * a.nt + j) * kPad;
+        } else {
+          double* zj = zseg_ptr(a, j, ld);
+          if (a.gen.generate && threadIdx.x < PB) {
+            const int64_t c = (int64_t)j * PB + threadIdx.x;
+            zj[(int64_t)threadIdx.x * ld] = (c < a.n && a.gen.z) ? a.gen.z[c] : 0.0;  // simulate: no z
+          }
+          flag = zs + j * kPad;
+        }
+        break;
+      }
       case kZTrsm: {
         double* zk = zseg_ptr(a, k, ld);
         z_trsm(zk, ld, a.W + (size_t)k * PB * PB, sm);
@@ -530,7 +597,7 @@ __device__ void pool_cta(const DagArgs& a, int* st, int* zs, double* sm) {
     __syncthreads();
     if (threadIdx.x == 0) {
       __threadfence();
-      st_release(flag, k + 1);
+      st_release(flag, type == kGen ? 1 : k + 2);
       if (a.trace) a.trace[4 * t + 3] = gtimer();
     }
   }
@@ -560,12 +627,17 @@ void dag_plan(int nt, int nproc, std::vector<int4>& order) {
     deps.push_back(std::move(d));
     return (int)tk.size() - 1;
   };
+  std::vector<int> genz(nt);
+  for (int j = 0; j < nt; ++j) {  // GEN tasks: Sigma's tiles inside n and the z row (Alg. 2 l.2)
+    for (int i = j; i < nt; ++i) gemm_prev[(size_t)i * nt + j] = add(kGen, i, j, 0, 1.5f, false, {});
+    genz[j] = add(kGen, nt, j, 0, 0.5f, false, {});
+  }
   for (int k = 0; k < nt; ++k) {
     potrf[k] = add(kPotrf, k, k, k, 13.f, true, {gemm_prev[(size_t)k * nt + k]});
     for (int i = k + 1; i < nt; ++i)
       trsm[(size_t)i * nt + k] = add(kTrsm, i, k, k, i == k + 1 ? 2.f : 4.f, i == k + 1,
                                      {potrf[k], gemm_prev[(size_t)i * nt + k]});
-    ztrsm[k] = add(kZTrsm, nt, k, k, 3.f, false, {potrf[k], k > 0 ? zgemm[(size_t)k * nt + k - 1] : -1});
+    ztrsm[k] = add(kZTrsm, nt, k, k, 3.f, false, {potrf[k], k > 0 ? zgemm[(size_t)k * nt + k - 1] : genz[k]});
     for (int j = k + 1; j < nt; ++j)
       for (int i = j; i < nt; ++i) {
         const size_t ij = (size_t)i * nt + j;
@@ -575,7 +647,7 @@ void dag_plan(int nt, int nproc, std::vector<int4>& order) {
       }
     for (int j = k + 1; j < nt; ++j)
       zgemm[(size_t)j * nt + k] = add(kZGemm, nt, j, k, 3.f, false,
-                                      {ztrsm[k], trsm[(size_t)j * nt + k], k > 0 ? zgemm[(size_t)j * nt + k - 1] : -1});
+                                      {ztrsm[k], trsm[(size_t)j * nt + k], k > 0 ? zgemm[(size_t)j * nt + k - 1] : genz[j]});
   }
   const int N = (int)tk.size();
   std::vector<std::vector<int>> succ(N);
@@ -642,8 +714,8 @@ cudaError_t dag_init() {
 }
 
 void launch_dag_factor(const Layout& L, double* ws, const int4* tasks, int ntasks, int nt, int* sync, double* W,
-                       double* slots, int* info, double* out3, unsigned long long* trace, int nctas,
-                       cudaStream_t s) {
+                       double* slots, int* info, double* out3, unsigned long long* trace, const DagGen& gen,
+                       int nctas, cudaStream_t s) {
   DagArgs a;
   a.L = L;
   a.ws = ws;
@@ -656,6 +728,7 @@ void launch_dag_factor(const Layout& L, double* ws, const int4* tasks, int ntask
   a.info = info;
   a.out3 = out3;
   a.n = L.n;
+  a.gen = gen;
   a.trace = trace;
   // cooperative: every CTA is co-resident (the chain CTA and the pool wait on each other)
   cudaLaunchConfig_t cfg = {};
@@ -672,5 +745,13 @@ void launch_dag_factor(const Layout& L, double* ws, const int4* tasks, int ntask
 }
 
 const void* dag_factor_kernel_fn() { return (const void*)dag_factor_kernel; }
+
+bool dag_args_generate(const void* args) { return static_cast<const DagArgs*>(args)->gen.generate; }
+
+void dag_args_with_theta(const void* args, const MaternConsts& mc, std::vector<char>& out) {
+  out.resize(sizeof(DagArgs));
+  memcpy(out.data(), args, sizeof(DagArgs));
+  reinterpret_cast<DagArgs*>(out.data())->gen.mc = mc;
+}
 
 }  // namespace exageo

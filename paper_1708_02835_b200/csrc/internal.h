@@ -177,11 +177,24 @@ void launch_syrk_panels_2d(const Layout& L, double* ws, const double* const* sli
 // dag_sync_ints(nt) ints, zeroed before each launch; W holds nt 64 x 64 blocks. The last CTA to
 // finish writes out3 = {loglik, logdet, quad} (so no separate reduction kernels follow).
 void dag_plan(int nt, int nproc, std::vector<int4>& order);
+// Fused generation (Alg. 2 l.2): when generate is set, the executor's GEN tasks write Sigma's
+// tiles inside n and the z row (Eq. (2) with mc; tab = the K1T table for general nu) ahead of
+// the factorization; otherwise they only mark the tiles ready.
+struct DagGen {
+  bool generate;
+  MaternConsts mc;
+  const double* tab;
+  const double *x, *y, *z;
+};
+// CUDA-graph support: does a captured executor node generate, and its argument block with
+// a new theta (for cudaGraphExecKernelNodeSetParams).
+bool dag_args_generate(const void* args);
+void dag_args_with_theta(const void* args, const MaternConsts& mc, std::vector<char>& out);
 int dag_sync_ints(int nt);
 cudaError_t dag_init();
 void launch_dag_factor(const Layout& L, double* ws, const int4* tasks, int ntasks, int nt, int* sync, double* W,
-                       double* slots, int* info, double* out3, unsigned long long* trace, int nctas,
-                       cudaStream_t s);
+                       double* slots, int* info, double* out3, unsigned long long* trace, const DagGen& gen,
+                       int nctas, cudaStream_t s);
 const void* dag_factor_kernel_fn();
 
 // Factor the PB x PB diagonal block at `a` (ld) in place, write W = L^{-1} (PB x PB,

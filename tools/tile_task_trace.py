@@ -25,7 +25,7 @@ with ex.Context(device=0, tile_tasks=1, graphs=-1) as c:
     print(f"n={n} device {1e3 * r.info['ms_total']:.1f} us (chol {1e3 * r.info['ms_chol']:.1f} us)")
 rows = [list(map(int, l.split())) for l in open(path) if not l.startswith("#")]
 rows = [r for r in rows if r[8] > 0]
-names = {0: "POTRF", 1: "TRSM", 2: "GEMM", 3: "ZTRSM", 4: "ZGEMM"}
+names = {0: "POTRF", 1: "TRSM", 2: "GEMM", 3: "ZTRSM", 4: "ZGEMM", 5: "GEN"}
 nt = (n + 63) // 64
 ntasks = len([r for r in rows if r[0] < len(rows)]) if False else None
 chain_first = max(r[0] for r in rows) + 1 - 3 * nt  # chain records follow the ticket list
