@@ -464,7 +464,7 @@ exageo_status factor_tile_tasks(exageo_ctx* c) {
   const int nctas = 1 + std::min(c->dag_nproc - 1, std::max(c->dag_ntasks, 1));  // chain CTA + pool
   DagGen g{c->dag_gen, c->dag_mc, c->mtab, c->dag_x, c->dag_y, c->dag_z};
   launch_dag_factor(L, R.ws, c->dag_tasks, c->dag_ntasks, c->dag_nt, c->dag_sync, c->dag_W, R.slots, R.info,
-                    c->out3, c->dag_trace, g, nctas, c->stream);
+                    c->out3, c->dag_res, c->dag_trace, g, nctas, c->stream);
   c->kernels += 1;
   if (c->dag_gen) c->gen_launches += 1;
   c->dag_gen = false;  // one generation per launch_generate
@@ -843,14 +843,19 @@ exageo_status graph_body(exageo_ctx* c, const MaternConsts& mc, const double* x,
   exageo_status st = launch_generate(c, mc, x, y, z, true);
   if (st != EXAGEO_OK) return st;
   CUDA_TRY(c, record_timing(c, c->ev[1], c->stream));
-  if ((st = do_factor(c)) != EXAGEO_OK) return st;
+  c->dag_res = (double*)c->h_res;  // the executor writes the results straight into h_res
+  st = do_factor(c);
+  c->dag_res = nullptr;
+  if (st != EXAGEO_OK) return st;
   CUDA_TRY(c, record_timing(c, c->ev[2], c->stream));
   if ((st = launch_finish(c)) != EXAGEO_OK) return st;
   double* hd = (double*)c->h_res;
   int* hi = (int*)(hd + 4);
-  CUDA_TRY(c, cudaMemcpyAsync(hd, c->out3, 3 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-  for (size_t i = 0; i < c->rs.size(); ++i)
-    CUDA_TRY(c, cudaMemcpyAsync(hi + i, c->rs[i].info, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  if (!c->dag_finished) {
+    CUDA_TRY(c, cudaMemcpyAsync(hd, c->out3, 3 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    for (size_t i = 0; i < c->rs.size(); ++i)
+      CUDA_TRY(c, cudaMemcpyAsync(hi + i, c->rs[i].info, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  }
   CUDA_TRY(c, record_timing(c, c->ev[3], c->stream));
   return EXAGEO_OK;
 }

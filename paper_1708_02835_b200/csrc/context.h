@@ -94,6 +94,7 @@ struct exageo_ctx {
   bool dag_finished = false;   // the last factorization ran on the executor (out3 written by it)
   // fused generation: launch_generate defers Sigma's tiles inside n to the executor's GEN tasks
   bool dag_gen = false;        // the next executor launch generates (params below)
+  double* dag_res = nullptr;   // set during graph capture: pinned result block the executor writes
   exageo::MaternConsts dag_mc{};
   const double *dag_x = nullptr, *dag_y = nullptr, *dag_z = nullptr;
   std::vector<const void*> dag_init_key;  // (ws, n, nb) whose padding / z block was generated

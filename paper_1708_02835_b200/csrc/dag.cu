@@ -64,6 +64,7 @@ struct DagArgs {
   double* out3;   // {loglik, logdet, quad}, written by the last CTA to leave (Alg. 2 l.5-7)
   int64_t n;
   DagGen gen;
+  double* res_h;  // optional (CUDA-graph replays): {loglik, logdet, quad, -, info} in pinned host memory
   unsigned long long* trace;  // optional: per ticket {cta, grabbed, inputs ready, done} (ns)
 };
 
@@ -227,28 +228,52 @@ __device__ __forceinline__ void z_gemm(double* zj, int64_t ldzj, const double* y
 // theta1 on the diagonal (R9); thread: row 64 i + (tid & 63), 16 columns from 16 (tid >> 6).
 // The upper half of a diagonal tile gets the symmetric values (never read).
 template <int KIND>
-__device__ __forceinline__ void gen_tile_k(const DagArgs& a, double* T, int64_t ld, int i, int j, double* sm) {
+__device__ __forceinline__ double gen_value(const DagArgs& a, int64_t gr, int64_t gc, double xr, double yr, double xc,
+                                            double yc) {
   const MaternConsts& mc = a.gen.mc;
-  const int r = threadIdx.x & 63, cb = 16 * (threadIdx.x >> 6);
-  const int64_t gr = (int64_t)i * PB + r;
-  const bool rin = gr < a.n;
-  double* xc = sm;  // the tile's 64 column sites, loaded once
+  if (gr >= a.n || gc >= a.n) return gr == gc ? 1.0 : 0.0;
+  if (gr == gc) return mc.theta1;
+  return mat::matern_eval_k<KIND>(mat::dist2d(xr, yr, xc, yc, mc), mc, a.gen.tab);
+}
+
+// Off-diagonal tile: thread = row (tid & 63) x 16 columns from 16 (tid >> 6).
+// Diagonal tile: the lower triangle only (K2 never reads above the diagonal), balanced: rows
+// p and 63 - p hold 65 entries together; 8 threads share a pair (<= 9 entries each). The FP64
+// sqrt / exp of Eq. (2) bound a tile on one SM, and A_00 is on the critical path.
+template <int KIND>
+__device__ __forceinline__ void gen_tile_k(const DagArgs& a, double* T, int64_t ld, int i, int j, double* sm) {
+  double* xc = sm;  // the tile's 64 row and column sites, loaded once
   double* yc = sm + PB;
-  if (threadIdx.x < PB) {
-    const int64_t gc = (int64_t)j * PB + threadIdx.x;
-    xc[threadIdx.x] = gc < a.n ? a.gen.x[gc] : 0.0;
-    yc[threadIdx.x] = gc < a.n ? a.gen.y[gc] : 0.0;
+  double* xr = sm + 2 * PB;
+  double* yr = sm + 3 * PB;
+  if (threadIdx.x < 2 * PB) {
+    const int t = threadIdx.x & 63;
+    const int64_t g = (int64_t)(threadIdx.x < PB ? j : i) * PB + t;
+    const double xv = g < a.n ? a.gen.x[g] : 0.0, yv = g < a.n ? a.gen.y[g] : 0.0;
+    if (threadIdx.x < PB) {
+      xc[t] = xv;
+      yc[t] = yv;
+    } else {
+      xr[t] = xv;
+      yr[t] = yv;
+    }
   }
-  const double xr = rin ? a.gen.x[gr] : 0.0, yr = rin ? a.gen.y[gr] : 0.0;
   __syncthreads();
+  if (i != j) {
+    const int r = threadIdx.x & 63, cb = 16 * (threadIdx.x >> 6);
+    const int64_t gr = (int64_t)i * PB + r;
 #pragma unroll(KIND == 0 ? 1 : 4)  // closed forms: independent entries in flight together
-  for (int cc = 0; cc < 16; ++cc) {
-    const int64_t gc = (int64_t)j * PB + cb + cc;
-    double v;
-    if (!rin || gc >= a.n) v = gr == gc ? 1.0 : 0.0;
-    else if (gr == gc) v = mc.theta1;
-    else v = mat::matern_eval_k<KIND>(mat::dist2d(xr, yr, xc[cb + cc], yc[cb + cc], mc), mc, a.gen.tab);
-    T[(int64_t)(cb + cc) * ld + r] = v;
+    for (int cc = 0; cc < 16; ++cc) {
+      const int c = cb + cc;
+      T[(int64_t)c * ld + r] = gen_value<KIND>(a, gr, (int64_t)j * PB + c, xr[r], yr[r], xc[c], yc[c]);
+    }
+  } else {
+    const int p = threadIdx.x >> 3, sub = threadIdx.x & 7;
+#pragma unroll(KIND == 0 ? 1 : 3)
+    for (int q = sub; q < 65; q += 8) {
+      const int r = q <= p ? p : 63 - p, c = q <= p ? q : q - p - 1;
+      T[(int64_t)c * ld + r] = gen_value<KIND>(a, (int64_t)i * PB + r, (int64_t)j * PB + c, xr[r], yr[r], xc[c], yc[c]);
+    }
   }
 }
 __device__ __forceinline__ void gen_tile(const DagArgs& a, double* T, int64_t ld, int i, int j, double* sm) {
@@ -363,15 +388,20 @@ __device__ void chain_cta(const DagArgs& a, int* st, double* sm) {
     }
   };
   for (int i = a.nt + threadIdx.x; i < a.L.owned() * nsub; i += 256) a.slots[i] = 0.0;  // padding blocks
-  {  // A_00 (after its GEN task) into the K2 body's input block; later blocks come from SYRK
-    if (threadIdx.x == 0) s_ok = wait_ge(stf(0, 0), 1, a.info);
-    __syncthreads();
-    if (!s_ok) return;
+  const unsigned long long t_entry = a.trace ? gtimer() : 0;
+  {  // A_00 into the K2 body's input block (GEN(0, 0) is the chain's own task: generated straight
+     // into shared memory, or read when generate.cu already wrote it); later blocks come from SYRK
     int64_t ld0;
-    stage_tile(sm, tile_ptr(a, 0, 0, ld0), ld0);
-    asm volatile("cp.async.wait_all;\n" ::: "memory");
+    double* A00 = tile_ptr(a, 0, 0, ld0);
+    if (a.gen.generate) {
+      gen_tile(a, sm, LDA2, 0, 0, X);
+    } else {
+      stage_tile(sm, A00, ld0);
+      asm volatile("cp.async.wait_all;\n" ::: "memory");
+    }
     __syncthreads();
   }
+  rec(3 * (a.nt - 1) + 1, t_entry, t_entry);  // (the last step has no TRSM): kernel entry .. A_00 ready
   for (int k = 0; k < a.nt; ++k) {
     const bool last = k + 1 == a.nt;
     int64_t ld, ldb = 0, ldd = 0;
@@ -477,9 +507,17 @@ __device__ void finish_tail(const DagArgs& a, double* red) {
       q += red[8 + w];
     }
     const double logdet = 2.0 * ld2;
-    a.out3[0] = -0.5 * q - 0.5 * logdet - 0.5 * (double)a.n * 1.8378770664093454835606594728112;
+    const double ll = -0.5 * q - 0.5 * logdet - 0.5 * (double)a.n * 1.8378770664093454835606594728112;
+    a.out3[0] = ll;
     a.out3[1] = logdet;
     a.out3[2] = q;
+    if (a.res_h) {  // straight into the caller's pinned result block (no copy nodes)
+      a.res_h[0] = ll;
+      a.res_h[1] = logdet;
+      a.res_h[2] = q;
+      reinterpret_cast<int*>(a.res_h + 4)[0] = *(volatile int*)a.info;
+      __threadfence_system();
+    }
   }
   // every other CTA has left: zero the counters this launch used, ready for the next one
   // (no memset node before each launch)
@@ -628,8 +666,9 @@ void dag_plan(int nt, int nproc, std::vector<int4>& order) {
     return (int)tk.size() - 1;
   };
   std::vector<int> genz(nt);
-  for (int j = 0; j < nt; ++j) {  // GEN tasks: Sigma's tiles inside n and the z row (Alg. 2 l.2)
-    for (int i = j; i < nt; ++i) gemm_prev[(size_t)i * nt + j] = add(kGen, i, j, 0, 1.5f, false, {});
+  for (int j = 0; j < nt; ++j) {  // GEN tasks: Sigma's tiles inside n and the z row (Alg. 2 l.2);
+    // GEN(0, 0) belongs to the chain CTA (it generates A_00 into its shared memory)
+    for (int i = j; i < nt; ++i) gemm_prev[(size_t)i * nt + j] = add(kGen, i, j, 0, 1.5f, i == 0, {});
     genz[j] = add(kGen, nt, j, 0, 0.5f, false, {});
   }
   for (int k = 0; k < nt; ++k) {
@@ -714,8 +753,8 @@ cudaError_t dag_init() {
 }
 
 void launch_dag_factor(const Layout& L, double* ws, const int4* tasks, int ntasks, int nt, int* sync, double* W,
-                       double* slots, int* info, double* out3, unsigned long long* trace, const DagGen& gen,
-                       int nctas, cudaStream_t s) {
+                       double* slots, int* info, double* out3, double* res_h, unsigned long long* trace,
+                       const DagGen& gen, int nctas, cudaStream_t s) {
   DagArgs a;
   a.L = L;
   a.ws = ws;
@@ -729,6 +768,7 @@ void launch_dag_factor(const Layout& L, double* ws, const int4* tasks, int ntask
   a.out3 = out3;
   a.n = L.n;
   a.gen = gen;
+  a.res_h = res_h;
   a.trace = trace;
   // cooperative: every CTA is co-resident (the chain CTA and the pool wait on each other)
   cudaLaunchConfig_t cfg = {};

@@ -193,8 +193,8 @@ void dag_args_with_theta(const void* args, const MaternConsts& mc, std::vector<c
 int dag_sync_ints(int nt);
 cudaError_t dag_init();
 void launch_dag_factor(const Layout& L, double* ws, const int4* tasks, int ntasks, int nt, int* sync, double* W,
-                       double* slots, int* info, double* out3, unsigned long long* trace, const DagGen& gen,
-                       int nctas, cudaStream_t s);
+                       double* slots, int* info, double* out3, double* res_h, unsigned long long* trace,
+                       const DagGen& gen, int nctas, cudaStream_t s);
 const void* dag_factor_kernel_fn();
 
 // Factor the PB x PB diagonal block at `a` (ld) in place, write W = L^{-1} (PB x PB,
