@@ -1013,6 +1013,24 @@ exageo_status loglik_device(exageo_ctx* c, const exageo_theta* t, int64_t n, con
       tr += ms;
     }
     info->ms_trailing = tr;
+    // tracing (env EXAGEO_U2_TRACE=<file>): each bulk trailing update's [start, end] in ms from
+    // the start of the factorization, appended per evaluation -- the gaps between them are
+    // the panel chain's stalls
+    if (const char* tp = getenv("EXAGEO_U2_TRACE")) {
+      if (FILE* f = fopen(tp, "a")) {
+        fprintf(f, "# n=%lld nb=%d steps=%d\n", (long long)c->G.n, c->G.nb, R.n_u2);
+        for (int i = 0; i < R.n_u2; ++i) {
+          float b = 0.f, e = 0.f;
+          cudaEventElapsedTime(&b, c->ev[1], R.u2b[i]);
+          cudaEventElapsedTime(&e, c->ev[1], R.u2e[i]);
+          fprintf(f, "%d %.4f %.4f\n", i, b, e);
+        }
+        float end = 0.f;
+        cudaEventElapsedTime(&end, c->ev[1], c->ev[2]);
+        fprintf(f, "end %.4f\n", end);
+        fclose(f);
+      }
+    }
   }
   return st;
 }

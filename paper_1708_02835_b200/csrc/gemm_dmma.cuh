@@ -174,7 +174,12 @@ struct SyrkMap {
     t.K = L.nb;
     t.m_valid = BM;
     t.n_valid = BN;
-    return gr + BM > gc;  // false: the tile lies strictly above the diagonal (skip it)
+    // skipped (false): tiles strictly above the diagonal; tiles of the identity padding (all
+    // rows or all columns >= n: their rows of panel k are zero, so the update is a no-op, R12);
+    // z-block tiles below its first BM rows (zero rows: only row N, the z row, is live)
+    if (gr + BM <= gc) return false;
+    if (gc >= L.n || (gr < L.N && gr >= L.n)) return false;
+    return gr < L.N + BM;
   }
   __host__ int64_t blocks(int BM, int BN) const {
     if (npan <= 0) return 0;
