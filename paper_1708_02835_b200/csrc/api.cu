@@ -269,13 +269,32 @@ bool tile_tasks_eligible(const exageo_ctx* c, int64_t n) {
   return c->tile_tasks > 0 || n <= kTileTasksAutoN;
 }
 
-// Plan (host list schedule, cached by nt and the CTA count) and buffers for the current layout.
-exageo_status prepare_tile_tasks(exageo_ctx* c) {
+// Tail hand-off: when the stream schedule runs a single-rank factorization, its last panels
+// (trailing size <= kTailN) are bound by the panel chain -- each step's trailing update is
+// shorter than F(k+1) -- so the executor factors that trailing matrix instead. Returns the
+// first panel it takes (0: no hand-off). EXAGEO_TAIL_N overrides the size (0 disables).
+int tail_stop(const exageo_ctx* c, const Layout& G) {
+  if (c->tile_tasks < 0 || c->world > 1 || c->virt || c->ind > 0 || c->comm) return 0;
+  if (tile_tasks_eligible(c, G.n)) return 0;  // the executor runs the whole factorization
+  static const int64_t tail_n = [] {
+    const char* e = getenv("EXAGEO_TAIL_N");
+    return e ? (int64_t)atoll(e) : (int64_t)2560;
+  }();
+  if (tail_n <= 0) return 0;
+  int k = (int)((G.n - tail_n + G.nb - 1) / G.nb);  // first panel whose trailing size <= tail_n
+  if (k < 1) k = 1;
+  return k < G.T ? k : 0;
+}
+
+// Plan (host list schedule, cached by nt and the CTA count) and buffers for the executor run
+// of this layout: the whole matrix (t0 = 0) or the trailing matrix from 64-block column t0.
+exageo_status prepare_tile_tasks(exageo_ctx* c, int t0 = 0) {
   const Layout& G = c->G;
-  const int nt = (int)((G.n + PB - 1) / PB);
+  const int nt = (int)((G.n + PB - 1) / PB) - t0;
+  c->dag_t0 = t0;
   int nsm = 0;
   CUDA_TRY(c, cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device));
-  if (c->dag_nt != nt || c->dag_nproc != nsm) {
+  if (c->dag_nt != nt || c->dag_nproc != nsm || c->dag_plan_t0 != t0) {
     std::vector<int4> order;
     dag_plan(nt, nsm, order);
     if ((int64_t)order.size() > c->dag_cap_tasks) {
@@ -297,6 +316,7 @@ exageo_status prepare_tile_tasks(exageo_ctx* c) {
     c->dag_ntasks = (int)order.size();
     c->dag_nt = nt;
     c->dag_nproc = nsm;
+    c->dag_plan_t0 = t0;
   }
   if (c->dag_cap_nt < nt) {
     cudaFree(c->dag_sync);
@@ -328,6 +348,7 @@ exageo_status prepare_generate(exageo_ctx* c, const exageo_theta* t, int64_t n, 
   exageo_status st = ensure_buffers(c);
   if (st != EXAGEO_OK) return st;
   // the tile-task plan and buffers exist before any launch (and outside graph capture)
+  if (const int ks = tail_stop(c, c->G)) return prepare_tile_tasks(c, ks * (nb / PB));
   if (!tile_tasks_eligible(c, n)) return EXAGEO_OK;
   if ((st = prepare_tile_tasks(c)) != EXAGEO_OK) return st;
   // the executor generates only the tiles inside n; the rest of the layout (identity padding,
@@ -454,16 +475,18 @@ void dump_tile_task_trace(exageo_ctx* c) {
 }
 
 exageo_status factor_tile_tasks(exageo_ctx* c) {
-  if (c->dag_nt != (int)((c->G.n + PB - 1) / PB) || c->dag_cap_nt < c->dag_nt)
+  if (c->dag_nt != (int)((c->G.n + PB - 1) / PB) - c->dag_t0 || c->dag_cap_nt < c->dag_nt)
     return fail(c, EXAGEO_EINVAL, "tile-task plan missing (prepare_generate)");
   RankState& R = c->rs[0];
   const Layout& L = R.L;
   // the counters are zero: set at allocation, reset by the last CTA of every launch
-  R.n_u2 = 0;
-  R.u2_flops = 0.0;
+  if (c->dag_t0 == 0) {
+    R.n_u2 = 0;
+    R.u2_flops = 0.0;
+  }
   const int nctas = 1 + std::min(c->dag_nproc - 1, std::max(c->dag_ntasks, 1));  // chain CTA + pool
   DagGen g{c->dag_gen, c->dag_mc, c->mtab, c->dag_x, c->dag_y, c->dag_z};
-  launch_dag_factor(L, R.ws, c->dag_tasks, c->dag_ntasks, c->dag_nt, c->dag_sync, c->dag_W, R.slots, R.info,
+  launch_dag_factor(L, R.ws, c->dag_tasks, c->dag_ntasks, c->dag_nt, c->dag_t0, c->dag_sync, c->dag_W, R.slots, R.info,
                     c->out3, c->dag_res, c->dag_trace, g, nctas, c->stream);
   c->kernels += 1;
   if (c->dag_gen) c->gen_launches += 1;
@@ -667,6 +690,7 @@ exageo_status do_factor(exageo_ctx* c) {
   const Layout& G = c->G;
   if (tile_tasks_eligible(c, G.n)) return factor_tile_tasks(c);
   c->dag_finished = false;
+  const int kstop = tail_stop(c, G);  // > 0: panels >= kstop go to the executor
   CUDA_TRY(c, cudaEventRecord(c->ev_fork, c->stream));
   for (auto& R : c->rs) {
     for (cudaStream_t s : {R.s_la, R.s_main, R.s_comm}) CUDA_TRY(c, cudaStreamWaitEvent(s, c->ev_fork, 0));
@@ -680,7 +704,7 @@ exageo_status do_factor(exageo_ctx* c) {
       CUDA_TRY(c, cudaEventRecord(R.ev_F, R.s_la));
     }
   if ((st = exchange_panel(c, 0)) != EXAGEO_OK) return st;
-  for (int k = 0; k + 1 < G.T; ++k) {
+  for (int k = 0; k + 1 < (kstop > 0 ? kstop + 1 : G.T); ++k) {
     for (auto& R : c->rs) {
       const Layout& L = R.L;
       const double* sl[kMaxP];
@@ -688,7 +712,8 @@ exageo_status do_factor(exageo_ctx* c) {
       panel_slices(R, k, sl, sld);
       // panel k's operands: the rank's own factored panel (1-D owner) or the exchange
       cudaEvent_t avail = (L.P == 1 && L.owns(k)) ? R.ev_F : R.ev_recv[k & 1];
-      const bool owns_next = L.owns(k + 1);
+      // at the hand-off step the bulk update also covers panel k + 1 (no U1 / F(k + 1))
+      const bool owns_next = L.owns(k + 1) && k + 1 != kstop;
       // U2(k) needs panel k: wait now, before ev_F is re-recorded for F(k+1) below
       CUDA_TRY(c, cudaStreamWaitEvent(R.s_main, avail, 0));
       if (owns_next) {
@@ -736,6 +761,11 @@ exageo_status do_factor(exageo_ctx* c) {
     CUDA_TRY(c, cudaEventRecord(R.ev_join[1], R.s_main));
     CUDA_TRY(c, cudaEventRecord(R.ev_join[2], R.s_comm));
     for (auto& ev : R.ev_join) CUDA_TRY(c, cudaStreamWaitEvent(c->stream, ev, 0));
+  }
+  if (kstop > 0) {  // the trailing matrix from panel kstop on: one executor launch (dag.cu)
+    st = check_launch(c);
+    if (st != EXAGEO_OK) return st;
+    return factor_tile_tasks(c);
   }
   return check_launch(c);
 }

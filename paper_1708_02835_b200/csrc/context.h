@@ -86,6 +86,7 @@ struct exageo_ctx {
   // single-rank context as one persistent kernel running the 64 x 64 tile DAG
   int tile_tasks = 0;          // 0 automatic (n <= kTileTasksAutoN), 1 always when eligible, -1 never
   int dag_nt = 0, dag_ntasks = 0, dag_nproc = 0;  // plan of the uploaded task list
+  int dag_t0 = 0, dag_plan_t0 = -1;  // first 64-block column of the executor run (tail hand-off)
   int4* dag_tasks = nullptr;
   int* dag_sync = nullptr;     // ticket + tile / z version counters
   double* dag_W = nullptr;     // W_k = L_kk^{-1}, 64 x 64 per tile column

@@ -56,7 +56,9 @@ struct DagArgs {
   double* ws;
   const int4* tasks;  // {type, i, j, k} in ticket order
   int ntasks;
-  int nt;             // tile columns inside n: ceil(n / 64)
+  int nt;             // tile columns the executor factors: ceil(n / 64) - t0
+  int t0;             // first of them (0: the whole matrix; > 0: the trailing matrix the stream
+                      // schedule hands over, already updated by panels < t0, not generated)
   int* sync;          // [0] ticket; [kSyncHead ..] st(i, j) at i * nt + j; then z(j)
   double* W;          // nt blocks of 64 x 64: W_k = L_kk^{-1}
   double* slots;      // log-det partials, one per 64-block column (panel p, sub-block sb)
@@ -84,12 +86,15 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 
 // Tile (i, j) (64-row / 64-column units) of the single-rank panel layout and its ld.
 __device__ __forceinline__ double* tile_ptr(const DagArgs& a, int i, int j, int64_t& ld) {
+  i += a.t0;  // task indices are relative to the first tile column the executor factors
+  j += a.t0;
   const int nsub = a.L.nb / PB, p = j / nsub, cb = (j % nsub) * PB;
   ld = a.L.ld(p);
   return a.ws + a.L.off(p) + (int64_t)cb * ld + ((int64_t)i * PB - (int64_t)p * a.L.nb);
 }
 // z row segment of column block j (entry t at ptr[t * ld]).
 __device__ __forceinline__ double* zseg_ptr(const DagArgs& a, int j, int64_t& ld) {
+  j += a.t0;
   const int nsub = a.L.nb / PB, p = j / nsub, cb = (j % nsub) * PB;
   ld = a.L.ld(p);
   return a.ws + a.L.off(p) + (int64_t)cb * ld + a.L.lrows(p);
@@ -387,14 +392,14 @@ __device__ void chain_cta(const DagArgs& a, int* st, double* sm) {
       r[3] = gtimer();
     }
   };
-  for (int i = a.nt + threadIdx.x; i < a.L.owned() * nsub; i += 256) a.slots[i] = 0.0;  // padding blocks
+  for (int i = a.t0 + a.nt + threadIdx.x; i < a.L.owned() * nsub; i += 256) a.slots[i] = 0.0;  // padding
   const unsigned long long t_entry = a.trace ? gtimer() : 0;
   {  // A_00 into the K2 body's input block (GEN(0, 0) is the chain's own task: generated straight
      // into shared memory, or read when generate.cu already wrote it); later blocks come from SYRK
     int64_t ld0;
     double* A00 = tile_ptr(a, 0, 0, ld0);
     if (a.gen.generate) {
-      gen_tile(a, sm, LDA2, 0, 0, X);
+      gen_tile(a, sm, LDA2, a.t0, a.t0, X);
     } else {
       stage_tile(sm, A00, ld0);
       asm volatile("cp.async.wait_all;\n" ::: "memory");
@@ -415,10 +420,11 @@ __device__ void chain_cta(const DagArgs& a, int* st, double* sm) {
     ChainPrefetch hook{last ? nullptr : stf(k + 1, k), last ? nullptr : stf(k + 1, k + 1), k + 1, X, Ab, ldb, Y, Ad, ldd,
                        &s_issued, hst};
     double* Wk = a.W + (size_t)k * PB * PB;
-    double* slot = a.slots + (k / nsub) * nsub + k % nsub;
-    const int64_t ncols = a.n - (int64_t)k * PB;  // ragged last block: only its real strips
+    const int gk = a.t0 + k;  // global 64-block column
+    double* slot = a.slots + gk;  // one log-det slot per 64-block column (panel gk / nsub, block gk % nsub)
+    const int64_t ncols = a.n - (int64_t)gk * PB;  // ragged last block: only its real strips
     const int nstrips = ncols >= PB ? 4 : (int)(ncols + 15) / 16;
-    const bool ok = potrf64_body<true>(Akk, ld, Wk, slot, a.info, (int64_t)k * PB, sm, hook, nstrips);
+    const bool ok = potrf64_body<true>(Akk, ld, Wk, slot, a.info, (int64_t)gk * PB, sm, hook, nstrips);
     if (!ok) {
       asm volatile("cp.async.wait_all;\n" ::: "memory");
       return;
@@ -604,12 +610,12 @@ __device__ void pool_cta(const DagArgs& a, int* st, int* zs, double* sm) {
       case kGen: {
         if (i < a.nt) {
           double* T = tile_ptr(a, i, j, ld);
-          if (a.gen.generate) gen_tile(a, T, ld, i, j, sm);
+          if (a.gen.generate) gen_tile(a, T, ld, i + a.t0, j + a.t0, sm);
           flag = st + (i * a.nt + j) * kPad;
         } else {
           double* zj = zseg_ptr(a, j, ld);
           if (a.gen.generate && threadIdx.x < PB) {
-            const int64_t c = (int64_t)j * PB + threadIdx.x;
+            const int64_t c = (int64_t)(j + a.t0) * PB + threadIdx.x;
             zj[(int64_t)threadIdx.x * ld] = (c < a.n && a.gen.z) ? a.gen.z[c] : 0.0;  // simulate: no z
           }
           flag = zs + j * kPad;
@@ -752,7 +758,7 @@ cudaError_t dag_init() {
                               kDagSmemDoubles * (int)sizeof(double));
 }
 
-void launch_dag_factor(const Layout& L, double* ws, const int4* tasks, int ntasks, int nt, int* sync, double* W,
+void launch_dag_factor(const Layout& L, double* ws, const int4* tasks, int ntasks, int nt, int t0, int* sync, double* W,
                        double* slots, int* info, double* out3, double* res_h, unsigned long long* trace,
                        const DagGen& gen, int nctas, cudaStream_t s) {
   DagArgs a;
@@ -761,6 +767,7 @@ void launch_dag_factor(const Layout& L, double* ws, const int4* tasks, int ntask
   a.tasks = tasks;
   a.ntasks = ntasks;
   a.nt = nt;
+  a.t0 = t0;
   a.sync = sync;
   a.W = W;
   a.slots = slots;

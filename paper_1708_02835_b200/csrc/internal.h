@@ -172,7 +172,9 @@ void launch_syrk_panels(const Layout& L, double* ws, const double* Pk, int k, in
 void launch_syrk_panels_2d(const Layout& L, double* ws, const double* const* slices, const int64_t* slds, int k,
                            int J0, int npan, const int* info, cudaStream_t s);
 // Tile-task executor (dag.cu): the factorization (with the fused forward solve) of a
-// single-rank layout as one persistent kernel over the 64 x 64 tile DAG. dag_plan lists the
+// single-rank layout as one persistent kernel over the 64 x 64 tile DAG -- the whole matrix
+// (t0 = 0), or the trailing matrix from 64-block column t0 on, handed over by the stream
+// schedule after the panels < t0 (already applied to it; no generation then). dag_plan lists the
 // tasks of nt = ceil(n / 64) tile columns in ticket order for nproc CTAs; sync holds
 // dag_sync_ints(nt) ints, zeroed before each launch; W holds nt 64 x 64 blocks. The last CTA to
 // finish writes out3 = {loglik, logdet, quad} (so no separate reduction kernels follow).
@@ -192,7 +194,7 @@ bool dag_args_generate(const void* args);
 void dag_args_with_theta(const void* args, const MaternConsts& mc, std::vector<char>& out);
 int dag_sync_ints(int nt);
 cudaError_t dag_init();
-void launch_dag_factor(const Layout& L, double* ws, const int4* tasks, int ntasks, int nt, int* sync, double* W,
+void launch_dag_factor(const Layout& L, double* ws, const int4* tasks, int ntasks, int nt, int t0, int* sync, double* W,
                        double* slots, int* info, double* out3, double* res_h, unsigned long long* trace,
                        const DagGen& gen, int nctas, cudaStream_t s);
 const void* dag_factor_kernel_fn();

@@ -115,3 +115,39 @@ def test_tile_tasks_predict_and_simulate():
     np.testing.assert_allclose(z, z_ref, rtol=1e-10, atol=1e-11)
     zp_ref = oracle.predict(x[:n], y[:n], z, x[n:], y[n:], theta)
     np.testing.assert_allclose(zp, zp_ref, rtol=1e-9, atol=1e-10)
+
+
+@pytest.mark.parametrize("n,nb", [(3300, 128), (4100, 256), (7000, 256), (12500, 384)])
+def test_tail_handoff_matches_stream_schedule(n, nb):
+    """Above the executor's own range the stream schedule hands the last panels (trailing size
+    <= 2560) to the executor (t0 > 0, no generation): same l, factor and y as the pure stream
+    schedule (tile_tasks=-1) to rounding."""
+    x, y = ex.gen_locations(n, 15)
+    z = si.normals(n, 16)
+    theta = (1.0, 0.1, 0.5)
+    rows = np.random.default_rng(n).integers(0, n, 500)
+    rows[:100] = n - 1 - np.arange(100)  # the handed-over trailing corner
+    cols = np.minimum(rows, np.random.default_rng(n + 1).integers(0, n, 500))
+    out = {}
+    for tt in (0, -1):
+        with ex.Context(device=0, nb=nb, tile_tasks=tt, graphs=-1) as c:
+            r = c.loglik(x, y, z, theta)
+            out[tt] = (r, c.read_entries(rows, cols), c.read_zrow(n))
+    (a, la, ya), (b, lb, yb) = out[0], out[-1]
+    assert a.info["kernels"] < b.info["kernels"]  # the tail ran as one launch
+    assert abs(a.loglik - b.loglik) <= 1e-11 * abs(b.loglik)
+    assert a.logdet == pytest.approx(b.logdet, rel=1e-12) and a.quad == pytest.approx(b.quad, rel=1e-11)
+    np.testing.assert_allclose(la, lb, rtol=1e-11, atol=1e-13)
+    np.testing.assert_allclose(ya, yb, rtol=1e-9, atol=1e-11)
+
+
+def test_tail_handoff_matches_oracle():
+    n = 3600
+    x, y = ex.gen_locations(n, 17)
+    z = oracle.simulate(x, y, (1.0, 0.1, 0.5), si.normals(n, 18))
+    theta = (1.0, 0.1, 0.9)
+    with ex.Context(device=0, nb=128) as c:  # graphs and the hand-off: the default path at this n
+        r = c.loglik(x, y, z, theta)
+        r2 = c.loglik(x, y, z, theta)
+    assert r.loglik == r2.loglik
+    assert_ll(r.loglik, oracle.loglik(x, y, z, theta), n)
