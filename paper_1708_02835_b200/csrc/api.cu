@@ -70,9 +70,8 @@ bool theta_ok(const exageo_theta* t) {
 // loses at 70/80k by 0.3-0.6%; the differences near the other switches are 1-4%)
 int auto_nb(int64_t n, int world = 1) {
   if (n >= 48000) return world > 1 ? 512 : 1024;  // distributed: more panels balance the ranks
-  if (n >= 21000) return 512;
-  if (n >= 15000) return 384;
-  if (n >= 12000) return 256;
+  if (n >= 14000) return 512;  // round-2 sweep (tail hand-off, padding-tile skip): 16k/20k best
+  if (n >= 6000) return 256;   // 8192 / 10k: 256 best
   return 128;
 }
 

@@ -20,7 +20,6 @@ cudaError_t gemm_init() {
   if ((e = set_smem<PanelCfg, true, DenseMap>()) != cudaSuccess) return e;
   if ((e = set_smem<PanelCfg, false, DenseMap>()) != cudaSuccess) return e;
   if ((e = set_smem<TrailCfg, true, SyrkMap>()) != cudaSuccess) return e;
-  if ((e = set_smem_persist<TrailCfg, SyrkMap>()) != cudaSuccess) return e;
   return set_smem<TrailCfg, true, Syrk2DMap>();
 }
 
@@ -57,20 +56,6 @@ int syrk_group(int nb) {
   return (int)(g < 1 ? 1 : (g > 8 ? 8 : g));
 }
 
-// Persistent trailing update (gemm_nt_dmma_persist): CTAs to launch, SMs x 4 (TrailCfg's
-// occupancy); EXAGEO_U2_PERSIST=0 selects the one-tile-per-CTA kernel (tuning).
-int persist_ctas() {
-  static const int v = [] {
-    const char* e = getenv("EXAGEO_U2_PERSIST");
-    if (e && atoi(e) == 0) return 0;
-    int dev = 0, nsm = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    return nsm * TrailCfg::MINB;
-  }();
-  return v;
-}
-
 void launch_syrk_panels(const Layout& L, double* ws, const double* Pk, int k, int J0, int npan, const int* info,
                         cudaStream_t s) {
   if (npan <= 0) return;
@@ -83,8 +68,7 @@ void launch_syrk_panels(const Layout& L, double* ws, const double* Pk, int k, in
   map.npan = npan;
   map.row_end = (int64_t)L.sb_end(k) * L.nb;  // N unless IND
   map.group = L.world == 1 ? syrk_group(L.nb) : 1;  // super panels: panel k's rows read once per group
-  if (persist_ctas() > 0) launch_persist<TrailCfg, SyrkMap>(map, info, s, persist_ctas());
-  else launch<TrailCfg, true, SyrkMap, true>(map, info, s);
+  launch<TrailCfg, true, SyrkMap, true>(map, info, s);
 }
 
 void launch_syrk_panels_2d(const Layout& L, double* ws, const double* const* slices, const int64_t* slds, int k,

@@ -383,123 +383,6 @@ __global__ void __launch_bounds__(C::NT, C::MINB) gemm_nt_dmma(Map map, const in
   }
 }
 
-// Persistent form of gemm_nt_dmma<C, true, Map, PRE = true> (C -= A B^T, accumulators
-// preloaded from C) with STAGES = 2: each CTA walks tiles blockIdx.x, + gridDim.x, ... and the
-// cp.async ring runs on across tile boundaries -- the next tile's first K slice is loaded
-// during the current tile's last one and its C block is pulled into L2 half-way through --
-// so a tile change costs the epilogue stores and an L2-latency accumulator reload instead of
-// a cold prologue (HBM latency of C plus the pipeline fill) per tile. Skipped tiles (Map
-// returns false) cost only their index arithmetic.
-template <class Map, int BM, int BN>
-__device__ __forceinline__ bool next_valid_tile(const Map& map, int64_t& bid, int64_t nblk, GemmTile& t) {
-  for (; bid < nblk; bid += gridDim.x)
-    if (map.template operator()<BM, BN>(bid, t)) return true;
-  return false;
-}
-
-template <class C, class Map>
-__global__ void __launch_bounds__(C::NT, C::MINB) gemm_nt_dmma_persist(Map map, int64_t nblk,
-                                                                       const int* __restrict__ info) {
-  constexpr int BM = C::BM, BN = C::BN, BK = C::BK, NT = C::NT;
-  constexpr int LDA_S = C::LDA_S, LDB_S = C::LDB_S;
-  constexpr int WM = BM / C::WARPS_M, WN = BN / C::WARPS_N;
-  constexpr int MI = WM / 8, NI = WN / 8;
-  static_assert(C::STAGES == 2, "persistent ring: two stages");
-  asm volatile("griddepcontrol.wait;\n" ::: "memory");
-  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
-  extern __shared__ __align__(16) double smem[];
-  double* sA = smem;
-  double* sB = smem + 2 * BK * LDA_S;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = warp % C::WARPS_M, wn = warp / C::WARPS_M;
-  const int fr = lane >> 2, fk = lane & 3;
-
-  auto load_stage = [&](int slot, const GemmTile& g, int kt) {
-    double* a_s = sA + slot * BK * LDA_S;
-    double* b_s = sB + slot * BK * LDB_S;
-    constexpr int CA = BK * BM / 2;
-#pragma unroll
-    for (int c = tid; c < CA; c += NT) {
-      const int col = c / (BM / 2), row = (c % (BM / 2)) * 2;
-      cp_async16(a_s + col * LDA_S + row, g.A + (int64_t)(kt * BK + col) * g.lda + row);
-    }
-    constexpr int CB = BK * BN / 2;
-#pragma unroll
-    for (int c = tid; c < CB; c += NT) {
-      const int col = c / (BN / 2), row = (c % (BN / 2)) * 2;
-      cp_async16(b_s + col * LDB_S + row, g.B + (int64_t)(kt * BK + col) * g.ldb + row);
-    }
-  };
-  auto load_acc = [&](double (&acc)[MI][NI][2], const GemmTile& g) {
-#pragma unroll
-    for (int i = 0; i < MI; ++i)
-#pragma unroll
-      for (int j = 0; j < NI; ++j)
-#pragma unroll
-        for (int e = 0; e < 2; ++e)
-          acc[i][j][e] = g.C[(int64_t)(wn * WN + j * 8 + fk * 2 + e) * g.ldc + wm * WM + i * 8 + fr];
-  };
-
-  int64_t bid = blockIdx.x;
-  GemmTile t, tn;
-  if (!next_valid_tile<Map, BM, BN>(map, bid, nblk, t)) return;
-  int64_t bidn = bid + gridDim.x;
-  bool haven = next_valid_tile<Map, BM, BN>(map, bidn, nblk, tn);
-  load_stage(0, t, 0);
-  cp_async_commit();
-  if (info != nullptr && *(volatile const int*)info != 0) {  // failed pivot upstream: nothing to do
-    cp_async_wait<0>();
-    return;
-  }
-  double acc[MI][NI][2];
-  load_acc(acc, t);
-  int g = 0;  // running K-slice counter across tiles: ring slot g & 1
-  for (;;) {
-    const int KT = t.K / BK;
-    for (int kt = 0; kt < KT; ++kt, ++g) {
-      cp_async_wait<0>();
-      __syncthreads();  // slice g landed; every warp is done with slice g - 1's slot
-      if (kt + 1 < KT) load_stage((g + 1) & 1, t, kt + 1);
-      else if (haven) load_stage((g + 1) & 1, tn, 0);
-      cp_async_commit();
-      if (haven && kt == KT / 2) {  // the next tile's C block into L2 for its accumulator reload
-        constexpr int LPC = BM / 16;
-        for (int l = tid; l < BN * LPC; l += NT) {
-          const double* p = tn.C + (int64_t)(l / LPC) * tn.ldc + (l % LPC) * 16;
-          asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p));
-        }
-      }
-      const double* a_s = sA + (g & 1) * BK * LDA_S + wm * WM + fr;
-      const double* b_s = sB + (g & 1) * BK * LDB_S + wn * WN + fr;
-#pragma unroll
-      for (int kk = 0; kk < BK; kk += 4) {
-        double af[MI], bf[NI];
-#pragma unroll
-        for (int i = 0; i < MI; ++i) af[i] = -a_s[(kk + fk) * LDA_S + i * 8];
-#pragma unroll
-        for (int j = 0; j < NI; ++j) bf[j] = b_s[(kk + fk) * LDB_S + j * 8];
-#pragma unroll
-        for (int i = 0; i < MI; ++i)
-#pragma unroll
-          for (int j = 0; j < NI; ++j) dmma(acc[i][j], af[i], bf[j]);
-      }
-    }
-#pragma unroll
-    for (int i = 0; i < MI; ++i)
-#pragma unroll
-      for (int j = 0; j < NI; ++j)
-#pragma unroll
-        for (int e = 0; e < 2; ++e)
-          t.C[(int64_t)(wn * WN + j * 8 + fk * 2 + e) * t.ldc + wm * WM + i * 8 + fr] = acc[i][j][e];
-    if (!haven) break;
-    t = tn;
-    load_acc(acc, t);
-    bidn += gridDim.x;
-    haven = next_valid_tile<Map, BM, BN>(map, bidn, nblk, tn);
-  }
-  cp_async_wait<0>();
-}
-
 template <class C, bool ACC, class Map>
 cudaError_t set_smem() {
   cudaError_t e =
@@ -507,20 +390,6 @@ cudaError_t set_smem() {
   if (e != cudaSuccess) return e;
   return cudaFuncSetAttribute(gemm_nt_dmma<C, ACC, Map, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               C::SMEM);
-}
-
-template <class C, class Map>
-cudaError_t set_smem_persist() {
-  return cudaFuncSetAttribute(gemm_nt_dmma_persist<C, Map>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-}
-
-// ctas: resident CTAs to launch (SMs x CTAs per SM); fewer when there are fewer tiles
-template <class C, class Map>
-void launch_persist(const Map& map, const int* info, cudaStream_t s, int ctas) {
-  const int64_t nblk = map.blocks(C::BM, C::BN);
-  if (nblk <= 0) return;
-  const int64_t g = nblk < ctas ? nblk : ctas;
-  gemm_nt_dmma_persist<C, Map><<<(unsigned)g, C::NT, C::SMEM, s>>>(map, nblk, info);
 }
 
 template <class C, bool ACC, class Map, bool PRE = false>
