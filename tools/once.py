@@ -16,4 +16,4 @@ z = si.normals(n, 2)
 X, Y, Z = (torch.from_numpy(a).cuda() for a in (x, y, z))
 with ex.Context(device=0, nb=nb, graphs=-1, tile_tasks=tt) as c:
     for _ in range(int(__import__("os").environ.get("EVALS", "2"))):
-        c.loglik_dev(X, Y, Z, (1.0, 0.1, 0.5))
+        c.loglik_dev(X, Y, Z, tuple(float(v) for v in __import__("os").environ.get("THETA", "1.0,0.1,0.5").split(",")))
