@@ -84,8 +84,8 @@ typedef struct {
   double radius;        /* sphere radius R for distance = 1 (units of theta2); 0 = 6371     */
   int graphs;           /* CUDA-graph replay of whole evaluations (capture once per problem
                            shape and buffer set, then replay with theta patched into the
-                           generator nodes): 0 = automatic (n <= 32768, no NCCL communicator,
-                           a non-default stream), 1 = always when possible, -1 = never      */
+                           generator nodes; with NCCL the collectives are graph nodes too): 0 = automatic
+                           (n <= 32768, a non-default stream), 1 = always when possible, -1 = never */
   int grid_rows;        /* P of the P x Q process grid (the 2-D block-cyclic
                            distribution of P:450-453): tile (I, J) on rank (I mod P) Q + J mod Q,
                            Q = ranks / P. 0 or 1 = 1 x ranks (panel j on rank j % ranks); must

@@ -834,7 +834,9 @@ exageo_status do_finish(exageo_ctx* c, double* out3, int64_t* pivot) {
 // removes the per-launch host overhead and the launch gaps of the ~8 launches per panel
 // that dominate small n (the MLE loop evaluates the same shape hundreds of times).
 bool graph_eligible(const exageo_ctx* c, int64_t n) {
-  if (c->graphs < 0 || c->comm) return false;  // NCCL collectives stay outside graphs
+  // NCCL contexts too: NCCL collectives are captured as graph nodes (every rank captures and
+  // replays the same SPMD sequence); the pivot all-reduce is part of the graph (graph_body)
+  if (c->graphs < 0) return false;
   if (c->stream == nullptr || c->stream == cudaStreamLegacy || c->stream == cudaStreamPerThread) return false;
   return c->graphs > 0 || n <= 32768;
 }
@@ -884,6 +886,12 @@ exageo_status graph_body(exageo_ctx* c, const MaternConsts& mc, const double* x,
     CUDA_TRY(c, cudaMemcpyAsync(hd, c->out3, 3 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     for (size_t i = 0; i < c->rs.size(); ++i)
       CUDA_TRY(c, cudaMemcpyAsync(hi + i, c->rs[i].info, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  }
+  if (c->comm) {  // the first failing pivot over all ranks (hd[3] holds it as an int64)
+    launch_pivot_key(c->rs[0].info, c->pivbuf, c->stream);
+    c->kernels += 1;
+    NCCL_TRY(c, nccl::AllReduce(c->pivbuf, c->pivbuf, 1, ncclInt64, ncclMin, c->comm, c->stream));
+    CUDA_TRY(c, cudaMemcpyAsync(hd + 3, c->pivbuf, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
   }
   CUDA_TRY(c, record_timing(c, c->ev[3], c->stream));
   return EXAGEO_OK;
@@ -979,6 +987,11 @@ exageo_status run_graph(exageo_ctx* c, const exageo_theta* t, int64_t n, const d
   int64_t best = -1;
   for (size_t i = 0; i < c->rs.size(); ++i)
     if (hi[i] > 0 && (best < 0 || hi[i] - 1 < best)) best = hi[i] - 1;
+  if (c->comm) {  // all-reduced in the graph
+    int64_t g;
+    memcpy(&g, hd + 3, sizeof(g));
+    best = g == std::numeric_limits<int64_t>::max() ? -1 : g;
+  }
   *pivot = best;
   if (best >= 0) {
     r3[0] = -std::numeric_limits<double>::infinity();

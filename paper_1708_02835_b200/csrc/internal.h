@@ -208,6 +208,8 @@ void launch_potrf_block(double* a, int64_t lda, double* W, double* logdet_slot, 
 // scratch: kQuadBlocks doubles.
 void launch_local_partials(const Layout& L, const double* ws, const double* slots, int nslots, double* scratch,
                            double* out2, cudaStream_t s);
+// key = this rank's first failing global pivot (info - 1), or INT64_MAX when none.
+void launch_pivot_key(const int* info, int64_t* key, cudaStream_t s);
 // out3 = {loglik, logdet, quad} from nparts pairs {logdet/2 partial, quad partial} summed in order.
 void launch_combine(const double* parts, int nparts, int64_t n, double* out3, cudaStream_t s);
 // Copy this rank's columns of the lower triangle to dense column-major dst (device).

@@ -95,6 +95,12 @@ __global__ void __launch_bounds__(1024) local_partials_kernel(const double* __re
   }
 }
 
+// NCCL + CUDA graphs: this rank's first failing pivot as an all-reduce(min) key (INT64_MAX: none).
+__global__ void pivot_key_kernel(const int* __restrict__ info, int64_t* __restrict__ key) {
+  const int v = *info;
+  *key = v > 0 ? (int64_t)v - 1 : (int64_t)0x7fffffffffffffffLL;
+}
+
 // Combine the ranks' pairs in rank order: logdet = 2 sum(slots), quad = sum(y^2),
 // l = -quad/2 - logdet/2 - (n/2) log 2 pi (Alg. 2 l.7).
 __global__ void combine_kernel(const double* __restrict__ parts, int nparts, int64_t n, double* __restrict__ out3) {
@@ -216,6 +222,8 @@ void launch_local_partials(const Layout& L, const double* ws, const double* slot
   quad_partial_kernel<<<kQuadBlocks, 512, 0, s>>>(L, ws, scratch);
   local_partials_kernel<<<1, 1024, 0, s>>>(slots, nslots, scratch, kQuadBlocks, out2);
 }
+
+void launch_pivot_key(const int* info, int64_t* key, cudaStream_t s) { pivot_key_kernel<<<1, 1, 0, s>>>(info, key); }
 
 void launch_combine(const double* parts, int nparts, int64_t n, double* out3, cudaStream_t s) {
   combine_kernel<<<1, 32, 0, s>>>(parts, nparts, n, out3);

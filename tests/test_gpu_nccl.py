@@ -41,3 +41,27 @@ def test_single_rank_nccl_equals_plain():
     assert ei.value.pivot == 100
     plain.close()
     nc.close()
+
+
+def test_nccl_graph_replay_equals_stream_launch():
+    """CUDA-graph replay with NCCL collectives captured in the graph (the {logdet, quad} and the
+    pivot all-reduces): bitwise equal to stream launches, over several theta (patched per
+    replay), and ENOTPD with the all-reduced pivot through the graph."""
+    n = 1300
+    x, y = ex.gen_locations(n, 3)
+    z = si.normals(n, 4)
+    uid = ex.nccl_unique_id()
+    g = ex.Context(device=0, nb=128, world=1, rank=0, nccl_id=uid, graphs=1)
+    s = ex.Context(device=0, nb=128, world=1, rank=0, nccl_id=ex.nccl_unique_id(), graphs=-1)
+    for th in [(1.0, 0.1, 0.5), (0.7, 0.2, 1.3), (1.5, 0.05, 0.9)]:
+        a, b = g.loglik(x, y, z, th), s.loglik(x, y, z, th)
+        assert a.loglik == b.loglik and a.logdet == b.logdet and a.quad == b.quad, th
+    xd = np.concatenate([x[:200], x[:1]])
+    yd = np.concatenate([y[:200], y[:1]])
+    for c in (g, s):
+        with pytest.raises(ex.NotPositiveDefinite) as ei:
+            c.loglik(xd, yd, np.ones(201), (1.0, 0.1, 0.5))
+        assert ei.value.pivot == 200
+    assert np.isfinite(g.loglik(x, y, z, (1.0, 0.1, 0.5)).loglik)  # recovers after the failure
+    g.close()
+    s.close()
