@@ -274,8 +274,11 @@ exageo_status exageo_predict(exageo_ctx* ctx, const exageo_theta* theta, int64_t
  * from the same factor: batches of new sites, Sigma21 generated on the GPU, a blocked
  * multi-right-hand-side forward solve with L (diagonal-tile substitution + DMMA update of
  * the rows below), column sums of squares. var: host array of m doubles. Work ~ n^2 m flop.
- * Single-rank contexts only (EXAGEO_EINVAL with world > 1 or virtual ranks), tile size
- * nb <= 1024 (EXAGEO_EINVAL otherwise). */
+ * Collective on distributed contexts (NCCL or virtual ranks, any P x Q grid): per tile row I
+ * the ranks of process row I mod P reduce their partial updates onto the diagonal rank, which
+ * solves with L_II and broadcasts V_I down its process column, whose ranks update their tile
+ * rows below; the diagonal ranks' column sums are all-reduced. Tile size nb <= 1024
+ * (EXAGEO_EINVAL otherwise). */
 exageo_status exageo_predict_var(exageo_ctx* ctx, const exageo_theta* theta, int64_t n, const double* x,
                                  const double* y, const double* z, int64_t m, const double* xnew,
                                  const double* ynew, double* znew, double* var);

@@ -1552,17 +1552,134 @@ exageo_status exageo_predict(exageo_ctx* c, const exageo_theta* t, int64_t n, co
   return EXAGEO_OK;
 }
 
+}  // extern "C"
+
+// Kriging variance on a distributed context (NCCL ranks or virtual ranks, any P x Q grid), after
+// exageo_predict left L of Sigma22 in the tiles: V = L^{-1} Sigma21 by a distributed forward
+// substitution over the tile rows I = 0 .. T-1 (the multi-right-hand-side form of Alg. 2 l.4):
+//   U_I^(q) = -sum_{j < I, j = q mod Q} L_Ij V_j   accumulated on rank (I mod P, q),
+//   S_I     = Sigma21[tile row I] + sum_q U_I^(q)  reduced along process row I mod P onto the
+//                                                  diagonal rank (I mod P, I mod Q),
+//   V_I     = L_II^{-1} S_I                         broadcast down process column I mod Q, whose
+//             ranks apply U_I' -= L_I'I V_I to their tile rows I' > I (DMMA);
+//   var_c   = theta1 - sum_I sum_r (V_I)_rc^2       (the diagonal ranks' column sums, all-reduced).
+// Batches of mc new sites keep each rank's accumulator U (its tile rows x mc) within ~1 GB.
+exageo_status predict_var_grid(exageo_ctx* c, const exageo_theta* t, int64_t n, const double* x, const double* y,
+                               int64_t m, const double* xnew, const double* ynew, double* var) {
+  const Layout& G = c->G;
+  const int nb = G.nb, T = G.T, P = c->P, Q = c->Q;
+  const Layout& L0 = c->rs[0].L;
+  int64_t tp_max = 1;
+  for (int pp = 0; pp < P; ++pp) tp_max = std::max<int64_t>(tp_max, L0.Tp_of(pp));
+  int64_t mc = std::max<int64_t>(64, ((int64_t)1 << 27) / (tp_max * nb) / 64 * 64);  // 1 GB of U per rank
+  mc = std::min<int64_t>(mc, (m + 63) / 64 * 64);
+  std::vector<double*> U(c->rs.size(), nullptr);
+  struct FreeAll {
+    std::vector<double*>& v;
+    double* d = nullptr;
+    ~FreeAll() {
+      for (double* p : v) cudaFree(p);
+      cudaFree(d);
+    }
+  } guard{U};
+  for (size_t i = 0; i < c->rs.size(); ++i)
+    CUDA_TRY(c, cudaMalloc(&U[i], sizeof(double) * (size_t)c->rs[i].L.Tp() * nb * mc + 8));
+  // shared: x, y (n), the batch's sites (2 mc), S_I / V_I (nb mc), V_I^T (mc nb), reduce buffer
+  // (nb mc), column sums (mc) and variances (mc)
+  const size_t tot = 2 * (size_t)n + 2 * (size_t)mc + 3 * (size_t)nb * mc + 2 * (size_t)mc;
+  CUDA_TRY(c, cudaMalloc(&guard.d, sizeof(double) * tot));
+  double *dx = guard.d, *dy = dx + n, *dxn = dy + n, *dyn = dxn + mc, *Sb = dyn + mc, *Vt = Sb + (size_t)nb * mc,
+         *red = Vt + (size_t)nb * mc, *acc = red + (size_t)nb * mc, *dvar = acc + mc;
+  CUDA_TRY(c, cudaMemcpyAsync(dx, x, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(c, cudaMemcpyAsync(dy, y, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
+  const MaternConsts mcs = make_consts(*t, c);
+  for (int64_t i0 = 0; i0 < m; i0 += mc) {
+    const int cols = (int)std::min<int64_t>(mc, m - i0);
+    CUDA_TRY(c, cudaMemcpyAsync(dxn, xnew + i0, sizeof(double) * cols, cudaMemcpyHostToDevice, c->stream));
+    CUDA_TRY(c, cudaMemcpyAsync(dyn, ynew + i0, sizeof(double) * cols, cudaMemcpyHostToDevice, c->stream));
+    for (size_t i = 0; i < c->rs.size(); ++i)
+      CUDA_TRY(c, cudaMemsetAsync(U[i], 0, sizeof(double) * (size_t)c->rs[i].L.Tp() * nb * mc, c->stream));
+    CUDA_TRY(c, cudaMemsetAsync(acc, 0, sizeof(double) * mc, c->stream));
+    for (int I = 0; I < T; ++I) {
+      const int pI = I % P, qI = I % Q;
+      const int64_t r0 = (int64_t)I * nb;
+      const int rv = (int)std::max<int64_t>(0, std::min<int64_t>(nb, n - r0));  // rows of tile I inside n
+      RankState* D = local_state(c, pI * Q + qI);
+      // (1) S_I = Sigma21[tile I] + sum_q U_I^(q) on the diagonal rank
+      auto gen_S = [&]() -> exageo_status {
+        CUDA_TRY(c, cudaMemsetAsync(Sb, 0, sizeof(double) * (size_t)nb * mc, c->stream));
+        if (rv > 0) launch_matern_dense(mcs, rv, dx + r0, dy + r0, cols, dxn, dyn, Sb, nb, c->mtab, c->stream);
+        return EXAGEO_OK;
+      };
+      if (c->virt) {
+        gen_S();
+        for (int qq = 0; qq < Q; ++qq) {  // fixed order
+          RankState& R = c->rs[pI * Q + qq];
+          launch_add_block(Sb, nb, U[pI * Q + qq] + (int64_t)((I - pI) / P) * nb, (int64_t)R.L.Tp() * nb, nb, cols,
+                           c->stream);
+        }
+      } else {
+        RankState& R = c->rs[0];
+        if (R.L.p == pI) {
+          CUDA_TRY(c, cudaMemcpy2DAsync(red, sizeof(double) * nb, U[0] + (int64_t)((I - pI) / P) * nb,
+                                        sizeof(double) * (size_t)R.L.Tp() * nb, sizeof(double) * nb, cols,
+                                        cudaMemcpyDeviceToDevice, c->stream));
+          NCCL_TRY(c, nccl::Reduce(red, red, (size_t)nb * cols, ncclDouble, ncclSum, qI, row_comm(c), c->stream));
+        }
+        if (D) {
+          gen_S();
+          launch_add_block(Sb, nb, red, nb, nb, cols, c->stream);
+        }
+      }
+      // (2) V_I = L_II^{-1} S_I (tile I is the first tile row of the diagonal rank's local panel I)
+      if (D) {
+        launch_diag_solve_cols(D->ws + D->L.off(I), D->L.ld(I), nb, Sb, nb, cols, c->stream);
+        launch_colsq_accum(Sb, nb, rv, cols, acc, c->stream);
+      }
+      // (3) V_I down process column I mod Q
+      if (!c->virt && P > 1 && c->rs[0].L.q == qI)
+        NCCL_TRY(c, nccl::Broadcast(Sb, Sb, (size_t)nb * cols, ncclDouble, pI, c->comm_col, c->stream));
+      // (4) the column's ranks: U_I' -= L_I'I V_I for their tile rows I' > I
+      bool transposed = false;
+      for (size_t i = 0; i < c->rs.size(); ++i) {
+        RankState& R = c->rs[i];
+        if (R.L.q != qI) continue;
+        const int64_t lr0 = R.L.p == pI ? nb : 0;
+        const int64_t rows = R.L.lrows(I) - lr0;
+        if (rows <= 0) continue;
+        if (!transposed) {  // V_I^T with row stride mc (16-byte aligned rows for cp.async)
+          launch_transpose(Sb, nb, nb, (int)mc, Vt, c->stream);
+          transposed = true;
+        }
+        launch_gemm_panel(rows, cols, nb, R.ws + R.L.off(I) + lr0, R.L.ld(I), Vt, mc,
+                          U[i] + (int64_t)R.L.i0(I) * nb + lr0, (int64_t)R.L.Tp() * nb, true, nullptr, c->stream);
+        c->kernels += 2;
+      }
+      c->kernels += 3;
+    }
+    if (!c->virt && c->comm) NCCL_TRY(c, nccl::AllReduce(acc, acc, cols, ncclDouble, ncclSum, c->comm, c->stream));
+    launch_var_from_acc(acc, cols, t->sigma2, dvar, c->stream);
+    exageo_status st = check_launch(c);
+    if (st != EXAGEO_OK) return st;
+    CUDA_TRY(c, cudaMemcpyAsync(var + i0, dvar, sizeof(double) * cols, cudaMemcpyDeviceToHost, c->stream));
+  }
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return EXAGEO_OK;
+}
+
+extern "C" {
+
 exageo_status exageo_predict_var(exageo_ctx* c, const exageo_theta* t, int64_t n, const double* x, const double* y,
                                  const double* z, int64_t m, const double* xnew, const double* ynew, double* znew,
                                  double* var) {
   if (!c) return fail(nullptr, EXAGEO_EINVAL, "NULL ctx");
   if (!var) return fail(c, EXAGEO_EINVAL, "NULL var");
-  if (c->world != 1 || c->virt) return fail(c, EXAGEO_EINVAL, "the kriging variance needs a single-rank context");
-  if ((c->nb_opt > 0 ? c->nb_opt : auto_nb(n, 1)) > 1024)
+  if ((c->nb_opt > 0 ? c->nb_opt : auto_nb(n, c->world)) > 1024)
     return fail(c, EXAGEO_EINVAL, "the kriging variance supports tile sizes nb <= 1024 (one thread per tile row)");
   // mean (Eq. 5) -- leaves L of Sigma22 in the workspace
   exageo_status st = exageo_predict(c, t, n, x, y, z, m, xnew, ynew, znew);
   if (st != EXAGEO_OK) return st;
+  if (c->world > 1 || c->virt) return predict_var_grid(c, t, n, x, y, m, xnew, ynew, var);
   // var_i = theta1 - sigma_i^T Sigma22^{-1} sigma_i = theta1 - ||L^{-1} sigma_i||^2, sigma_i = Sigma21[:, i]:
   // batches of mc new sites, S = Sigma21 (N x mc, identity padding rows zero), forward solve
   // panel by panel (diagonal tile substitution, then the DMMA update of the rows below).

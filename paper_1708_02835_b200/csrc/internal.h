@@ -244,6 +244,11 @@ void launch_diag_solve_cols(const double* P, int64_t ld, int nb, double* S, int6
 void launch_transpose(const double* S, int64_t lds, int rows, int cols, double* Bt, cudaStream_t s);
 void launch_column_var(const double* V, int64_t ldv, int64_t n, int cols, double theta1, double* var,
                        cudaStream_t s);
+// Distributed kriging variance pieces: dst += src (rows x cols blocks); acc[c] += sum_{r<rows}
+// V_rc^2; var[c] = theta1 - acc[c].
+void launch_add_block(double* dst, int64_t ldd, const double* src, int64_t lds, int rows, int cols, cudaStream_t s);
+void launch_colsq_accum(const double* V, int64_t ldv, int rows, int cols, double* acc, cudaStream_t s);
+void launch_var_from_acc(const double* acc, int cols, double theta1, double* var, cudaStream_t s);
 // K8 (matern.cu): znew_i = sum_j C(||snew_i - s_j||; theta) w_j (Eq. (5), Alg. 3 l.8), the
 // covariance block Sigma12 generated on the fly and never stored. part: krige_chunks(n) * m.
 int krige_chunks(int64_t n);

@@ -176,7 +176,51 @@ __global__ void __launch_bounds__(256) column_var_kernel(const double* __restric
   }
 }
 
+// dst (rows x cols, ld ldd) += src (rows x cols, ld lds)
+__global__ void add_block_kernel(double* __restrict__ dst, int64_t ldd, const double* __restrict__ src, int64_t lds,
+                                 int rows, int cols) {
+  const int c = blockIdx.y;
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += gridDim.x * blockDim.x)
+    dst[(int64_t)c * ldd + r] += src[(int64_t)c * lds + r];
+}
+
+// acc[c] += sum_{r < rows} V_rc^2 (one CTA per column, fixed-order tree)
+__global__ void __launch_bounds__(256) colsq_accum_kernel(const double* __restrict__ V, int64_t ldv, int rows,
+                                                          double* __restrict__ acc) {
+  __shared__ double red[8];
+  const double* col = V + (int64_t)blockIdx.x * ldv;
+  double a = 0.0;
+  for (int k = threadIdx.x; k < rows; k += blockDim.x) a += col[k] * col[k];
+  for (int o = 16; o > 0; o >>= 1) a += __shfl_down_sync(0xffffffffu, a, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = a;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s2 = 0.0;
+    for (int q = 0; q < 8; ++q) s2 += red[q];
+    acc[blockIdx.x] += s2;
+  }
+}
+
+__global__ void var_from_acc_kernel(const double* __restrict__ acc, int cols, double theta1, double* __restrict__ var) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < cols) var[c] = theta1 - acc[c];
+}
+
 }  // namespace
+
+void launch_add_block(double* dst, int64_t ldd, const double* src, int64_t lds, int rows, int cols, cudaStream_t s) {
+  if (rows <= 0 || cols <= 0) return;
+  add_block_kernel<<<dim3((rows + 255) / 256, cols), 256, 0, s>>>(dst, ldd, src, lds, rows, cols);
+}
+
+void launch_colsq_accum(const double* V, int64_t ldv, int rows, int cols, double* acc, cudaStream_t s) {
+  if (rows <= 0 || cols <= 0) return;
+  colsq_accum_kernel<<<cols, 256, 0, s>>>(V, ldv, rows, acc);
+}
+
+void launch_var_from_acc(const double* acc, int cols, double theta1, double* var, cudaStream_t s) {
+  var_from_acc_kernel<<<(cols + 255) / 256, 256, 0, s>>>(acc, cols, theta1, var);
+}
 
 void launch_diag_solve_cols(const double* P, int64_t ld, int nb, double* S, int64_t lds, int cols, cudaStream_t s) {
   diag_solve_cols_kernel<<<(cols + kRhs - 1) / kRhs, nb, kRhs * nb * sizeof(double), s>>>(P, ld, nb, S, lds, cols);

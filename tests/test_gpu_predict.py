@@ -109,9 +109,25 @@ def test_predict_var_matches_oracle(n, m, nb, theta):
     assert np.all(var >= -1e-9) and np.all(var <= theta[0])
 
 
-def test_predict_var_rejects_distributed():
-    x, y = ex.gen_locations(200, 1)
-    with ex.Context(device=0, virtual_ranks=2) as c:
-        with pytest.raises(ex.ExageoError) as ei:
-            c.predict_var(x, y, np.ones(200), [0.5], [0.5], (1.0, 0.1, 0.5))
-        assert ei.value.status == ex.EINVAL
+@pytest.mark.parametrize("world,P,n,nb", [(2, 1, 1100, 128), (2, 2, 1100, 128), (4, 2, 1500, 128), (3, 1, 900, 256),
+                                          (6, 2, 2000, 128), (8, 2, 1700, 128)])
+def test_predict_var_distributed_virtual_ranks(world, P, n, nb):
+    """The distributed kriging variance (process-row reduce of the partial updates onto the
+    diagonal rank, broadcast of V_I down the process column) on virtual ranks of a P x Q grid:
+    equal to the single-rank variance to rounding and to the oracle's."""
+    m = 45
+    x, y = ex.gen_locations(n, 31)
+    z = si.normals(n, 32)
+    theta = (1.2, 0.08, 0.9)
+    rng = np.random.default_rng(world)
+    xn = np.concatenate([rng.random(m - 2), [x[7], 40.0]])
+    yn = np.concatenate([rng.random(m - 2), [y[7], 40.0]])
+    with ex.Context(device=0, nb=nb, virtual_ranks=world, grid_rows=P) as c:
+        mean, var = c.predict_var(x, y, z, xn, yn, theta)
+    with ex.Context(device=0, nb=nb) as c1:
+        mean1, var1 = c1.predict_var(x, y, z, xn, yn, theta)
+    np.testing.assert_allclose(mean, mean1, rtol=1e-10, atol=1e-11)
+    assert np.abs(var - var1).max() <= 1e-11 * theta[0]
+    ref = oracle.predict_var(x, y, xn, yn, theta)
+    assert np.abs(var - ref).max() <= 1e-9 * theta[0]
+    assert abs(var[-2]) <= 1e-9 * theta[0] and var[-1] == theta[0]
