@@ -79,13 +79,21 @@ int main(int argc, char** argv) {
   fill<<<1024, 256>>>(ws, (int64_t)(bytes / 8));
   cudaDeviceSynchronize();
   printf("n=%lld T=%d workspace %.2f GB\n", (long long)n, L.T, bytes / 1e9);
+  const int group = [&] {  // the product's super-panel size (gemm_dmma.cu syrk_group)
+    const int64_t g = ((int64_t)2 << 20) / ((int64_t)nb * nb);
+    return (int)(g < 1 ? 1 : (g > 8 ? 8 : g));
+  }();
+  const int which = argc > 3 ? atoi(argv[3]) : 0;  // 0: all steps below; 1: k = 0 only
   for (int k : {0, L.T / 2, (3 * L.T) / 4}) {
-    run<Cfg<64, 64, 16, 2, 2, 2, 4>, 2>("64x64x16 st2 preC (product)", L, ws, k, 3, 8);
-    run<Cfg<64, 64, 16, 2, 2, 3, 4>, 2>("64x64x16 st3 preC", L, ws, k, 3, 8);
-    run<Cfg<64, 64, 32, 2, 2, 2, 3>, 2>("64x64x32 st2 preC", L, ws, k, 3, 8);
-    run<Cfg<64, 64, 8, 2, 2, 4, 4>, 2>("64x64x8 st4 preC", L, ws, k, 3, 8);
-    run<Cfg<64, 64, 16, 2, 2, 2, 5>, 2>("64x64x16 st2 preC 5 CTA", L, ws, k, 3, 8);
-    run<Cfg<128, 64, 16, 2, 2, 2, 2>, 2>("128x64x16 st2 preC", L, ws, k, 3, 8);
+    if (which == 1 && k != 0) break;
+    run<Cfg<64, 64, 16, 2, 2, 2, 4>, 2>("64x64x16 st2 preC (product)", L, ws, k, 3, group);
+    // the cuBLAS DGEMM kernel on this B200 (ncu: cutlass_80_tensorop_d884gemm_64x128_16x3,
+    // 128 threads, 220 registers, 2 CTAs/SM, DMMA pipe 96.5%): warp tiles 32x64 / 64x32
+    run<Cfg<64, 128, 16, 2, 2, 3, 2>, 2>("64x128x16 st3 preC 2 CTA (warp 32x64)", L, ws, k, 3, group);
+    run<Cfg<128, 64, 16, 2, 2, 3, 2>, 2>("128x64x16 st3 preC 2 CTA (warp 64x32)", L, ws, k, 3, group);
+    run<Cfg<64, 128, 16, 2, 2, 2, 2>, 2>("64x128x16 st2 preC 2 CTA", L, ws, k, 3, group);
+    run<Cfg<64, 128, 16, 2, 2, 4, 2>, 2>("64x128x16 st4 preC 2 CTA", L, ws, k, 3, group);
+    run<Cfg<128, 128, 16, 2, 4, 3, 1>, 2>("128x128x16 st3 preC 8 warps 1 CTA (warp 64x32)", L, ws, k, 3, group);
   }
   return 0;
 }
