@@ -69,7 +69,12 @@ bool theta_ok(const exageo_theta* t) {
 // 384 from 15k, 512 from 21k, 1024 from 48k: 1024 wins at 50/60/90/100k by 1.4-1.7% and
 // loses at 70/80k by 0.3-0.6%; the differences near the other switches are 1-4%)
 int auto_nb(int64_t n, int world = 1) {
-  if (n >= 48000) return world > 1 ? 512 : 1024;  // distributed: more panels balance the ranks
+  if (world > 1) return n >= 14000 ? 512 : (n >= 6000 ? 256 : 128);  // more panels balance the ranks
+  // round-2 sweeps (tools/nb_sweep.py): with the 12.7 us K2 the longer panel chain of a wide
+  // tile costs less than the wider trailing update gains (K = nb per DMMA tile):
+  // 40k: 1024 647 ms vs 512 655; 60k-120k: 2048 best (100k: 9803 ms vs 9875 at 1024)
+  if (n >= 56000) return 2048;
+  if (n >= 36000) return 1024;
   if (n >= 14000) return 512;  // round-2 sweep (tail hand-off, padding-tile skip): 16k/20k best
   if (n >= 6000) return 256;   // 8192 / 10k: 256 best
   return 128;
@@ -1674,10 +1679,14 @@ exageo_status exageo_predict_var(exageo_ctx* c, const exageo_theta* t, int64_t n
                                  double* var) {
   if (!c) return fail(nullptr, EXAGEO_EINVAL, "NULL ctx");
   if (!var) return fail(c, EXAGEO_EINVAL, "NULL var");
-  if ((c->nb_opt > 0 ? c->nb_opt : auto_nb(n, c->world)) > 1024)
+  if (c->nb_opt > 1024)
     return fail(c, EXAGEO_EINVAL, "the kriging variance supports tile sizes nb <= 1024 (one thread per tile row)");
-  // mean (Eq. 5) -- leaves L of Sigma22 in the workspace
+  // mean (Eq. 5) -- leaves L of Sigma22 in the workspace; an automatic tile size above 1024
+  // (single GPU, n >= 56k) is capped at 1024 for this call
+  const int nb_saved = c->nb_opt;
+  if (nb_saved == 0 && auto_nb(n, c->world) > 1024) c->nb_opt = 1024;
   exageo_status st = exageo_predict(c, t, n, x, y, z, m, xnew, ynew, znew);
+  c->nb_opt = nb_saved;
   if (st != EXAGEO_OK) return st;
   if (c->world > 1 || c->virt) return predict_var_grid(c, t, n, x, y, m, xnew, ynew, var);
   // var_i = theta1 - sigma_i^T Sigma22^{-1} sigma_i = theta1 - ||L^{-1} sigma_i||^2, sigma_i = Sigma21[:, i]:

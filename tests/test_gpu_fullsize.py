@@ -1,5 +1,6 @@
-"""Full-size GPU parity at BASELINE's headline size (n = 100k, nb = 1024, the launch
-configuration bench.py times), where the O(n^3) oracle cannot run:
+"""Full-size GPU parity at BASELINE's headline size (n = 100k, nb = 2048, the launch
+configuration bench.py times: stream schedule, then the tile-task executor for the last
+panel -- the tail hand-off), where the O(n^3) oracle cannot run:
 
   * AR(1) / Kac-Murdock-Szego closed form of l (exact in O(n), nu = 1/2, collinear sites);
   * sampled generated entries vs the oracle's Matern function;
@@ -45,7 +46,7 @@ def test_ar1_closed_form_full_size(ctx):
     x, y = si.collinear_sites(N, h)
     z = si.normals(N, 5)
     r = ctx.loglik(x, y, z, (t1, t2, 0.5))
-    assert r.info["nb"] == 1024 and r.info["ntiles"] == 98  # the bench's launch configuration
+    assert r.info["nb"] == 2048 and r.info["ntiles"] == 49  # the bench's launch configuration
     rho = math.exp(-h / t2)
     logdet = N * math.log(t1) + (N - 1) * math.log1p(-rho * rho)
     w = np.empty(N)
@@ -77,11 +78,12 @@ def test_sampled_entries_and_factor_residual_full_size(ctx):
 
 
 # rows of L read back for the L L^T check: every panel-edge class of the bench layout
-# (nb = 1024, 64-column POTRF blocks, T = 98, N = 100352): first/last row of a panel and of a
-# 64-block, the rows either side of them, and the ragged last panel (panel 97 starts at 99328;
-# rows 99328..99999 are real, 100000..100351 identity padding), plus random rows
-EDGE_ROWS = [0, 1, 63, 64, 127, 128, 1023, 1024, 1025, 2047, 2048, 49151, 49152, 49215, 49216, 98303, 98304,
-             99327, 99328, 99391, 99392, 99967, 99968, 99998, 99999]
+# (nb = 2048, 64-column POTRF blocks, T = 49, N = 100352): first/last row of a panel and of a
+# 64-block, the rows either side of them, and the ragged last panel (panel 48 starts at 98304;
+# rows 98304..99999 are real, 100000..100351 identity padding; it is factored by the tile-task
+# executor after the stream schedule's hand-off), plus random rows
+EDGE_ROWS = [0, 1, 63, 64, 127, 128, 1023, 1024, 1025, 2047, 2048, 2049, 4095, 4096, 49151, 49152, 49215,
+             49216, 98303, 98304, 98305, 98367, 98368, 99327, 99328, 99967, 99968, 99998, 99999]
 
 
 def check_llt_sample(ctx, x, y, theta=THETA, extra=15):
