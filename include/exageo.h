@@ -116,6 +116,12 @@ typedef struct {
   double ms_trailing;        /* sum of their durations (CUDA events on their stream) */
   double trailing_flops;     /* algorithmic flops of those launches: 2 nb per (row, column)
                                 pair of the true lower triangle updated, incl. the z row */
+  /* the same trailing-update kernel over all its launches of the evaluation -- the bulk
+     updates U2 and the lookahead updates U1 of the next panel, which run concurrently on
+     another stream: their algorithmic flops and the union of their [start, end] spans */
+  int64_t update_launches;
+  double ms_update_union;
+  double update_flops;
 } exageo_loglik_info;
 
 /* Human-readable name of a status. Never NULL. */

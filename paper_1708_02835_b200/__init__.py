@@ -50,7 +50,9 @@ class LoglikInfo(ctypes.Structure):
                 ("ntiles", ctypes.c_int64), ("flops", ctypes.c_double), ("ms_total", ctypes.c_double),
                 ("ms_gen", ctypes.c_double), ("ms_chol", ctypes.c_double), ("ms_reduce", ctypes.c_double),
                 ("kernels", ctypes.c_int64), ("trailing_launches", ctypes.c_int64),
-                ("ms_trailing", ctypes.c_double), ("trailing_flops", ctypes.c_double)]
+                ("ms_trailing", ctypes.c_double), ("trailing_flops", ctypes.c_double),
+                ("update_launches", ctypes.c_int64), ("ms_update_union", ctypes.c_double),
+                ("update_flops", ctypes.c_double)]
 
     def as_dict(self) -> dict:
         return {k: getattr(self, k) for k, _ in self._fields_}

@@ -487,6 +487,8 @@ exageo_status factor_tile_tasks(exageo_ctx* c) {
   if (c->dag_t0 == 0) {
     R.n_u2 = 0;
     R.u2_flops = 0.0;
+    R.n_u1 = 0;
+    R.u1_flops = 0.0;
   }
   const int nctas = 1 + std::min(c->dag_nproc - 1, std::max(c->dag_ntasks, 1));  // chain CTA + pool
   DagGen g{c->dag_gen, c->dag_mc, c->mtab, c->dag_x, c->dag_y, c->dag_z};
@@ -700,6 +702,8 @@ exageo_status do_factor(exageo_ctx* c) {
     for (cudaStream_t s : {R.s_la, R.s_main, R.s_comm}) CUDA_TRY(c, cudaStreamWaitEvent(s, c->ev_fork, 0));
     R.n_u2 = 0;
     R.u2_flops = 0.0;
+    R.n_u1 = 0;
+    R.u1_flops = 0.0;
   }
   exageo_status st;
   for (auto& R : c->rs)
@@ -724,8 +728,19 @@ exageo_status do_factor(exageo_ctx* c) {
         CUDA_TRY(c, cudaStreamWaitEvent(R.s_la, avail, 0));
         if (k > 0) CUDA_TRY(c, cudaStreamWaitEvent(R.s_la, R.ev_U2[(k - 1) & 1], 0));
         if (k + 1 < L.sb_end(k)) {  // (IND: panel k+1 opens a new super tile: no update)
+          if ((int)R.u1b.size() <= R.n_u1) {
+            cudaEvent_t b, e;
+            CUDA_TRY(c, cudaEventCreate(&b));
+            CUDA_TRY(c, cudaEventCreate(&e));
+            R.u1b.push_back(b);
+            R.u1e.push_back(e);
+          }
+          CUDA_TRY(c, record_timing(c, R.u1b[R.n_u1], R.s_la));
           if (L.P == 1) launch_syrk_panels(L, R.ws, sl[0], k, k + 1, 1, R.info, R.s_la);  // U1(k)
           else launch_syrk_panels_2d(L, R.ws, sl, sld, k, k + 1, 1, R.info, R.s_la);
+          CUDA_TRY(c, record_timing(c, R.u1e[R.n_u1], R.s_la));
+          ++R.n_u1;
+          R.u1_flops += update_flops(L, k, k + 1, 1);
           c->kernels += 1;
         }
         CUDA_TRY(c, cudaEventRecord(R.ev_U1[k & 1], R.s_la));
@@ -908,12 +923,16 @@ exageo_status run_graph(exageo_ctx* c, const exageo_theta* t, int64_t n, const d
   if (st != EXAGEO_OK) return st;
   if (!c->h_res) CUDA_TRY(c, cudaMallocHost(&c->h_res, sizeof(double) * 4 + sizeof(int) * c->rs.size()));
   for (auto& R : c->rs)  // timing events of every U2 launch exist before the capture
-    while ((int)R.u2b.size() < R.L.T) {
-      cudaEvent_t b, e;
+    while ((int)R.u2b.size() < R.L.T || (int)R.u1b.size() < R.L.T) {
+      cudaEvent_t b, e, b1, e1;
       CUDA_TRY(c, cudaEventCreate(&b));
       CUDA_TRY(c, cudaEventCreate(&e));
+      CUDA_TRY(c, cudaEventCreate(&b1));
+      CUDA_TRY(c, cudaEventCreate(&e1));
       R.u2b.push_back(b);
       R.u2e.push_back(e);
+      R.u1b.push_back(b1);
+      R.u1e.push_back(e1);
     }
   const MaternConsts mc = make_consts(*t, c);
   std::vector<const void*> key = graph_key(c, x, y, z, mc.kind);
@@ -958,11 +977,15 @@ exageo_status run_graph(exageo_ctx* c, const exageo_theta* t, int64_t n, const d
     for (auto& R : c->rs) {
       R.g_n_u2 = R.n_u2;
       R.g_u2_flops = R.u2_flops;
+      R.g_n_u1 = R.n_u1;
+      R.g_u1_flops = R.u1_flops;
     }
   } else {
     for (auto& R : c->rs) {
       R.n_u2 = R.g_n_u2;
       R.u2_flops = R.g_u2_flops;
+      R.n_u1 = R.g_n_u1;
+      R.u1_flops = R.g_u1_flops;
     }
     for (cudaGraphNode_t nd : c->gen_nodes) {  // new theta into every K1 / K1T node
       cudaKernelNodeParams kp;
@@ -1060,6 +1083,30 @@ exageo_status loglik_device(exageo_ctx* c, const exageo_theta* t, int64_t n, con
       tr += ms;
     }
     info->ms_trailing = tr;
+    // all launches of the trailing-update kernel (U1 + U2): union of their spans
+    std::vector<std::pair<float, float>> iv;
+    auto span = [&](cudaEvent_t b, cudaEvent_t e) {
+      float tb = 0.f, te = 0.f;
+      if (cudaEventElapsedTime(&tb, c->ev[1], b) == cudaSuccess && cudaEventElapsedTime(&te, c->ev[1], e) == cudaSuccess)
+        iv.push_back({tb, te});
+    };
+    for (int i = 0; i < R.n_u2; ++i) span(R.u2b[i], R.u2e[i]);
+    for (int i = 0; i < R.n_u1; ++i) span(R.u1b[i], R.u1e[i]);
+    std::sort(iv.begin(), iv.end());
+    double uni = 0.0, cur_b = -1.0, cur_e = -1.0;
+    for (auto& v : iv) {
+      if (v.first > cur_e) {
+        if (cur_e > cur_b) uni += cur_e - cur_b;
+        cur_b = v.first;
+        cur_e = v.second;
+      } else if (v.second > cur_e) {
+        cur_e = v.second;
+      }
+    }
+    if (cur_e > cur_b) uni += cur_e - cur_b;
+    info->update_launches = R.n_u2 + R.n_u1;
+    info->ms_update_union = uni;
+    info->update_flops = R.u2_flops + R.u1_flops;
     // tracing (env EXAGEO_U2_TRACE=<file>): each bulk trailing update's [start, end] in ms from
     // the start of the factorization, appended per evaluation -- the gaps between them are
     // the panel chain's stalls
@@ -1120,6 +1167,8 @@ void destroy_rank(RankState& R) {
     if (ev) cudaEventDestroy(ev);
   for (cudaEvent_t ev : R.u2b) cudaEventDestroy(ev);
   for (cudaEvent_t ev : R.u2e) cudaEventDestroy(ev);
+  for (cudaEvent_t ev : R.u1b) cudaEventDestroy(ev);
+  for (cudaEvent_t ev : R.u1e) cudaEventDestroy(ev);
   for (cudaStream_t s : {R.s_la, R.s_main, R.s_comm})
     if (s) cudaStreamDestroy(s);
 }

@@ -50,6 +50,11 @@ struct RankState {
   double u2_flops = 0.0;
   int g_n_u2 = 0;                                // n_u2 / u2_flops of the captured graph
   double g_u2_flops = 0.0;
+  std::vector<cudaEvent_t> u1b, u1e;             // timing of the lookahead updates U1
+  int n_u1 = 0;
+  double u1_flops = 0.0;
+  int g_n_u1 = 0;
+  double g_u1_flops = 0.0;
 };
 
 }  // namespace exageo

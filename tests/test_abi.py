@@ -37,7 +37,7 @@ def test_strerror_and_workspace_size():
     N = T * nb
     expect = 8 * nb * sum(N - nb * j + 128 for j in range(T)) + 256 * 8
     assert ex.workspace_bytes(100_000, 512) == expect
-    T2, nb2 = 98, 1024  # auto nb = 1024 at n >= 48k (single GPU)
+    T2, nb2 = 49, 2048  # auto nb = 2048 at n >= 56k (single GPU)
     N2 = T2 * nb2
     assert ex.workspace_bytes(100_000) == 8 * nb2 * sum(N2 - nb2 * j + 128 for j in range(T2)) + 256 * 8
 
