@@ -107,7 +107,10 @@ struct Frag {
   double v[4][2][2];
 };
 __device__ __forceinline__ int frag_r0() { return 32 * ((threadIdx.x >> 5) & 1); }
-__device__ __forceinline__ int frag_c0() { return 16 * (threadIdx.x >> 6); }
+// column block of warp w: 16 * {0, 1, 3, 2}[w >> 1], so the two warps of each sub-partition
+// (w, w + 4) hold column blocks {0, 3} or {1, 2}: the triangular TRSM (column block q needs
+// 16 (q + 1) of the 64 k-steps) is balanced over the four DMMA sub-pipes
+__device__ __forceinline__ int frag_c0() { return 16 * ((0x2310 >> (4 * (threadIdx.x >> 6))) & 3); }
 
 // dst (shared, ld LDS) <- 64 x 64 tile at src (global, ld) by cp.async (L2 only); committed
 // as one group, not waited for.
@@ -153,6 +156,25 @@ __device__ __forceinline__ void frag_store(const Frag& f, double* C, int64_t ldc
     for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
       for (int e = 0; e < 2; ++e) C[(int64_t)(c0 + 8 * nt + 2 * fk + e) * ldc + r0 + 8 * mt + fr] = f.v[mt][nt][e];
+}
+// f += sgn * A[r0:, kbeg:kend] B[c0:, kbeg:kend]^T for the 32 x 16 block at (r0, c0)
+__device__ __forceinline__ void frag_mma_at(Frag& f, const double* As, const double* Bs, double sgn, int r0, int c0,
+                                            int kbeg, int kend) {
+  const int lane = threadIdx.x & 31, fr = lane >> 2, fk = lane & 3;
+#pragma unroll 4
+  for (int kk = kbeg; kk < kend; kk += 4) {
+    const double* as = As + (kk + fk) * LDS + r0 + fr;
+    const double* bs = Bs + (kk + fk) * LDS + c0 + fr;
+    double af[4], bf[2];
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt) af[mt] = sgn * as[8 * mt];
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) bf[nt] = bs[8 * nt];
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) dmma64(f.v[mt][nt], af[mt], bf[nt]);
+  }
 }
 // f += sgn * A[:, 0:kend] B[:, 0:kend]^T (A, B shared, ld LDS)
 __device__ __forceinline__ void frag_mma(Frag& f, const double* As, const double* Bs, double sgn, int kend) {
@@ -465,10 +487,40 @@ __device__ void chain_cta(const DagArgs& a, int* st, double* sm) {
       __syncthreads();
     }
     const unsigned long long t5 = a.trace ? gtimer() : 0;
-    if (!frag_upper()) {
-      frag_load_s(f, Y);
-      frag_mma(f, X, X, -1.0, PB);
-      frag_store(f, sm, LDA2);
+    // six 32 x 16 blocks hold the lower triangle; warps 4 and 6 (no block of their own) take the
+    // upper half of the K range of warps 5 and 7's blocks (32, 48) and (32, 32), so each of the
+    // four DMMA sub-pipes runs 3 / 2 blocks' worth instead of 2 / 1 (partials added via the
+    // K2 body's W region, free after the TRSM)
+    {
+      const int warp = threadIdx.x >> 5;
+      double* part = sm + PB * LDA2;  // W region: 2 partial blocks x 32 lanes x 16 values
+      if (warp == 4 || warp == 6) {
+        frag_zero(f);
+        frag_mma_at(f, X, X, -1.0, 32, warp == 4 ? 48 : 32, 32, PB);
+        double* pp = part + (warp == 4 ? 0 : 512) + lane * 16;
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < 2; ++nt) {
+            pp[4 * mt + 2 * nt] = f.v[mt][nt][0];
+            pp[4 * mt + 2 * nt + 1] = f.v[mt][nt][1];
+          }
+      } else {
+        frag_load_s(f, Y);
+        frag_mma(f, X, X, -1.0, (warp == 5 || warp == 7) ? 32 : PB);
+      }
+      __syncthreads();
+      if (warp == 5 || warp == 7) {
+        const double* pp = part + (warp == 5 ? 0 : 512) + lane * 16;
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < 2; ++nt) {
+            f.v[mt][nt][0] += pp[4 * mt + 2 * nt];
+            f.v[mt][nt][1] += pp[4 * mt + 2 * nt + 1];
+          }
+      }
+      if (!frag_upper()) frag_store(f, sm, LDA2);
     }
     __syncthreads();
     rec(3 * k + 2, t4, t5);
