@@ -34,8 +34,25 @@ def nvcc() -> str:
     raise RuntimeError("nvcc not found")
 
 
+def cutlass_include() -> str:
+    """The CUTLASS header tree vendored in this image (flashinfer's, else tilelang's copy): the
+    trailing-update kernel builds its DMMA mainloop and epilogue from CUTLASS's SM80 templates
+    inside our own kernel (gemm_dmma.cu). Fails loudly when no tree is found."""
+    import site
+    roots = [os.environ.get("EXAGEO_CUTLASS_INCLUDE", "")]
+    for sp in site.getsitepackages() + [site.getusersitepackages()]:
+        roots += [os.path.join(sp, "flashinfer", "data", "cutlass", "include"),
+                  os.path.join(sp, "tilelang", "3rdparty", "cutlass", "include")]
+    for r in roots:
+        if r and os.path.exists(os.path.join(r, "cutlass", "gemm", "kernel", "default_gemm.h")):
+            return r
+    raise RuntimeError("CUTLASS headers not found (set EXAGEO_CUTLASS_INCLUDE to a cutlass/include tree)")
+
+
 def _flags(src: str) -> list[str]:
     f = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-ffp-contract=off", "-I", INCLUDE, "-I", CSRC]
+    if src == "gemm_dmma.cu":
+        f += ["-I", cutlass_include()]
     f += ARCH
     if src.endswith(".cu"):
         f += ["-Xptxas", "-warn-spills"]

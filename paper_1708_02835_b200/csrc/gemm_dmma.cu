@@ -1,6 +1,15 @@
-#include <cstdlib>
 // gemm_dmma.cu -- instantiations and launchers of the DMMA contraction kernels
-// (gemm_dmma.cuh) used by the tiled Cholesky schedule in api.cu.
+// (gemm_dmma.cuh) used by the tiled Cholesky schedule in api.cu, and the trailing-update
+// kernel (U1/U2: SyrkMap / Syrk2DMap tiles) whose mainloop and epilogue are CUTLASS's SM80
+// FP64 tensor-op templates (mma.sync.m8n8k4.f64 = DMMA, 3-stage cp.async, 64x128x16 CTA tile,
+// 32x64 warp tiles: the tiling of the cuBLAS DGEMM kernel on this B200) instantiated inside our
+// own kernel: the tile -> (A, B, C) pointers come from our maps (triangular tile enumeration,
+// panel layout, skipped padding tiles), the epilogue is C <- C - A B^T in place.
+#include <cstdlib>
+
+#include "cutlass/cutlass.h"
+#include "cutlass/epilogue/thread/linear_combination.h"
+#include "cutlass/gemm/kernel/default_gemm.h"
 #include "gemm_dmma.cuh"
 
 namespace exageo {
@@ -15,12 +24,61 @@ using PanelCfg = Cfg<64, 64, 16, 2, 2, 2, 4>;
 using TrailCfg = Cfg<64, 64, 16, 2, 2, 2, 4>;
 }  // namespace
 
+// ---- CUTLASS-mainloop trailing update ------------------------------------------------------
+// Per CTA tile (BM = 64 rows x BN = 128 columns of C, K = nb) the transposed problem:
+// C^T (BN x BM, a row-major view of our column-major C, ld ldc) <- C^T - B (BN x K, column-major,
+// ld ldb) . A^T (K x BM, a row-major view of our column-major A, ld lda). tools/gemm_cutlass_tune.cu:
+// U2(0) at n = 100k, nb = 2048: 36.28 TF vs 34.25 for gemm_nt_dmma 64x64x16 (profiles/).
+using TrailGK = cutlass::gemm::kernel::DefaultGemm<
+    double, cutlass::layout::ColumnMajor, 1, double, cutlass::layout::RowMajor, 1, double, cutlass::layout::RowMajor,
+    double, cutlass::arch::OpClassTensorOp, cutlass::arch::Sm80, cutlass::gemm::GemmShape<128, 64, 16>,
+    cutlass::gemm::GemmShape<64, 32, 16>, cutlass::gemm::GemmShape<8, 8, 4>,
+    cutlass::epilogue::thread::LinearCombination<double, 1, double, double>,
+    cutlass::gemm::threadblock::GemmIdentityThreadblockSwizzle<>, 3, false, cutlass::arch::OpMultiplyAdd>::GemmKernel;
+constexpr int kTrailBM = 64, kTrailBN = 128;
+constexpr int kTrailSmem = (int)sizeof(TrailGK::SharedStorage);
+
+template <class Map>
+__global__ void __launch_bounds__(TrailGK::kThreadCount, 2) trail_update_kernel(Map map, const int* __restrict__ info) {
+  extern __shared__ __align__(16) uint8_t smem_t[];
+  GemmTile t;
+  if (!map.template operator()<kTrailBM, kTrailBN>((int64_t)blockIdx.x, t)) return;
+  if (info != nullptr && *(volatile const int*)info != 0) return;  // a pivot failed upstream
+  using Mma = TrailGK::Mma;
+  using Epi = TrailGK::Epilogue;
+  auto& ss = *reinterpret_cast<TrailGK::SharedStorage*>(smem_t);
+  const int tid = threadIdx.x, warp = __shfl_sync(0xffffffffu, tid / 32, 0), lane = tid % 32;
+  Mma::IteratorA itA(Mma::IteratorA::Params(cutlass::layout::ColumnMajor(t.ldb)), const_cast<double*>(t.B),
+                     {kTrailBN, t.K}, tid, {0, 0});
+  Mma::IteratorB itB(Mma::IteratorB::Params(cutlass::layout::RowMajor(t.lda)), const_cast<double*>(t.A),
+                     {t.K, kTrailBM}, tid, {0, 0});
+  Mma mma(ss.main_loop, tid, warp, lane);
+  Mma::FragmentC acc;
+  acc.clear();
+  mma(t.K / 16, acc, itA, itB, acc);
+  Epi::OutputTileIterator::Params pC(cutlass::layout::RowMajor(t.ldc));
+  Epi::OutputTileIterator itC(pC, t.C, {kTrailBN, kTrailBM}, tid, {0, 0});
+  Epi::OutputTileIterator itD(pC, t.C, {kTrailBN, kTrailBM}, tid, {0, 0});
+  Epi epi(ss.epilogue, tid, warp, lane);
+  Epi::OutputOp op(Epi::OutputOp::Params(-1.0, 1.0));
+  epi(op, itD, acc, itC);
+}
+
+template <class Map>
+void launch_trail(const Map& map, const int* info, cudaStream_t s) {
+  const int64_t nblk = map.blocks(kTrailBM, kTrailBN);
+  if (nblk <= 0) return;
+  trail_update_kernel<Map><<<(unsigned)nblk, TrailGK::kThreadCount, kTrailSmem, s>>>(map, info);
+}
+
 cudaError_t gemm_init() {
   cudaError_t e;
   if ((e = set_smem<PanelCfg, true, DenseMap>()) != cudaSuccess) return e;
   if ((e = set_smem<PanelCfg, false, DenseMap>()) != cudaSuccess) return e;
-  if ((e = set_smem<TrailCfg, true, SyrkMap>()) != cudaSuccess) return e;
-  return set_smem<TrailCfg, true, Syrk2DMap>();
+  if ((e = cudaFuncSetAttribute(trail_update_kernel<SyrkMap>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                kTrailSmem)) != cudaSuccess)
+    return e;
+  return cudaFuncSetAttribute(trail_update_kernel<Syrk2DMap>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTrailSmem);
 }
 
 void launch_gemm_panel(int64_t M, int N, int K, const double* A, int64_t lda, const double* B, int64_t ldb,
@@ -68,7 +126,7 @@ void launch_syrk_panels(const Layout& L, double* ws, const double* Pk, int k, in
   map.npan = npan;
   map.row_end = (int64_t)L.sb_end(k) * L.nb;  // N unless IND
   map.group = L.world == 1 ? syrk_group(L.nb) : 1;  // super panels: panel k's rows read once per group
-  launch<TrailCfg, true, SyrkMap, true>(map, info, s);
+  launch_trail(map, info, s);
 }
 
 void launch_syrk_panels_2d(const Layout& L, double* ws, const double* const* slices, const int64_t* slds, int k,
@@ -85,7 +143,7 @@ void launch_syrk_panels_2d(const Layout& L, double* ws, const double* const* sli
   map.J0 = J0;
   map.npan = npan;
   map.Eb = L.sb_end(k);
-  launch<TrailCfg, true, Syrk2DMap, true>(map, info, s);
+  launch_trail(map, info, s);
 }
 
 }  // namespace exageo
