@@ -55,8 +55,8 @@ typedef struct exageo_ctx exageo_ctx;
 
 typedef struct {
   int device;   /* CUDA device ordinal                                               */
-  int nb;       /* tile size (multiple of 128); 0 = automatic (single GPU: 128 below n = 6000, 256
-                   below 14k, 512 below 36k, 1024 below 56k, else 2048; world > 1: at most 512) */
+  int nb;       /* tile size (multiple of 128); 0 = automatic (single GPU: 128 below n = 6000, 512
+                   below 20k, 1024 below 56k, else 2048; world > 1: at most 512)               */
   void* stream; /* cudaStream_t to run on; NULL = the library creates its own stream */
   /* Distribution: the tiles are dealt 2-D block-cyclically over a
    * grid_rows x (world / grid_rows) process grid (1 x world by default: panel j on rank

@@ -73,10 +73,11 @@ int auto_nb(int64_t n, int world = 1) {
   // round-2 sweeps (tools/nb_sweep.py): with the 12.7 us K2 the longer panel chain of a wide
   // tile costs less than the wider trailing update gains (K = nb per DMMA tile):
   // 40k: 1024 647 ms vs 512 655; 60k-120k: 2048 best (100k: 9803 ms vs 9875 at 1024)
+  // after the CUTLASS-mainloop trailing update: 8192 / 10k / 16k 512 best, 20k / 30k / 40k
+  // 1024, 60k / 100k 2048 (100k: 9281 ms vs 9312 at 1536, 9373 at 1024)
   if (n >= 56000) return 2048;
-  if (n >= 36000) return 1024;
-  if (n >= 14000) return 512;  // round-2 sweep (tail hand-off, padding-tile skip): 16k/20k best
-  if (n >= 6000) return 256;   // 8192 / 10k: 256 best
+  if (n >= 20000) return 1024;
+  if (n >= 6000) return 512;
   return 128;
 }
 

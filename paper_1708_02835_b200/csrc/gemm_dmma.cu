@@ -56,6 +56,7 @@ __global__ void __launch_bounds__(TrailGK::kThreadCount, 2) trail_update_kernel(
   Mma::FragmentC acc;
   acc.clear();
   mma(t.K / 16, acc, itA, itB, acc);
+  __syncthreads();  // the epilogue reuses the mainloop's shared memory
   Epi::OutputTileIterator::Params pC(cutlass::layout::RowMajor(t.ldc));
   Epi::OutputTileIterator itC(pC, t.C, {kTrailBN, kTrailBM}, tid, {0, 0});
   Epi::OutputTileIterator itD(pC, t.C, {kTrailBN, kTrailBM}, tid, {0, 0});
@@ -71,12 +72,57 @@ void launch_trail(const Map& map, const int* info, cudaStream_t s) {
   trail_update_kernel<Map><<<(unsigned)nblk, TrailGK::kThreadCount, kTrailSmem, s>>>(map, info);
 }
 
+// ---- CUTLASS-mainloop panel kernels (N = 64: the left-looking panel update and the TRSM by
+// the inverted diagonal block) -------------------------------------------------------------
+// 64 x 64 CTA tiles (32 x 32 warps, 3 stages) over the rows of the panel, transposed as above;
+// partial row tiles through the predicated iterators; accumulate: C <- C - A B^T, else
+// C <- A B^T (C may alias A: the CTA owns all 64 columns of its rows and reads them first).
+using PanelGK = cutlass::gemm::kernel::DefaultGemm<
+    double, cutlass::layout::ColumnMajor, 1, double, cutlass::layout::RowMajor, 1, double, cutlass::layout::RowMajor,
+    double, cutlass::arch::OpClassTensorOp, cutlass::arch::Sm80, cutlass::gemm::GemmShape<64, 64, 16>,
+    cutlass::gemm::GemmShape<32, 32, 16>, cutlass::gemm::GemmShape<8, 8, 4>,
+    cutlass::epilogue::thread::LinearCombination<double, 1, double, double>,
+    cutlass::gemm::threadblock::GemmIdentityThreadblockSwizzle<>, 3, false, cutlass::arch::OpMultiplyAdd>::GemmKernel;
+constexpr int kPanelSmem = (int)sizeof(PanelGK::SharedStorage);
+
+__global__ void __launch_bounds__(PanelGK::kThreadCount, 4) panel_gemm_kernel(DenseMap map, bool accumulate,
+                                                                              const int* __restrict__ info) {
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");  // programmatic dependent launch (panel chain)
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  extern __shared__ __align__(16) uint8_t smem_p[];
+  GemmTile t;
+  map.operator()<64, 64>((int64_t)blockIdx.x, t);
+  if (info != nullptr && *(volatile const int*)info != 0) return;
+  using Mma = PanelGK::Mma;
+  using Epi = PanelGK::Epilogue;
+  auto& ss = *reinterpret_cast<PanelGK::SharedStorage*>(smem_p);
+  const int tid = threadIdx.x, warp = __shfl_sync(0xffffffffu, tid / 32, 0), lane = tid % 32;
+  Mma::IteratorA itA(Mma::IteratorA::Params(cutlass::layout::ColumnMajor(t.ldb)), const_cast<double*>(t.B),
+                     {t.n_valid, t.K}, tid, {0, 0});
+  Mma::IteratorB itB(Mma::IteratorB::Params(cutlass::layout::RowMajor(t.lda)), const_cast<double*>(t.A),
+                     {t.K, t.m_valid}, tid, {0, 0});
+  Mma mma(ss.main_loop, tid, warp, lane);
+  Mma::FragmentC acc;
+  acc.clear();
+  mma((t.K + 15) / 16, acc, itA, itB, acc);
+  __syncthreads();  // C may alias A: every warp has consumed its tiles of A before any store
+  Epi::OutputTileIterator::Params pC(cutlass::layout::RowMajor(t.ldc));
+  Epi::OutputTileIterator itC(pC, t.C, {t.n_valid, t.m_valid}, tid, {0, 0});
+  Epi::OutputTileIterator itD(pC, t.C, {t.n_valid, t.m_valid}, tid, {0, 0});
+  Epi epi(ss.epilogue, tid, warp, lane);
+  Epi::OutputOp op(accumulate ? Epi::OutputOp::Params(-1.0, 1.0) : Epi::OutputOp::Params(1.0, 0.0));
+  epi(op, itD, acc, itC);
+}
+
 cudaError_t gemm_init() {
   cudaError_t e;
   if ((e = set_smem<PanelCfg, true, DenseMap>()) != cudaSuccess) return e;
   if ((e = set_smem<PanelCfg, false, DenseMap>()) != cudaSuccess) return e;
   if ((e = cudaFuncSetAttribute(trail_update_kernel<SyrkMap>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 kTrailSmem)) != cudaSuccess)
+    return e;
+  if ((e = cudaFuncSetAttribute(panel_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kPanelSmem)) !=
+      cudaSuccess)
     return e;
   return cudaFuncSetAttribute(trail_update_kernel<Syrk2DMap>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTrailSmem);
 }
@@ -95,6 +141,25 @@ void launch_gemm_panel(int64_t M, int N, int K, const double* A, int64_t lda, co
   map.N = N;
   map.K = K;
   map.mblocks = (int)((M + PanelCfg::BM - 1) / PanelCfg::BM);
+  static const int min_k = [] {  // tuning: EXAGEO_PANEL_CUTLASS_MINK
+    const char* e = getenv("EXAGEO_PANEL_CUTLASS_MINK");
+    return e ? atoi(e) : 512;
+  }();
+  if (N == 64 && K >= min_k) {  // long panel updates: CUTLASS mainloop (64 x 64 tiles)
+    const unsigned nblk = (unsigned)map.blocks(64, 64);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(nblk);
+    cfg.blockDim = dim3(PanelGK::kThreadCount);
+    cfg.dynamicSmemBytes = kPanelSmem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, panel_gemm_kernel, map, accumulate, info);
+    return;
+  }
   if (accumulate) launch<PanelCfg, true, DenseMap, true>(map, info, s, pdl);
   else launch<PanelCfg, false>(map, info, s, pdl);
 }
