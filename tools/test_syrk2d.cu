@@ -38,6 +38,7 @@ Layout grid_layout(int T, int nb, int P, int Q, int rank, int ind, std::vector<i
 static double ws_dummy[1];
 static double slice_dummy[kMaxP][1];
 
+template <int BM, int BN>
 int check(int T, int nb, int P, int Q, int rank, int k, int J0, int npan, int ind) {
   std::vector<int64_t> offs;
   Layout L = grid_layout(T, nb, P, Q, rank, ind, offs);
@@ -56,11 +57,11 @@ int check(int T, int nb, int P, int Q, int rank, int k, int J0, int npan, int in
   std::vector<std::vector<int64_t>> so(P);
   std::vector<Layout> SL;
   for (int pp = 0; pp < P; ++pp) SL.push_back(grid_layout(T, nb, P, Q, pp * Q + k % Q, ind, so[pp]));
-  const int64_t nblk = m.blocks(64, 64);
+  const int64_t nblk = m.blocks(BM, BN);
   std::set<std::tuple<int, int64_t, int64_t>> seen;  // (J, global row, global col)
   for (int64_t b = 0; b < nblk; ++b) {
     GemmTile t;
-    if (!m.operator()<64, 64>(b, t)) continue;
+    if (!m.operator()<BM, BN>(b, t)) continue;
     // locate the C tile: which local panel, which local row / column
     int J = -1;
     int64_t lr = -1, cc = -1;
@@ -95,7 +96,7 @@ int check(int T, int nb, int P, int Q, int rank, int k, int J0, int npan, int in
              (long long)gr, (long long)gc);
       return 1;
     }
-    if (gr < L.N && (gr / nb >= L.sb_end(k) || gr + 64 <= gc)) {
+    if (gr < L.N && (gr / nb >= L.sb_end(k) || gr + BM <= gc)) {
       printf("tile outside the updated lower triangle\n");
       return 1;
     }
@@ -109,10 +110,10 @@ int check(int T, int nb, int P, int Q, int rank, int k, int J0, int npan, int in
     const int J = J0 + i * Q;
     for (int I = J; I < L.sb_end(k); ++I)
       if (I % P == L.p)
-        for (int rt = 0; rt < nb / 64; ++rt)
-          for (int ct = 0; ct < nb / 64; ++ct)
-            if (I > J || rt >= ct) ++expect;
-    if (L.has_z()) expect += (int64_t)(ZR / 64) * (nb / 64);
+        for (int rt = 0; rt < nb / BM; ++rt)
+          for (int ct = 0; ct < nb / BN; ++ct)
+            if (I > J || rt * BM + BM > ct * BN) ++expect;  // not strictly above the diagonal
+    if (L.has_z()) expect += (int64_t)(ZR / BM) * (nb / BN);
   }
   if ((int64_t)seen.size() != expect) {
     printf("count %lld != %lld (T=%d nb=%d P=%d Q=%d rank=%d k=%d J0=%d npan=%d)\n", (long long)seen.size(),
@@ -176,10 +177,14 @@ int main() {
               std::vector<int64_t> offs;
               Layout L = grid_layout(T, nb, P, Q, rank, ind, offs);
               const int e = L.sb_end(k);
-              if (L.owns(k + 1) && k + 1 < e) bad += check(T, nb, P, Q, rank, k, k + 1, 1, ind);
+              if (L.owns(k + 1) && k + 1 < e)
+                bad += check<64, 64>(T, nb, P, Q, rank, k, k + 1, 1, ind) +
+                       check<64, 128>(T, nb, P, Q, rank, k, k + 1, 1, ind);
               const int J0 = L.first_owned_from(L.owns(k + 1) ? k + 2 : k + 1);
               const int npan = J0 < e ? (e - 1 - J0) / Q + 1 : 0;
-              if (npan > 0) bad += check(T, nb, P, Q, rank, k, J0, npan, ind);
+              if (npan > 0)
+                bad += check<64, 64>(T, nb, P, Q, rank, k, J0, npan, ind) +
+                       check<64, 128>(T, nb, P, Q, rank, k, J0, npan, ind);  // the trailing-update tile
               n += 2;
             }
         }

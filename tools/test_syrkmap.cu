@@ -165,6 +165,7 @@ int main() {
             const int npan = J0 < T ? (T - 1 - J0) / world + 1 : 0;
             if (npan > 0) {
               bad += check<64, 64>(T, nb, world, rank, k, J0, npan);
+              bad += check<64, 128>(T, nb, world, rank, k, J0, npan);  // the trailing-update kernel's tile
               bad += check<128, 128>(T, nb, world, rank, k, J0, npan);
             }
             n += 2;
@@ -199,6 +200,7 @@ int main() {
             const int npan = T - J0;
             if (npan <= 0) continue;
             bad += check<64, 64>(T, nb, 1, 0, k, J0, npan, 0, group);
+            bad += check<64, 128>(T, nb, 1, 0, k, J0, npan, 0, group);
             bad += check<128, 64>(T, nb, 1, 0, k, J0, npan, 0, group);
             bad += check<64, 64>(T, nb, 1, 0, k, J0, npan, (int64_t)((J0 + npan) * nb), group);
             n += 3;
