@@ -421,8 +421,8 @@ def run_gpu(args):
             "cholesky_frac_fp64_peak": chol_tf / FP64_PEAK_TFLOPS,
             "cholesky_frac_cublas_dgemm": chol_tf / DGEMM_TFLOPS,
             "roofline": {"bound": "tensor",
-                         "kernel": "gemm_nt_dmma<SyrkMap> (trailing update: bulk U2 + lookahead U1 launches, "
-                                   "union of their spans)",
+                         "kernel": "trail_update_kernel<SyrkMap> (trailing update, CUTLASS DMMA mainloop: bulk "
+                                   "U2 + lookahead U1 launches, union of their spans)",
                          "u2_only": {"achieved": u2_tf, "frac": (u2_tf / FP64_PEAK_TFLOPS) if u2_tf else None,
                                      "note": "U2 flops over U2 spans; U1 and the panel chain share the GPU "
                                              "during them"},

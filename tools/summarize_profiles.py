@@ -28,9 +28,9 @@ PROF = os.path.join(ROOT, "profiles")
 
 def kernel_class(name: str) -> str:
     if "SyrkMap" in name:
-        return "gemm_nt_dmma<SyrkMap> (trailing update U1/U2)"
+        return "trail_update_kernel<SyrkMap> (trailing update U1/U2)"
     if "DenseMap" in name:
-        return "gemm_nt_dmma<DenseMap> (panel update / TRSM)"
+        return "panel_gemm_kernel / gemm_nt_dmma<DenseMap> (panel update / TRSM)"
     return name.split("(")[0].replace("exageo::<unnamed>::", "").replace("void ", "")[:60]
 
 
@@ -99,7 +99,7 @@ def summarize_full(path: str, rnd: str, n: int, nb: int):
     flops = 2.0 * nb * (m * (m + 1) / 2 + m)
     out = os.path.join(PROF, f"{rnd}_u2_full_summary.txt")
     with open(out, "w") as f:
-        f.write(f"# ncu --set full --clock-control none, kernel gemm_nt_dmma<SyrkMap> U2(0) at n={n}, nb={nb}\n")
+        f.write(f"# ncu --set full --clock-control none, kernel trail_update_kernel<SyrkMap> U2(0) at n={n}, nb={nb}\n")
         for h in METRICS:
             if h in got:
                 f.write(f"{h:80s} {got[h][0]:>18s} {got[h][1]}\n")
