@@ -213,42 +213,6 @@ __device__ __forceinline__ void tile_trsm(double* A, int64_t ld, const double* W
 }
 // C (global, ld) -= A B^T with A, B in shared memory; diagonal tile (A == B): skip the warp
 // tiles above the diagonal.
-// Pool GEMM task: A_ij -= L_ik L_jk^T with the operands staged in four 16-column K chunks (one
-// cp.async group each, A and B chunk q together) and the DMMA work of chunk q started as soon as
-// it has landed, so the L2 -> shared transfer of the later chunks overlaps the products.
-__device__ __forceinline__ void tile_update_pipelined(double* C, int64_t ldc, const double* A, int64_t lda,
-                                                      const double* B, int64_t ldb, bool diag, double* As,
-                                                      double* Bs) {
-  const bool same = A == B;
-  const int tid = threadIdx.x;
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-#pragma unroll
-    for (int u = 2 * q; u < 2 * q + 2; ++u) {
-      const int idx = tid + 256 * u, r2 = idx & 31, c = idx >> 5;  // c in [16 q, 16 q + 16)
-      cp_async16(As + c * LDS + 2 * r2, A + (int64_t)c * lda + 2 * r2);
-      if (!same) cp_async16(Bs + c * LDS + 2 * r2, B + (int64_t)c * ldb + 2 * r2);
-    }
-    asm volatile("cp.async.commit_group;\n" ::: "memory");
-  }
-  const bool active = !(diag && frag_upper());
-  Frag f;
-  if (active) frag_load(f, C, ldc);
-  const double* Bsrc = same ? As : Bs;
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    switch (q) {
-      case 0: asm volatile("cp.async.wait_group 3;\n" ::: "memory"); break;
-      case 1: asm volatile("cp.async.wait_group 2;\n" ::: "memory"); break;
-      case 2: asm volatile("cp.async.wait_group 1;\n" ::: "memory"); break;
-      default: asm volatile("cp.async.wait_group 0;\n" ::: "memory"); break;
-    }
-    __syncthreads();  // chunk q of every thread's copies is in shared memory
-    if (active) frag_mma_at(f, As, Bsrc, -1.0, frag_r0(), frag_c0(), 16 * q, 16 * q + 16);
-  }
-  if (active) frag_store(f, C, ldc);
-}
-
 __device__ __forceinline__ void tile_update(double* C, int64_t ldc, const double* As, const double* Bs, bool diag) {
   if (diag && frag_upper()) return;
   Frag f;
@@ -687,9 +651,11 @@ __device__ void pool_cta(const DagArgs& a, int* st, int* zs, double* sm) {
       case kGemm: {
         int64_t ldi, ldj;
         double* Aij = tile_ptr(a, i, j, ld);
-        const double* Lik = tile_ptr(a, i, k, ldi);
-        const double* Ljk = i != j ? tile_ptr(a, j, k, ldj) : Lik;
-        tile_update_pipelined(Aij, ld, Lik, ldi, Ljk, i != j ? ldj : ldi, i == j, As, Bs);
+        stage_tile(As, tile_ptr(a, i, k, ldi), ldi);
+        if (i != j) stage_tile(Bs, tile_ptr(a, j, k, ldj), ldj);
+        asm volatile("cp.async.wait_all;\n" ::: "memory");
+        __syncthreads();
+        tile_update(Aij, ld, As, i != j ? Bs : As, i == j);
         flag = st + (i * a.nt + j) * kPad;
         break;
       }
