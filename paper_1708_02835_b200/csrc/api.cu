@@ -275,7 +275,7 @@ bool tile_tasks_eligible(const exageo_ctx* c, int64_t n) {
 }
 
 // Tail hand-off: when the stream schedule runs a single-rank factorization, its last panels
-// (trailing size <= kTailN) are bound by the panel chain -- each step's trailing update is
+// (trailing size <= 2900) are bound by the panel chain -- each step's trailing update is
 // shorter than F(k+1) -- so the executor factors that trailing matrix instead. Returns the
 // first panel it takes (0: no hand-off). EXAGEO_TAIL_N overrides the size (0 disables).
 int tail_stop(const exageo_ctx* c, const Layout& G) {
@@ -283,7 +283,7 @@ int tail_stop(const exageo_ctx* c, const Layout& G) {
   if (tile_tasks_eligible(c, G.n)) return 0;  // the executor runs the whole factorization
   static const int64_t tail_n = [] {
     const char* e = getenv("EXAGEO_TAIL_N");
-    return e ? (int64_t)atoll(e) : (int64_t)2560;
+    return e ? (int64_t)atoll(e) : (int64_t)2900;  // sweeps: 8192 best at 2560 rows, 10k at 2832 (profiles/r02_tail_sweep.txt)
   }();
   if (tail_n <= 0) return 0;
   int k = (int)((G.n - tail_n + G.nb - 1) / G.nb);  // first panel whose trailing size <= tail_n
