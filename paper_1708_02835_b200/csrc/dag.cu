@@ -157,17 +157,25 @@ __device__ __forceinline__ void frag_store(const Frag& f, double* C, int64_t ldc
 #pragma unroll
       for (int e = 0; e < 2; ++e) C[(int64_t)(c0 + 8 * nt + 2 * fk + e) * ldc + r0 + 8 * mt + fr] = f.v[mt][nt][e];
 }
-// f += sgn * A[r0:, kbeg:kend] B[c0:, kbeg:kend]^T for the 32 x 16 block at (r0, c0)
-__device__ __forceinline__ void frag_mma_at(Frag& f, const double* As, const double* Bs, double sgn, int r0, int c0,
-                                            int kbeg, int kend) {
+// f = -f (exact; lets every product accumulate with +: C - A B^T = -(-C + A B^T), same bits)
+__device__ __forceinline__ void frag_neg(Frag& f) {
+#pragma unroll
+  for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) f.v[mt][nt][0] = -f.v[mt][nt][0], f.v[mt][nt][1] = -f.v[mt][nt][1];
+}
+// f += A[r0:, kbeg:kend] B[c0:, kbeg:kend]^T for the 32 x 16 block at (r0, c0); kend - kbeg a
+// multiple of 16
+__device__ __forceinline__ void frag_mma_at(Frag& f, const double* As, const double* Bs, int r0, int c0, int kbeg,
+                                            int kend) {
   const int lane = threadIdx.x & 31, fr = lane >> 2, fk = lane & 3;
-#pragma unroll 4
+#pragma unroll 8
   for (int kk = kbeg; kk < kend; kk += 4) {
     const double* as = As + (kk + fk) * LDS + r0 + fr;
     const double* bs = Bs + (kk + fk) * LDS + c0 + fr;
     double af[4], bf[2];
 #pragma unroll
-    for (int mt = 0; mt < 4; ++mt) af[mt] = sgn * as[8 * mt];
+    for (int mt = 0; mt < 4; ++mt) af[mt] = as[8 * mt];
 #pragma unroll
     for (int nt = 0; nt < 2; ++nt) bf[nt] = bs[8 * nt];
 #pragma unroll
@@ -176,16 +184,16 @@ __device__ __forceinline__ void frag_mma_at(Frag& f, const double* As, const dou
       for (int nt = 0; nt < 2; ++nt) dmma64(f.v[mt][nt], af[mt], bf[nt]);
   }
 }
-// f += sgn * A[:, 0:kend] B[:, 0:kend]^T (A, B shared, ld LDS)
-__device__ __forceinline__ void frag_mma(Frag& f, const double* As, const double* Bs, double sgn, int kend) {
+// f += A[:, 0:kend] B[:, 0:kend]^T (A, B shared, ld LDS) for this warp's block
+__device__ __forceinline__ void frag_mma(Frag& f, const double* As, const double* Bs, int kend) {
   const int lane = threadIdx.x & 31, fr = lane >> 2, fk = lane & 3, r0 = frag_r0(), c0 = frag_c0();
-#pragma unroll 4
+#pragma unroll 8
   for (int kk = 0; kk < kend; kk += 4) {
     const double* as = As + (kk + fk) * LDS + r0 + fr;
     const double* bs = Bs + (kk + fk) * LDS + c0 + fr;
     double af[4], bf[2];
 #pragma unroll
-    for (int mt = 0; mt < 4; ++mt) af[mt] = sgn * as[8 * mt];
+    for (int mt = 0; mt < 4; ++mt) af[mt] = as[8 * mt];
 #pragma unroll
     for (int nt = 0; nt < 2; ++nt) bf[nt] = bs[8 * nt];
 #pragma unroll
@@ -206,7 +214,7 @@ __device__ __forceinline__ void tile_trsm(double* A, int64_t ld, const double* W
   frag_zero(f);
   asm volatile("cp.async.wait_all;\n" ::: "memory");
   __syncthreads();
-  frag_mma(f, X, Ws, 1.0, frag_c0() + 16);
+  frag_mma(f, X, Ws, frag_c0() + 16);
   __syncthreads();  // every warp has read X
   frag_store(f, A, ld);
   frag_store(f, X, LDS);
@@ -217,7 +225,9 @@ __device__ __forceinline__ void tile_update(double* C, int64_t ldc, const double
   if (diag && frag_upper()) return;
   Frag f;
   frag_load(f, C, ldc);
-  frag_mma(f, As, Bs, -1.0, PB);
+  frag_neg(f);
+  frag_mma(f, As, Bs, PB);
+  frag_neg(f);
   frag_store(f, C, ldc);
 }
 
@@ -469,7 +479,7 @@ __device__ void chain_cta(const DagArgs& a, int* st, double* sm) {
     const unsigned long long t3 = a.trace ? gtimer() : 0;
     Frag f;
     frag_zero(f);
-    frag_mma(f, X, Ws, 1.0, frag_c0() + 16);
+    frag_mma(f, X, Ws, frag_c0() + 16);
     __syncthreads();  // every warp has read X
     frag_store(f, Ab, ldb);
     frag_store(f, X, LDS);
@@ -496,7 +506,7 @@ __device__ void chain_cta(const DagArgs& a, int* st, double* sm) {
       double* part = sm + PB * LDA2;  // W region: 2 partial blocks x 32 lanes x 16 values
       if (warp == 4 || warp == 6) {
         frag_zero(f);
-        frag_mma_at(f, X, X, -1.0, 32, warp == 4 ? 48 : 32, 32, PB);
+        frag_mma_at(f, X, X, 32, warp == 4 ? 48 : 32, 32, PB);
         double* pp = part + (warp == 4 ? 0 : 512) + lane * 16;
 #pragma unroll
         for (int mt = 0; mt < 4; ++mt)
@@ -507,7 +517,8 @@ __device__ void chain_cta(const DagArgs& a, int* st, double* sm) {
           }
       } else {
         frag_load_s(f, Y);
-        frag_mma(f, X, X, -1.0, (warp == 5 || warp == 7) ? 32 : PB);
+        frag_neg(f);
+        frag_mma(f, X, X, (warp == 5 || warp == 7) ? 32 : PB);
       }
       __syncthreads();
       if (warp == 5 || warp == 7) {
@@ -520,7 +531,10 @@ __device__ void chain_cta(const DagArgs& a, int* st, double* sm) {
             f.v[mt][nt][1] += pp[4 * mt + 2 * nt + 1];
           }
       }
-      if (!frag_upper()) frag_store(f, sm, LDA2);
+      if (!frag_upper()) {
+        frag_neg(f);
+        frag_store(f, sm, LDA2);
+      }
     }
     __syncthreads();
     rec(3 * k + 2, t4, t5);
