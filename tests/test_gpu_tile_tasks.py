@@ -151,3 +151,30 @@ def test_tail_handoff_matches_oracle():
         r2 = c.loglik(x, y, z, theta)
     assert r.loglik == r2.loglik
     assert_ll(r.loglik, oracle.loglik(x, y, z, theta), n)
+
+
+def test_tile_tasks_fuzz_against_stream_schedule():
+    """Randomised n (1 .. 3200, ragged and tile-aligned) and theta: the
+    executor (one persistent kernel, device-side list schedule, per-tile version counters)
+    against the stream schedule on the same inputs, and bitwise against itself on a repeat --
+    a scheduling race (a task reading a tile before its inputs are final) would show as a
+    mismatch in some draw."""
+    rng = np.random.default_rng(2024)
+    ns = sorted(set([1, 63, 64, 65, 129, 1024, 3200] + [int(v) for v in rng.integers(2, 3201, 14)]))
+    with ex.Context(device=0, tile_tasks=1) as ce, ex.Context(device=0, tile_tasks=-1) as cs:
+        for n in ns:
+            x, y = ex.gen_locations(n, n + 7)
+            z = si.normals(n, n + 8)
+            # well conditioned part of the MLE box (the ill-conditioned part: test_gpu_edge.py)
+            theta = (float(rng.uniform(0.3, 3.0)), float(rng.uniform(0.02, 0.15)), float(rng.uniform(0.3, 1.0)))
+            try:
+                a = ce.loglik(x, y, z, theta)
+            except ex.NotPositiveDefinite:
+                with pytest.raises(ex.NotPositiveDefinite):
+                    cs.loglik(x, y, z, theta)
+                continue
+            b = cs.loglik(x, y, z, theta)
+            again = ce.loglik(x, y, z, theta)
+            assert again.loglik == a.loglik, (n, theta)
+            scale = max(abs(b.loglik), 0.5 * abs(b.logdet), 0.5 * b.quad, 0.5 * n * 1.8378770664093453)
+            assert abs(a.loglik - b.loglik) <= 1e-10 * scale, (n, theta, a.loglik, b.loglik)
