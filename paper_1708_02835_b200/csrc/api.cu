@@ -1270,6 +1270,7 @@ exageo_status exageo_create(exageo_ctx** out, const exageo_opts* opts) {
   if ((e = gemm_init()) != cudaSuccess) return bail(e, "gemm_init");
   if ((e = potrf_init()) != cudaSuccess) return bail(e, "potrf_init");
   if ((e = dag_init()) != cudaSuccess) return bail(e, "dag_init");
+  if ((e = trsv_init()) != cudaSuccess) return bail(e, "trsv_init");
   if (o.stream) {
     c->stream = (cudaStream_t)o.stream;
   } else {

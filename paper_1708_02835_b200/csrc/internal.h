@@ -140,6 +140,7 @@ struct MaternConsts {
 // Set kernel attributes (dynamic shared memory) on the current device.
 cudaError_t gemm_init();
 cudaError_t potrf_init();
+cudaError_t trsv_init();
 
 // ---- launchers (all asynchronous on `s`) ----
 // K1T: per-theta Chebyshev table of the Matern function for general nu (matern.cu);

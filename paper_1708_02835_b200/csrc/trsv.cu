@@ -208,6 +208,16 @@ __global__ void var_from_acc_kernel(const double* __restrict__ acc, int cols, do
 
 }  // namespace
 
+// tile_solve_kernel keeps the nb-entry right-hand side and a 64 x 65 block in shared memory:
+// above 48 KB (nb > 1984, e.g. the automatic nb = 2048 of n >= 56k) it needs the opt-in limit
+// (200 KB: nb up to 21k).
+cudaError_t trsv_init() {
+  cudaError_t e = cudaFuncSetAttribute(tile_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(diag_solve_cols_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)(kRhs * 1024 * sizeof(double)));
+}
+
 void launch_add_block(double* dst, int64_t ldd, const double* src, int64_t lds, int rows, int cols, cudaStream_t s) {
   if (rows <= 0 || cols <= 0) return;
   add_block_kernel<<<dim3((rows + 255) / 256, cols), 256, 0, s>>>(dst, ldd, src, lds, rows, cols);

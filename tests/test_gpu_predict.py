@@ -131,3 +131,20 @@ def test_predict_var_distributed_virtual_ranks(world, P, n, nb):
     ref = oracle.predict_var(x, y, xn, yn, theta)
     assert np.abs(var - ref).max() <= 1e-9 * theta[0]
     assert abs(var[-2]) <= 1e-9 * theta[0] and var[-1] == theta[0]
+
+
+@pytest.mark.parametrize("nb", [1024, 2048])
+def test_predict_wide_tiles(nb):
+    """The automatic tile size of large single-GPU problems (nb = 2048 from n = 56k): the backward
+    solve's diagonal-tile kernel needs more than 48 KB of shared memory there (regression: an
+    n = 144k predict failed with 'invalid argument' before the opt-in)."""
+    n, m = 5000, 20
+    x, y = ex.gen_locations(n, 41)
+    z = si.normals(n, 42)
+    theta = (1.0, 0.1, 0.5)
+    rng = np.random.default_rng(nb)
+    xn, yn = rng.random(m), rng.random(m)
+    with ex.Context(device=0, nb=nb) as c:
+        got = c.predict(x, y, z, xn, yn, theta)
+    ref = oracle.predict(x, y, z, xn, yn, theta)
+    np.testing.assert_allclose(got, ref, rtol=1e-9, atol=1e-10)
