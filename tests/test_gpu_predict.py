@@ -138,7 +138,7 @@ def test_predict_wide_tiles(nb):
     """The automatic tile size of large single-GPU problems (nb = 2048 from n = 56k): the backward
     solve's diagonal-tile kernel needs more than 48 KB of shared memory there (regression: an
     n = 144k predict failed with 'invalid argument' before the opt-in)."""
-    n, m = 5000, 20
+    n, m = 2500, 20
     x, y = ex.gen_locations(n, 41)
     z = si.normals(n, 42)
     theta = (1.0, 0.1, 0.5)
