@@ -163,6 +163,10 @@ int main(int argc, char** argv) {
             if (d > mdu) mdu = d;
             continue;
           }
+          // identity padding (rows / columns >= n): never touched in a real layout (their panel
+          // rows are zero); the synthetic fill here is not zero there, so the 64- and 128-wide
+          // tiles' different skip boundaries show
+          if ((int64_t)J * nb + cc >= L.n || (lr < L.lrows(J) && (int64_t)J * nb + lr >= L.n)) continue;
           ++nlow;
           if (d > md) md = d;
           if (fabs(h1[i]) > mx) mx = fabs(h1[i]);
