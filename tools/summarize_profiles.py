@@ -154,9 +154,39 @@ def summarize_aux(paths, rnd: str):
     print(open(out).read())
 
 
+def summarize_mid(items, rnd: str):
+    """U2(0) captures at mid n (tools/r02_mid_profiles.sh): n:nb:path triples -> one table."""
+    out = os.path.join(PROF, f"{rnd}_u2_mid_summary.txt")
+    keys = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+            "sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active", "launch__grid_size"]
+    unit_scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+    tscale = {"nsecond": 1e-9, "ns": 1e-9, "usecond": 1e-6, "us": 1e-6, "msecond": 1e-3, "ms": 1e-3, "second": 1.0}
+    with open(out, "w") as f:
+        f.write("# ncu --set full --clock-control none, trail_update_kernel<SyrkMap> U2(0) (panel 0 updating panels\n"
+                "# 2..T-1) at mid n; algorithmic flops 2 nb (m(m+1)/2 + m), algorithmic C bytes 16 m(m+1)/2,\n"
+                "# m = n - 2 nb. DRAM bytes per algorithmic flop fall with K = nb (the delayed-update lever).\n")
+        f.write(f"{'n':>6s} {'nb':>5s} {'grid':>7s} {'time ms':>9s} {'TF/s':>6s} {'DMMA pipe':>9s} "
+                f"{'DRAM GB':>8s} {'C alg GB':>8s} {'B/flop':>7s}\n")
+        for n, nb, path in items:
+            n, nb = int(n), int(nb)
+            raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
+                                 text=True).stdout
+            rows = list(csv.reader(raw.splitlines()))
+            got = {h: (v.replace(",", ""), u) for h, u, v in zip(rows[0], rows[1], rows[2]) if h in keys}
+            dur = float(got[keys[0]][0]) * tscale.get(got[keys[0]][1], 1e-9)
+            dram = sum(float(got[k][0]) * unit_scale.get(got[k][1], 1) for k in keys[1:3])
+            m = n - 2 * nb
+            flops = 2.0 * nb * (m * (m + 1) / 2 + m)
+            f.write(f"{n:6d} {nb:5d} {got[keys[4]][0]:>7s} {dur * 1e3:9.3f} {flops / dur / 1e12:6.2f} "
+                    f"{float(got[keys[3]][0]):8.1f}% {dram / 1e9:8.3f} {16 * m * (m + 1) / 2 / 1e9:8.3f} "
+                    f"{dram / flops:7.4f}\n")
+    print(open(out).read())
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--aux", nargs="*", default=None, help="label::path.ncu-rep pairs for summarize_aux")
+    ap.add_argument("--mid", nargs="*", default=None, help="n:nb:path.ncu-rep triples for summarize_mid")
     ap.add_argument("--round", default="r01")
     ap.add_argument("--launches", default=os.path.join(ROOT, "gpurun_out", "launches_bench.csv"))
     ap.add_argument("--full", default=os.path.join(ROOT, "gpurun_out", "prof_u2_100k.ncu-rep"))
@@ -164,6 +194,9 @@ def main():
     ap.add_argument("--nb", type=int, default=512)
     a = ap.parse_args()
     os.makedirs(PROF, exist_ok=True)
+    if a.mid:
+        summarize_mid([tuple(x.split(":", 2)) for x in a.mid], a.round)
+        return
     if a.aux:
         summarize_aux([tuple(x.split("::", 1)) for x in a.aux], a.round)
         return
