@@ -54,6 +54,7 @@ def _flags(src: str) -> list[str]:
     if src == "gemm_dmma.cu":
         f += ["-I", cutlass_include()]
     f += ARCH
+    f += os.environ.get("EXAGEO_EXTRA_NVCC_FLAGS", "").split()  # development builds (e.g. -DEXAGEO_POTRF_TRACE)
     if src.endswith(".cu"):
         f += ["-Xptxas", "-warn-spills"]
     return f

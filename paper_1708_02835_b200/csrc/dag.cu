@@ -40,6 +40,9 @@ namespace exageo {
 namespace {
 
 #include "potrf64.cuh"
+#ifdef EXAGEO_POTRF_TRACE  // development: the chain's K2 strip stamps of step 6 (tools/chain_k2_trace.py)
+__device__ long long g_potrf_snap[64];
+#endif
 
 constexpr int LDS = PB + 4;  // shared leading dimension of staged tiles (4 mod 16 doubles)
 constexpr int kTileSmem = 2 * PB * LDS;
@@ -461,6 +464,10 @@ __device__ void chain_cta(const DagArgs& a, int* st, double* sm) {
       asm volatile("cp.async.wait_all;\n" ::: "memory");
       return;
     }
+#ifdef EXAGEO_POTRF_TRACE
+    if (k == 6 && threadIdx.x == 0)
+      for (int i = 0; i < 64; ++i) g_potrf_snap[i] = g_potrf_trace[i];
+#endif
     release_by(0, stf(k, k), k + 2);  // body ended with a barrier: L_kk, W_k stored
     rec(3 * k, t0, t0);
     if (last) break;
@@ -868,3 +875,9 @@ void dag_args_with_theta(const void* args, const MaternConsts& mc, std::vector<c
 }
 
 }  // namespace exageo
+
+#ifdef EXAGEO_POTRF_TRACE
+extern "C" int exageo_dbg_chain_potrf_trace(long long* out) {
+  return (int)cudaMemcpyFromSymbol(out, exageo::g_potrf_snap, 64 * sizeof(long long));
+}
+#endif

@@ -103,13 +103,13 @@ __device__ __forceinline__ void acc_store(const double (&acc)[2][2][2], F C) {
 // pivot. Returns the first bad pivot (strip-local) or -1 (same in every factor warp).
 constexpr int NFW = 3;  // factor warps
 
-template <int H>
-__device__ __forceinline__ int factor_strip(double* As, double* dv, double* rs, double* colbuf,
-                                            double* __restrict__ a, int64_t lda) {
-  constexpr int c0 = PB - H;
+// One instantiation for the four strips (runtime K): the unrolled pivot loop exists once in the
+// binary -- four copies pushed the persistent tile-task kernel's K2 out of the instruction cache.
+__device__ __forceinline__ int factor_strip(const int K, double* As, double* dv, double* rs, double* colbuf) {
+  const int c0 = 16 * K, H = PB - c0;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  constexpr int NW = (H - 16) / 16 > 0 ? (H - 16) / 16 : 1;  // factor warps with rows in this strip
-  if constexpr (c0 > 0) {
+  const int NW = H > 32 ? (H - 16) / 16 : 1;  // factor warps with rows in this strip
+  if (c0 > 0) {
     if (16 * w < H) {  // this warp's 16 strip rows of the update
       const int fr = lane >> 2, fk = lane & 3;
       const int rb = c0 + 16 * w;
@@ -120,7 +120,7 @@ __device__ __forceinline__ int factor_strip(double* As, double* dv, double* rs, 
         for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
           for (int e = 0; e < 2; ++e) acc[mt][nt][e] = As[(c0 + 8 * nt + 2 * fk + e) * LDA2 + rb + 8 * mt + fr];
-#pragma unroll
+#pragma unroll 4
       for (int kk = 0; kk < c0; kk += 4) {
         const double* col = As + (kk + fk) * LDA2 + fr;
         double af[2], bf[2];
@@ -159,22 +159,31 @@ __device__ __forceinline__ int factor_strip(double* As, double* dv, double* rs, 
     long long tj[17];
     tj[0] = clock64();
 #endif
+    // software-pipelined: the broadcast and reciprocal of pivot j+1 are issued as soon as its
+    // diagonal is known, ahead of pivot j's remaining row updates (which fill their latency)
+    double d = __shfl_sync(0xffffffffu, dn, 0);
+    double rd = rcp_nr(d);
+    double dm = 1.0;  // lane j < 16: its own pivot d_j
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
-      const double d = __shfl_sync(0xffffffffu, dn, j);
       dd[j] = d;
+      dm = (lane == j) ? d : dm;
       bad = (bad < 0 && !(d > 0.0)) ? j : bad;
-      const double rd = rcp_nr(d);
       const double f = (r > j) ? v[j] * rd : 0.0;
       const double* cj = cb + 16 * (j & 1);  // a_cj, c = 0..15, of the diagonal block
+      double d_next = 0.0, rd_next = 0.0;
       if (j + 1 < 16) {
         dn = fma(-f, v[j], v[j + 1]);  // lane j+1: a_{j+1,j+1} - f a_{j+1,j}, lane-local
+        d_next = __shfl_sync(0xffffffffu, dn, j + 1);
+        rd_next = rcp_nr(d_next);
         v[j + 1] = fma(-f, cj[j + 1], v[j + 1]);
         if (lane < 16) cb[16 * ((j + 1) & 1) + lane] = v[j + 1];  // column j+1 for the next pivot
       }
 #pragma unroll
       for (int c = j + 2; c < 16; ++c) v[c] = fma(-f, cj[c], v[c]);
       __syncwarp();
+      d = d_next;
+      rd = rd_next;
 #ifdef EXAGEO_POTRF_TRACE
       tj[j + 1] = clock64();
 #endif
@@ -183,27 +192,25 @@ __device__ __forceinline__ int factor_strip(double* As, double* dv, double* rs, 
     if (c0 == 0 && lane == 0 && w == 0)
       for (int j = 0; j < 16; ++j) g_potrf_trace[32 + j] = tj[j + 1] - tj[j];
 #endif
-    // 1/sqrt(d_j) by lane j (own pivot), shared through rs; then L_rc = a_rc / sqrt(d_c) below
-    // the diagonal, L_cc = d_c / sqrt(d_c), zeros above -- into As and straight to global memory
-    double dm = dd[0];
-#pragma unroll
-    for (int j = 1; j < 16; ++j) dm = (lane == j) ? dd[j] : dm;
+    // 1/sqrt(d_j) by lane j (own pivot), shared within the warp by shuffles (warp 0 also
+    // publishes d_j and 1/sqrt(d_j) for the helper warps); then L_rc = a_rc / sqrt(d_c) below
+    // the diagonal, L_cc = d_c / sqrt(d_c), zeros above -- into As (helper warp 7 copies the strip
+    // to global memory: no global stores queue up in front of the factor warps' loads)
+    const double ism = rsqrt_nr(dm);
     if (lane < 16 && w == 0) {
       dv[c0 + lane] = dm;
-      rs[c0 + lane] = rsqrt_nr(dm);
+      rs[c0 + lane] = ism;
     }
-    named_sync(6, 32 * NFW);
+    double isv[16];
+#pragma unroll
+    for (int c = 0; c < 16; ++c) isv[c] = __shfl_sync(0xffffffffu, ism, c);
     if (valid && (lane >= 16 || w == 0)) {
 #pragma unroll
       for (int c = 0; c < 16; ++c) {
-        const double is = rs[c0 + c];
-        const double l = (r > c) ? v[c] * is : ((r == c) ? dd[c] * is : 0.0);
+        const double l = (r > c) ? v[c] * isv[c] : ((r == c) ? dd[c] * isv[c] : 0.0);
         As[(c0 + c) * LDA2 + c0 + r] = l;
-        a[(int64_t)(c0 + c) * lda + c0 + r] = l;
       }
     }
-  } else {
-    named_sync(6, 32 * NFW);
   }
   named_sync(6, 32 * NFW);
   return bad;
@@ -215,7 +222,8 @@ __device__ __forceinline__ int factor_strip(double* As, double* dv, double* rs, 
 // non-positive (or NaN) pivot as a global index (R14; every later kernel reads info and exits).
 //   warps 0..2: the four strips in order (factor_strip), announcing strip K on named barrier 1+K;
 //   warps 3..7: after strip K, T_K = L_KK^{-1} (warp 3, per-lane column substitution) and the
-//               W row block K: W_KC = -T_K G_KC, G_KC = sum_{M=C}^{K-1} L_KM W_MC (warp 4+C);
+//               W row block K: W_KC = -T_K G_KC, G_KC = sum_{M=C}^{K-1} L_KM W_MC (warp 5, 6, 4
+//               for C = 0, 1, 2);
 //               they trail the factor warps by about one strip, off their critical path.
 // Called by all 256 threads of a CTA with kPotrfSmemDoubles of shared memory at smem_p.
 // Loads the block with L1-bypassing loads (ld.global.cg): in the tile-task kernel (dag.cu)
@@ -267,13 +275,7 @@ __device__ __forceinline__ bool potrf64_body(double* __restrict__ a, int64_t lda
     int first = -1;
 #pragma unroll 1
     for (int K = 0; K < nstrips; ++K) {
-      int b;
-      switch (K) {
-        case 0: b = factor_strip<64>(As, dv, rs, colbuf, a, lda); break;
-        case 1: b = factor_strip<48>(As, dv, rs, colbuf, a, lda); break;
-        case 2: b = factor_strip<32>(As, dv, rs, colbuf, a, lda); break;
-        default: b = factor_strip<16>(As, dv, rs, colbuf, a, lda); break;
-      }
+      const int b = factor_strip(K, As, dv, rs, colbuf);
       if (first < 0 && b >= 0) first = 16 * K + b;
       PTRACE(2 + K);
       named_arrive(1 + K, 256);
@@ -281,13 +283,6 @@ __device__ __forceinline__ bool potrf64_body(double* __restrict__ a, int64_t lda
     if (tid == 0 && first >= 0) badj = first;
   } else {
     constexpr int NH = 256 - 32 * NFW;  // helper threads
-    // zeros above the diagonal blocks (rows 0 .. 16K-1 of column block K), as a dpotrf leaves them
-    for (int idx = tid - 32 * NFW; idx < 16 * 16 * 6; idx += NH) {
-      const int K = idx < 256 ? 1 : (idx < 768 ? 2 : 3);
-      const int base = K == 1 ? 0 : (K == 2 ? 256 : 768);
-      const int r = (idx - base) % (16 * K), c = 16 * K + (idx - base) / (16 * K);
-      a[(int64_t)c * lda + r] = 0.0;
-    }
 #pragma unroll 1
     for (int K = 0; K < 4; ++K) {
       const int k0 = 16 * K;
@@ -301,6 +296,15 @@ __device__ __forceinline__ bool potrf64_body(double* __restrict__ a, int64_t lda
         continue;
       }
       named_sync(1 + K, 256);  // strip K is in As
+      // log-det terms of strip K on warp 4, beside T_K (warp 3) and the G products (warps 5, 6):
+      // off the tail after the last strip
+      if (warp == 4 && lane < 16) lgv[k0 + lane] = 0.5 * log(dv[k0 + lane]);
+      if (warp == 7) {  // L strip K (columns k0..k0+15; zeros above row k0, as a dpotrf leaves them) to global memory
+#pragma unroll 4
+        for (int c = k0; c < k0 + 16; ++c)
+          *reinterpret_cast<double2*>(a + (int64_t)c * lda + 2 * lane) =
+              2 * lane >= k0 ? *reinterpret_cast<const double2*>(As + c * LDA2 + 2 * lane) : make_double2(0.0, 0.0);
+      }
       if (warp == NFW && lane < 16) {  // column c = lane of T_K: t_r = (delta_rc - sum_{m<r} L_rm t_m) / L_rr
         const int c = lane;
         double acc[16], t[16];
@@ -320,7 +324,9 @@ __device__ __forceinline__ bool potrf64_body(double* __restrict__ a, int64_t lda
         }
       }
       double g[2][2][2] = {};
-      const int C = warp - NFW - 1;
+      // column block C of W row block K on warps 5, 6, 4 (C = 0, 1, 2): the heavy C = 0 and 1 off
+      // SMSP 0, which runs factor warp 0 -- the only factor warp of strips 2 and 3
+      const int C = warp == 5 ? 0 : (warp == 6 ? 1 : (warp == 4 ? 2 : -1));
       if (C >= 0 && C < K) {  // G_KC = sum_{M=C}^{K-1} L_KM W_MC
 #pragma unroll 1
         for (int M = C; M < K; ++M)
@@ -345,7 +351,6 @@ __device__ __forceinline__ bool potrf64_body(double* __restrict__ a, int64_t lda
         const int r = idx & 15, c = idx >> 4;
         W[c * PB + k0 + r] = (c < k0 + 16) ? Ws[c * LDA2 + k0 + r] : 0.0;
       }
-      if (warp == NFW && lane < 16) lgv[k0 + lane] = 0.5 * log(dv[k0 + lane]);
     }
     if (warp == 7) hook(4);
   }
