@@ -224,10 +224,15 @@ __device__ __forceinline__ void tile_trsm(double* A, int64_t ld, const double* W
 }
 // C (global, ld) -= A B^T with A, B in shared memory; diagonal tile (A == B): skip the warp
 // tiles above the diagonal.
+// The C fragments are loaded before the operand tiles' cp.async group is waited for (their
+// latencies overlap); the caller has issued the staging.
 __device__ __forceinline__ void tile_update(double* C, int64_t ldc, const double* As, const double* Bs, bool diag) {
-  if (diag && frag_upper()) return;
+  const bool skip = diag && frag_upper();
   Frag f;
-  frag_load(f, C, ldc);
+  if (!skip) frag_load(f, C, ldc);
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+  __syncthreads();
+  if (skip) return;
   frag_neg(f);
   frag_mma(f, As, Bs, PB);
   frag_neg(f);
@@ -674,8 +679,6 @@ __device__ void pool_cta(const DagArgs& a, int* st, int* zs, double* sm) {
         double* Aij = tile_ptr(a, i, j, ld);
         stage_tile(As, tile_ptr(a, i, k, ldi), ldi);
         if (i != j) stage_tile(Bs, tile_ptr(a, j, k, ldj), ldj);
-        asm volatile("cp.async.wait_all;\n" ::: "memory");
-        __syncthreads();
         tile_update(Aij, ld, As, i != j ? Bs : As, i == j);
         flag = st + (i * a.nt + j) * kPad;
         break;
