@@ -731,7 +731,13 @@ __device__ void pool_cta(const DagArgs& a, int* st, int* zs, double* sm) {
 // ordered by its start time in a simulated greedy list schedule on the other nproc - 1 CTAs
 // (priority: bottom level = cost of the longest path to the end; the chain tasks run on
 // their own processor in the simulation). Costs are rough measured durations in
-// microseconds (K2 ~13, a 64^3 DMMA tile ~3-5, a z-row task ~3); only proportions matter.
+// microseconds (tools/tile_task_trace.py at n = 1600, round 2: chain K2 10.5, chain TRSM / SYRK
+// 2.5 + staging; pool tasks' execution + the ~1 us release-to-poll latency); only proportions
+// and the chain : pool ratio matter. (A fused TRSM + GEMM + SYRK feeder task for the next chain
+// step, as a ticket or on a dedicated CTA, was slower from n = 1600 to 2400: it waits on the
+// previous versions of its tiles, which come from ordinary tickets.)
+constexpr float kCostPotrf = 10.5f, kCostChainTrsm = 2.5f, kCostChainSyrk = 3.f, kCostTrsm = 5.5f, kCostGemm = 6.5f,
+                kCostGen = 6.f, kCostGenZ = 1.f, kCostZ = 4.f;
 void dag_plan(int nt, int nproc, std::vector<int4>& order) {
   std::vector<int4> tk;
   std::vector<float> cost;
@@ -750,24 +756,24 @@ void dag_plan(int nt, int nproc, std::vector<int4>& order) {
   std::vector<int> genz(nt);
   for (int j = 0; j < nt; ++j) {  // GEN tasks: Sigma's tiles inside n and the z row (Alg. 2 l.2);
     // GEN(0, 0) belongs to the chain CTA (it generates A_00 into its shared memory)
-    for (int i = j; i < nt; ++i) gemm_prev[(size_t)i * nt + j] = add(kGen, i, j, 0, 1.5f, i == 0, {});
-    genz[j] = add(kGen, nt, j, 0, 0.5f, false, {});
+    for (int i = j; i < nt; ++i) gemm_prev[(size_t)i * nt + j] = add(kGen, i, j, 0, kCostGen, i == 0, {});
+    genz[j] = add(kGen, nt, j, 0, kCostGenZ, false, {});
   }
   for (int k = 0; k < nt; ++k) {
-    potrf[k] = add(kPotrf, k, k, k, 13.f, true, {gemm_prev[(size_t)k * nt + k]});
+    potrf[k] = add(kPotrf, k, k, k, kCostPotrf, true, {gemm_prev[(size_t)k * nt + k]});
     for (int i = k + 1; i < nt; ++i)
-      trsm[(size_t)i * nt + k] = add(kTrsm, i, k, k, i == k + 1 ? 2.f : 4.f, i == k + 1,
+      trsm[(size_t)i * nt + k] = add(kTrsm, i, k, k, i == k + 1 ? kCostChainTrsm : kCostTrsm, i == k + 1,
                                      {potrf[k], gemm_prev[(size_t)i * nt + k]});
-    ztrsm[k] = add(kZTrsm, nt, k, k, 3.f, false, {potrf[k], k > 0 ? zgemm[(size_t)k * nt + k - 1] : genz[k]});
+    ztrsm[k] = add(kZTrsm, nt, k, k, kCostZ, false, {potrf[k], k > 0 ? zgemm[(size_t)k * nt + k - 1] : genz[k]});
     for (int j = k + 1; j < nt; ++j)
       for (int i = j; i < nt; ++i) {
         const size_t ij = (size_t)i * nt + j;
         const bool ch = i == k + 1 && j == k + 1;
-        gemm_prev[ij] = add(kGemm, i, j, k, ch ? 2.5f : 5.f, ch,
+        gemm_prev[ij] = add(kGemm, i, j, k, ch ? kCostChainSyrk : kCostGemm, ch,
                             {trsm[(size_t)i * nt + k], i != j ? trsm[(size_t)j * nt + k] : -1, gemm_prev[ij]});
       }
     for (int j = k + 1; j < nt; ++j)
-      zgemm[(size_t)j * nt + k] = add(kZGemm, nt, j, k, 3.f, false,
+      zgemm[(size_t)j * nt + k] = add(kZGemm, nt, j, k, kCostZ, false,
                                       {ztrsm[k], trsm[(size_t)j * nt + k], k > 0 ? zgemm[(size_t)j * nt + k - 1] : genz[j]});
   }
   const int N = (int)tk.size();

@@ -52,3 +52,12 @@ for k in range(min(nt, 40)):
         e = chain.get((ty, k))
         cells.append(f"{e[0] / 1e3:8.2f} {e[1] / 1e3:8.2f} {e[2] / 1e3:8.2f}" if e else " " * 26)
     print(f"{k:4d}  " + " | ".join(cells))
+# the pool tasks that feed chain step k: TRSM(k+1, k-1) and the last updates of A_{k+1,k}, A_{k+1,k+1}
+print("feeders of step k: ticket [grab, ready, done] us for TRSM(k+1,k-1) | GEMM(k+1,k,k-1) | GEMM(k+1,k+1,k-1)")
+pool = {(ty, i, j, k): (t, g, rd, d) for t, ty, i, j, k, cta, g, rd, d in rows if t < chain_first}
+for k in range(1, min(nt - 1, 16)):
+    cells = []
+    for key in ((1, k + 1, k - 1, k - 1), (2, k + 1, k, k - 1), (2, k + 1, k + 1, k - 1)):
+        e = pool.get(key)
+        cells.append(f"#{e[0]:5d} {e[1] / 1e3:7.2f} {e[2] / 1e3:7.2f} {e[3] / 1e3:7.2f}" if e else " " * 30)
+    print(f"{k:4d}  " + " | ".join(cells))
