@@ -224,21 +224,6 @@ __device__ __forceinline__ void tile_trsm(double* A, int64_t ld, const double* W
 }
 // C (global, ld) -= A B^T with A, B in shared memory; diagonal tile (A == B): skip the warp
 // tiles above the diagonal.
-// The C fragments are loaded before the operand tiles' cp.async group is waited for (their
-// latencies overlap); the caller has issued the staging.
-__device__ __forceinline__ void tile_update(double* C, int64_t ldc, const double* As, const double* Bs, bool diag) {
-  const bool skip = diag && frag_upper();
-  Frag f;
-  if (!skip) frag_load(f, C, ldc);
-  asm volatile("cp.async.wait_all;\n" ::: "memory");
-  __syncthreads();
-  if (skip) return;
-  frag_neg(f);
-  frag_mma(f, As, Bs, PB);
-  frag_neg(f);
-  frag_store(f, C, ldc);
-}
-
 // y_k <- z_k W_k^T: y_c = sum_{t <= c} z_t W_ct (W lower triangular); 256 threads, four per
 // column c over interleaved t, combined in a fixed order.
 __device__ __forceinline__ void z_trsm(double* zp, int64_t ldz, const double* Wk, double* sm) {
@@ -624,34 +609,46 @@ __global__ void __launch_bounds__(256, 1) dag_factor_kernel(DagArgs a) {
   finish_tail(a, sm);
 }
 
-// Pool CTAs: tickets in list-schedule order (dag_plan).
+// Pool CTAs: tickets in list-schedule order (dag_plan). A GEMM task takes the CTA's next
+// ticket while its own operands are landing; if that is a GEMM too and its two operand tiles
+// are already final (a non-blocking look at their counters), their staging is issued at once
+// into the other buffer pair and lands during this task's products. The next task's C tile
+// version is waited for when it starts; nothing waits on the next ticket before the current
+// task is published, so the ticket order stays deadlock free.
 __device__ void pool_cta(const DagArgs& a, int* st, int* zs, double* sm) {
-  __shared__ int s_task, s_ok;
+  __shared__ int s_task, s_ok, s_pre;
   unsigned long long t_grab = 0;
-  double* As = sm;
-  double* Bs = sm + PB * LDS;
+  auto stf = [&](int r, int c) { return st + (r * a.nt + c) * kPad; };
+  int t = 0, b = 0;
+  bool have = false, pre = false;  // have: ticket t already taken; pre: its operands in flight into pair b
   for (;;) {
-    if (threadIdx.x == 0) {
-      s_task = atomicAdd(a.sync, 1);
-      if (a.trace) t_grab = gtimer();
+    if (!have) {
+      if (threadIdx.x == 0) {
+        s_task = atomicAdd(a.sync, 1);
+        if (a.trace) t_grab = gtimer();
+      }
+      __syncthreads();
+      t = s_task;
+      pre = false;
     }
-    __syncthreads();
-    const int t = s_task;
+    have = false;
     if (t >= a.ntasks) return;
     const int4 tk = a.tasks[t];
     const int type = tk.x, i = tk.y, j = tk.z, k = tk.w;
+    double* As = sm + 2 * b * PB * LDS;
+    double* Bs = As + PB * LDS;
     if (threadIdx.x == 0) {
       bool ok = true;
       switch (type) {
-        case kTrsm: ok = wait_ge(st + (k * a.nt + k) * kPad, k + 2, a.info) && wait_ge(st + (i * a.nt + k) * kPad, k + 1, a.info); break;
+        case kTrsm: ok = wait_ge(stf(k, k), k + 2, a.info) && wait_ge(stf(i, k), k + 1, a.info); break;
         case kGemm:
-          ok = wait_ge(st + (i * a.nt + k) * kPad, k + 2, a.info) && wait_ge(st + (j * a.nt + k) * kPad, k + 2, a.info) &&
-               wait_ge(st + (i * a.nt + j) * kPad, k + 1, a.info);
+          ok = (pre || (wait_ge(stf(i, k), k + 2, a.info) && wait_ge(stf(j, k), k + 2, a.info))) &&
+               wait_ge(stf(i, j), k + 1, a.info);
           break;
-        case kZTrsm: ok = wait_ge(st + (k * a.nt + k) * kPad, k + 2, a.info) && wait_ge(zs + k * kPad, k + 1, a.info); break;
+        case kZTrsm: ok = wait_ge(stf(k, k), k + 2, a.info) && wait_ge(zs + k * kPad, k + 1, a.info); break;
         case kGen: break;
         default:
-          ok = wait_ge(zs + k * kPad, k + 2, a.info) && wait_ge(st + (j * a.nt + k) * kPad, k + 2, a.info) &&
+          ok = wait_ge(zs + k * kPad, k + 2, a.info) && wait_ge(stf(j, k), k + 2, a.info) &&
                wait_ge(zs + j * kPad, k + 1, a.info);
           break;
       }
@@ -663,7 +660,10 @@ __device__ void pool_cta(const DagArgs& a, int* st, int* zs, double* sm) {
       }
     }
     __syncthreads();
-    if (!s_ok) return;  // a pivot failed: ENOTPD, nothing later matters
+    if (!s_ok) {  // a pivot failed: ENOTPD, nothing later matters
+      asm volatile("cp.async.wait_all;\n" ::: "memory");
+      return;
+    }
     int* flag;
     int64_t ld, ld2;
     switch (type) {
@@ -671,23 +671,67 @@ __device__ void pool_cta(const DagArgs& a, int* st, int* zs, double* sm) {
         double* Aik = tile_ptr(a, i, k, ld);
         stage_tile(Bs, a.W + (size_t)k * PB * PB, PB);
         tile_trsm(Aik, ld, Bs, As);
-        flag = st + (i * a.nt + k) * kPad;
+        flag = stf(i, k);
         break;
       }
       case kGemm: {
-        int64_t ldi, ldj;
         double* Aij = tile_ptr(a, i, j, ld);
-        stage_tile(As, tile_ptr(a, i, k, ldi), ldi);
-        if (i != j) stage_tile(Bs, tile_ptr(a, j, k, ldj), ldj);
-        tile_update(Aij, ld, As, i != j ? Bs : As, i == j);
-        flag = st + (i * a.nt + j) * kPad;
+        if (!pre) {
+          int64_t ldi, ldj;
+          stage_tile(As, tile_ptr(a, i, k, ldi), ldi);
+          if (i != j) stage_tile(Bs, tile_ptr(a, j, k, ldj), ldj);
+        }
+        // C -= A B^T; diagonal tile (A == B): the warp tiles above the diagonal are skipped.
+        // The C fragments load, and the next ticket is taken, while the operands land.
+        const bool skip = i == j && frag_upper();
+        Frag f;
+        if (!skip) frag_load(f, Aij, ld);
+        if (threadIdx.x == 0) {
+          const int tn = atomicAdd(a.sync, 1);
+          if (a.trace) t_grab = gtimer();
+          int p = 0;
+          if (tn < a.ntasks) {
+            const int4 n4 = a.tasks[tn];
+            p = n4.x == kGemm && ld_acquire(stf(n4.y, n4.w)) >= n4.w + 2 && ld_acquire(stf(n4.z, n4.w)) >= n4.w + 2;
+          }
+          s_task = tn;
+          s_pre = p;
+        }
+        __syncthreads();
+        const int nb = b ^ 1;
+        if (s_pre) {  // the next GEMM's operands into the other pair, one cp.async group
+          const int4 n4 = a.tasks[s_task];
+          double* An = sm + 2 * nb * PB * LDS;
+          int64_t ldi, ldj;
+          const double* src_a = tile_ptr(a, n4.y, n4.w, ldi);
+          const double* src_b = n4.y != n4.z ? tile_ptr(a, n4.z, n4.w, ldj) : nullptr;
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int idx = threadIdx.x + 256 * u, r2 = idx & 31, c = idx >> 5;
+            cp_async16(An + c * LDS + 2 * r2, src_a + (int64_t)c * ldi + 2 * r2);
+            if (src_b) cp_async16(An + PB * LDS + c * LDS + 2 * r2, src_b + (int64_t)c * ldj + 2 * r2);
+          }
+          asm volatile("cp.async.commit_group;\n" ::: "memory");
+          asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+        } else {
+          asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+        }
+        __syncthreads();
+        if (!skip) {
+          frag_neg(f);
+          frag_mma(f, As, i != j ? Bs : As, PB);
+          frag_neg(f);
+          frag_store(f, Aij, ld);
+        }
+        have = true;
+        flag = stf(i, j);
         break;
       }
       case kGen: {
         if (i < a.nt) {
           double* T = tile_ptr(a, i, j, ld);
           if (a.gen.generate) gen_tile(a, T, ld, i + a.t0, j + a.t0, sm);
-          flag = st + (i * a.nt + j) * kPad;
+          flag = stf(i, j);
         } else {
           double* zj = zseg_ptr(a, j, ld);
           if (a.gen.generate && threadIdx.x < PB) {
@@ -719,6 +763,13 @@ __device__ void pool_cta(const DagArgs& a, int* st, int* zs, double* sm) {
       __threadfence();
       st_release(flag, type == kGen ? 1 : k + 2);
       if (a.trace) a.trace[4 * t + 3] = gtimer();
+    }
+    if (have) {
+      t = s_task;
+      pre = s_pre;
+      b = pre ? b ^ 1 : 0;
+    } else {
+      b = 0;
     }
   }
 }
