@@ -267,11 +267,18 @@ exageo_status set_offsets(exageo_ctx* c, RankState& R) {
 // ---------------------------------------------------------------------------- tile-task executor
 // The whole factorization as one persistent kernel over the 64 x 64 tile DAG (dag.cu): used
 // where the stream schedule is bound by its critical path and launch count (small n).
-constexpr int64_t kTileTasksAutoN = 3200;
+// Automatic crossover (tools/tile_tasks_timing.py); EXAGEO_TILE_TASKS_N overrides it.
+int64_t tile_tasks_auto_n() {
+  static const int64_t v = [] {
+    const char* e = getenv("EXAGEO_TILE_TASKS_N");
+    return e ? (int64_t)atoll(e) : (int64_t)3200;
+  }();
+  return v;
+}
 
 bool tile_tasks_eligible(const exageo_ctx* c, int64_t n) {
   if (c->tile_tasks < 0 || c->world > 1 || c->virt || c->ind > 0 || c->comm) return false;
-  return c->tile_tasks > 0 || n <= kTileTasksAutoN;
+  return c->tile_tasks > 0 || n <= tile_tasks_auto_n();
 }
 
 // Tail hand-off: when the stream schedule runs a single-rank factorization, its last panels

@@ -89,7 +89,7 @@ struct exageo_ctx {
   cudaEvent_t ev_wait = nullptr;  // exageo_stream_wait
   // tile-task executor (dag.cu; exageo_opts.tile_tasks): the whole factorization of a
   // single-rank context as one persistent kernel running the 64 x 64 tile DAG
-  int tile_tasks = 0;          // 0 automatic (n <= kTileTasksAutoN), 1 always when eligible, -1 never
+  int tile_tasks = 0;          // 0 automatic (n <= tile_tasks_auto_n()), 1 always when eligible, -1 never
   int dag_nt = 0, dag_ntasks = 0, dag_nproc = 0;  // plan of the uploaded task list
   int dag_t0 = 0, dag_plan_t0 = -1;  // first 64-block column of the executor run (tail hand-off)
   int4* dag_tasks = nullptr;
