@@ -78,9 +78,13 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
   asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+// Publishing a tile: the CTA's stores, a barrier, then one thread's st.release.gpu (a release
+// pattern, cumulative over what the barrier ordered before it -- CUTLASS's barrier does the same
+// with fence.acq_rel + a relaxed red); no fence.sc (__threadfence) on the critical path.
 __device__ __forceinline__ void st_release(int* p, int v) {
   asm volatile("st.release.gpu.global.b32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
 }
+__device__ __forceinline__ void fence_acq_rel() { asm volatile("fence.acq_rel.gpu;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async16(double* s, const double* g) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(s);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(g) : "memory");
@@ -331,7 +335,7 @@ __device__ __forceinline__ bool wait_ge(const int* f, int v, const int* info) {
       if (++spins > 4) __nanosleep(40);
     }
   }
-  __threadfence();
+  fence_acq_rel();  // acquire: the relaxed (volatile) polls, then this fence
   return true;
 }
 
@@ -367,6 +371,7 @@ struct ChainPrefetch {
     int done = st[0];
     if (K > 0 && done != 3) {
       const int c1 = __shfl_sync(0xffffffffu, st[1], 0), c2 = __shfl_sync(0xffffffffu, st[2], 0);
+      if ((!(done & 1) && c1 >= need) || (!(done & 2) && c2 >= need)) __syncwarp();  // after lane 0's acquire loads
       if (!(done & 1) && c1 >= need) {
         stage_tile_warp(X, A1, ld1);
         done |= 1;
@@ -378,8 +383,8 @@ struct ChainPrefetch {
       st[0] = done;
     }
     if (K < 4 && done != 3 && lane == 0) {  // loads for the next look (in flight until then)
-      st[1] = *(volatile const int*)f1;
-      st[2] = *(volatile const int*)f2;
+      st[1] = ld_acquire(f1);
+      st[2] = ld_acquire(f2);
     }
     if (K == 4 && lane == 0) *issued = done;
   }
@@ -403,10 +408,7 @@ __device__ void chain_cta(const DagArgs& a, int* st, double* sm) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   auto stf = [&](int i, int j) { return st + (i * a.nt + j) * kPad; };
   auto release_by = [&](int w, int* f, int v) {  // after a barrier: one lane of warp w publishes
-    if (warp == w && lane == 0) {
-      __threadfence();
-      st_release(f, v);
-    }
+    if (warp == w && lane == 0) st_release(f, v);
   };
   auto rec = [&](int slot, unsigned long long t0, unsigned long long t1) {
     if (a.trace && threadIdx.x == 0) {
@@ -760,7 +762,6 @@ __device__ void pool_cta(const DagArgs& a, int* st, int* zs, double* sm) {
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-      __threadfence();
       st_release(flag, type == kGen ? 1 : k + 2);
       if (a.trace) a.trace[4 * t + 3] = gtimer();
     }
