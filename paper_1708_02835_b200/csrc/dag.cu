@@ -41,7 +41,15 @@ namespace {
 
 #include "potrf64.cuh"
 #ifdef EXAGEO_POTRF_TRACE  // development: the chain's K2 strip stamps of step 6 (tools/chain_k2_trace.py)
-__device__ long long g_potrf_snap[64];
+__device__ long long g_potrf_snap[80];  // [64..]: chain TRSM / SYRK phase stamps of step 6
+#define CTRACE(k, i)                                                      \
+  do {                                                                    \
+    if ((k) == 6 && threadIdx.x == 0) g_potrf_snap[64 + (i)] = clock64(); \
+  } while (0)
+#else
+#define CTRACE(k, i) \
+  do {               \
+  } while (0)
 #endif
 
 constexpr int LDS = PB + 4;  // shared leading dimension of staged tiles (4 mod 16 doubles)
@@ -464,6 +472,7 @@ __device__ void chain_cta(const DagArgs& a, int* st, double* sm) {
     rec(3 * k, t0, t0);
     if (last) break;
     // TRSM(k+1, k): L_{k+1,k} = A_{k+1,k} W_k^T
+    CTRACE(k, 0);
     const unsigned long long t2 = a.trace ? gtimer() : 0;
     const int issued = s_issued;
     if (warp == 7) asm volatile("cp.async.wait_all;\n" ::: "memory");
@@ -477,12 +486,16 @@ __device__ void chain_cta(const DagArgs& a, int* st, double* sm) {
     __syncthreads();
     const unsigned long long t3 = a.trace ? gtimer() : 0;
     Frag f;
+    CTRACE(k, 1);
     frag_zero(f);
     frag_mma(f, X, Ws, frag_c0() + 16);
+    CTRACE(k, 2);
     __syncthreads();  // every warp has read X
+    CTRACE(k, 3);
     frag_store(f, Ab, ldb);
     frag_store(f, X, LDS);
     __syncthreads();
+    CTRACE(k, 4);
     release_by(4, stf(k + 1, k), k + 2);  // warp 4 has no SYRK block
     rec(3 * k + 1, t2, t3);
     // SYRK(k+1, k+1, k): A_{k+1,k+1} -= L_{k+1,k} L_{k+1,k}^T into the body's input block As
@@ -495,6 +508,7 @@ __device__ void chain_cta(const DagArgs& a, int* st, double* sm) {
       asm volatile("cp.async.wait_all;\n" ::: "memory");
       __syncthreads();
     }
+    CTRACE(k, 5);
     const unsigned long long t5 = a.trace ? gtimer() : 0;
     // six 32 x 16 blocks hold the lower triangle; warps 4 and 6 (no block of their own) take the
     // upper half of the K range of warps 5 and 7's blocks (32, 48) and (32, 32), so each of the
@@ -520,6 +534,7 @@ __device__ void chain_cta(const DagArgs& a, int* st, double* sm) {
         frag_mma(f, X, X, (warp == 5 || warp == 7) ? 32 : PB);
       }
       __syncthreads();
+      CTRACE(k, 6);
       if (warp == 5 || warp == 7) {
         const double* pp = part + (warp == 5 ? 0 : 512) + lane * 16;
 #pragma unroll
@@ -536,6 +551,7 @@ __device__ void chain_cta(const DagArgs& a, int* st, double* sm) {
       }
     }
     __syncthreads();
+    CTRACE(k, 7);
     rec(3 * k + 2, t4, t5);
   }
 }
@@ -939,6 +955,6 @@ void dag_args_with_theta(const void* args, const MaternConsts& mc, std::vector<c
 
 #ifdef EXAGEO_POTRF_TRACE
 extern "C" int exageo_dbg_chain_potrf_trace(long long* out) {
-  return (int)cudaMemcpyFromSymbol(out, exageo::g_potrf_snap, 64 * sizeof(long long));
+  return (int)cudaMemcpyFromSymbol(out, exageo::g_potrf_snap, 80 * sizeof(long long));
 }
 #endif
