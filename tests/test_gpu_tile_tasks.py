@@ -178,3 +178,28 @@ def test_tile_tasks_fuzz_against_stream_schedule():
             assert again.loglik == a.loglik, (n, theta)
             scale = max(abs(b.loglik), 0.5 * abs(b.logdet), 0.5 * b.quad, 0.5 * n * 1.8378770664093453)
             assert abs(a.loglik - b.loglik) <= 1e-10 * scale, (n, theta, a.loglik, b.loglik)
+
+
+@pytest.mark.parametrize("n,reps", [(1000, 40), (3200, 12)])
+def test_tile_tasks_repeat_bitwise(n, reps):
+    """Many executor runs with two alternating theta (racing CTAs; tiles published by a barrier
+    plus st.release and acquired by relaxed polls plus fence.acq_rel; the pool's early ticket and
+    operand prefetch; the chain's prefetch hook): every run reproduces its theta's first result
+    bit for bit -- l, logdet, quad and a sample of factor entries -- so no task ever read a tile
+    before its producer published it, nor a stale version from the other theta's run."""
+    x, y = ex.gen_locations(n, 21)
+    z = si.normals(n, 22)
+    thetas = [(1.0, 0.1, 0.5), (1.4, 0.05, 1.1)]
+    rows = np.random.default_rng(n).integers(0, n, 300)
+    cols = np.minimum(rows, np.random.default_rng(n + 7).integers(0, n, 300))
+    with ex.Context(device=0, tile_tasks=1, graphs=-1) as c:
+        ref = {}
+        for th in thetas:
+            r = c.loglik(x, y, z, th)
+            ref[th] = ((r.loglik, r.logdet, r.quad), c.read_entries(rows, cols))
+        for it in range(reps):
+            th = thetas[it % 2]
+            r = c.loglik(x, y, z, th)
+            assert (r.loglik, r.logdet, r.quad) == ref[th][0], (it, th)
+            if it % 4 < 2:
+                np.testing.assert_array_equal(c.read_entries(rows, cols), ref[th][1])
