@@ -1,6 +1,7 @@
 """Per-step timeline of the stream schedule at one n (env EXAGEO_U2_TRACE): each bulk trailing
 update U2(k)'s duration and the gap before it (time the trailing update waited for the panel
-chain F(k+1) / U1(k)). Usage: u2_trace.py n [nb]"""
+chain F(k+1) / U1(k)). Usage: u2_trace.py n [nb] [tile_tasks] (default -1: no executor tail; 0: the
+automatic tail hand-off, whose time is then part of "after last U2")"""
 import os
 import sys
 import tempfile
@@ -8,6 +9,7 @@ import tempfile
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 n = int(sys.argv[1])
 nb = int(sys.argv[2]) if len(sys.argv) > 2 else 0
+tt = int(sys.argv[3]) if len(sys.argv) > 3 else -1
 path = os.path.join(tempfile.gettempdir(), f"u2_{n}_{nb}.txt")
 if os.path.exists(path):
     os.remove(path)
@@ -20,7 +22,7 @@ import synth_inputs as si  # noqa: E402
 x, y = ex.gen_locations(n, 1)
 z = si.normals(n, 2)
 X, Y, Z = (torch.from_numpy(a).cuda() for a in (x, y, z))
-with ex.Context(device=0, nb=nb, graphs=-1, tile_tasks=-1) as c:
+with ex.Context(device=0, nb=nb, graphs=-1, tile_tasks=tt) as c:
     for _ in range(3):
         r = c.loglik_dev(X, Y, Z, (1.0, 0.1, 0.5))
 blocks = open(path).read().split("# ")[1:]
