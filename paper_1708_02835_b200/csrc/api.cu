@@ -425,7 +425,21 @@ double* w_block(RankState& R, int k, int sb) {
 // Factor local panel k on its diagonal rank (left-looking over PB-wide column blocks) on s:
 // the diagonal tile is the top of the local panel, every row below (the rank's other tile rows
 // of column k and the z row block, if stored here) gets the panel update and the TRSM.
+// Right-looking inside the panel: after block sb's POTRF and TRSM one wide K = 64 update of all
+// later column blocks, instead of each block's left-looking update with K = 64 sb on M / 64
+// CTAs. Shorter panel chain where it is the critical path (n <= 24000: 8192 7.97 -> 7.64 ms,
+// 10k 13.02 -> 12.72, 20k 83.6 -> 82.6); above, its wide launches take SMs from the concurrent
+// bulk update (100k 9.26 -> 9.36 s), so the left-looking form stays. EXAGEO_PANEL_RIGHT=0/1 forces.
+bool panel_right_looking(int64_t n) {
+  static const int forced = [] {
+    const char* e = getenv("EXAGEO_PANEL_RIGHT");
+    return e ? (atoi(e) != 0 ? 1 : 0) : -1;
+  }();
+  return forced >= 0 ? forced == 1 : n <= 24000;
+}
+
 exageo_status factor_panel(exageo_ctx* c, RankState& R, int k, cudaStream_t s) {
+  const bool right = panel_right_looking(R.L.n);
   const Layout& L = R.L;
   const int nsub = L.nb / PB;
   double* Pk = R.ws + L.off(k);
@@ -444,7 +458,7 @@ exageo_status factor_panel(exageo_ctx* c, RankState& R, int k, cudaStream_t s) {
     // dependent launch (each launches while its predecessor runs and waits on the device)
     const bool pdl = L.n <= 32768;
     const bool first = sb == 0;  // follows U1 / an event wait: ordinary launch
-    if (sb > 0) {
+    if (sb > 0 && !right) {
       launch_gemm_panel(ldk - c0, PB, (int)c0, Pk + c0, ldk, Pk + c0, ldk, Pk + c0 * ldk + c0, ldk, true, R.info, s,
                         pdl);
       c->kernels += 1;
@@ -455,6 +469,14 @@ exageo_status factor_panel(exageo_ctx* c, RankState& R, int k, cudaStream_t s) {
     double* below = Pk + c0 * ldk + c0 + PB;
     launch_gemm_panel(ldk - c0 - PB, PB, PB, below, ldk, W, PB, below, ldk, false, R.info, s, pdl);
     c->kernels += 2;
+    if (right) {  // the panel's later column blocks (inside n) -= L(:, block sb) L(rows of those blocks, block sb)^T
+      const int64_t cols_left = std::min<int64_t>(L.nb, L.n - (int64_t)k * L.nb) - (c0 + PB);
+      if (cols_left > 0) {
+        launch_gemm_panel(ldk - c0 - PB, (int)((cols_left + PB - 1) / PB * PB), PB, below, ldk, below, ldk,
+                          Pk + (c0 + PB) * ldk + c0 + PB, ldk, true, R.info, s, pdl);
+        c->kernels += 1;
+      }
+    }
   }
   return EXAGEO_OK;
 }
