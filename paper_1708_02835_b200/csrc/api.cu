@@ -422,7 +422,8 @@ double* w_block(RankState& R, int k, int sb) {
   return R.lkk[k & 1] + (size_t)R.L.nb * R.L.nb + (size_t)sb * PB * PB;
 }
 
-// Factor local panel k on its diagonal rank (left-looking over PB-wide column blocks) on s:
+// Factor local panel k on its diagonal rank (over PB-wide column blocks, right- or left-looking:
+// panel_right_looking) on s:
 // the diagonal tile is the top of the local panel, every row below (the rank's other tile rows
 // of column k and the z row block, if stored here) gets the panel update and the TRSM.
 // Right-looking inside the panel: after block sb's POTRF and TRSM one wide K = 64 update of all
