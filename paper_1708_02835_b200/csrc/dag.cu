@@ -347,6 +347,23 @@ __device__ __forceinline__ bool wait_ge(const int* f, int v, const int* info) {
   return true;
 }
 
+// Up to three counters at once (f2 / f3 may be null): the loads of one poll are issued together,
+// so a task whose inputs are all published pays one L2 round trip, not one per input.
+__device__ __forceinline__ bool wait_ge3(const int* f1, int v1, const int* f2, int v2, const int* f3, int v3,
+                                         const int* info) {
+  int spins = 0;
+  for (;;) {
+    const int a = *(volatile const int*)f1;
+    const int b = f2 ? *(volatile const int*)f2 : v2;
+    const int c = f3 ? *(volatile const int*)f3 : v3;
+    if (a >= v1 && b >= v2 && c >= v3) break;
+    if (*(volatile const int*)info != 0) return false;
+    if (++spins > 4) __nanosleep(40);
+  }
+  fence_acq_rel();
+  return true;
+}
+
 // Warp-level stage of a 64 x 64 tile (one warp issues all 512 16-byte copies; committed).
 __device__ __forceinline__ void stage_tile_warp(double* dst, const double* src, int64_t ld) {
   const int lane = threadIdx.x & 31;
@@ -658,17 +675,14 @@ __device__ void pool_cta(const DagArgs& a, int* st, int* zs, double* sm) {
     if (threadIdx.x == 0) {
       bool ok = true;
       switch (type) {
-        case kTrsm: ok = wait_ge(stf(k, k), k + 2, a.info) && wait_ge(stf(i, k), k + 1, a.info); break;
+        case kTrsm: ok = wait_ge3(stf(k, k), k + 2, stf(i, k), k + 1, nullptr, 0, a.info); break;
         case kGemm:
-          ok = (pre || (wait_ge(stf(i, k), k + 2, a.info) && wait_ge(stf(j, k), k + 2, a.info))) &&
-               wait_ge(stf(i, j), k + 1, a.info);
+          ok = pre ? wait_ge(stf(i, j), k + 1, a.info)
+                   : wait_ge3(stf(i, k), k + 2, stf(j, k), k + 2, stf(i, j), k + 1, a.info);
           break;
-        case kZTrsm: ok = wait_ge(stf(k, k), k + 2, a.info) && wait_ge(zs + k * kPad, k + 1, a.info); break;
+        case kZTrsm: ok = wait_ge3(stf(k, k), k + 2, zs + k * kPad, k + 1, nullptr, 0, a.info); break;
         case kGen: break;
-        default:
-          ok = wait_ge(zs + k * kPad, k + 2, a.info) && wait_ge(stf(j, k), k + 2, a.info) &&
-               wait_ge(zs + j * kPad, k + 1, a.info);
-          break;
+        default: ok = wait_ge3(zs + k * kPad, k + 2, stf(j, k), k + 2, zs + j * kPad, k + 1, a.info); break;
       }
       s_ok = ok;
       if (a.trace) {
