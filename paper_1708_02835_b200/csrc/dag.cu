@@ -389,29 +389,54 @@ struct ChainPrefetch {
   double* Y;
   const double* A2;
   int64_t ld2;
-  int* issued;  // shared: written at K = 4 for the rest of the CTA
-  int* st;      // registers of warp 7: {issued bits, counter 1, counter 2} (lane 0 loads)
+  int* claim;  // shared: bits of the tiles whose staging is issued (1 X, 2 Y); claimed by atomicOr
+  int* st;     // registers of warp 7: {unused, counter 1, counter 2} (lane 0 loads)
+  // warp 7 at the start of helper phase K = 1..3: counters loaded at K - 1 are looked at; a
+  // ready tile is claimed and staged by the warp. K = 4 (the W tail) stages nothing: the
+  // factor warps, idle by then, look again (after_strips).
   __device__ __forceinline__ void operator()(int K) const {
     const int lane = threadIdx.x & 31;
-    int done = st[0];
-    if (K > 0 && done != 3) {
-      const int c1 = __shfl_sync(0xffffffffu, st[1], 0), c2 = __shfl_sync(0xffffffffu, st[2], 0);
-      if ((!(done & 1) && c1 >= need) || (!(done & 2) && c2 >= need)) __syncwarp();  // after lane 0's acquire loads
-      if (!(done & 1) && c1 >= need) {
-        stage_tile_warp(X, A1, ld1);
-        done |= 1;
+    if (K > 0 && K < 4 && *(volatile int*)claim != 3) {
+      int win = 0;
+      if (lane == 0) {
+        const int want = (st[1] >= need ? 1 : 0) | (st[2] >= need ? 2 : 0);
+        if (want) win = want & ~atomicOr(claim, want);
       }
-      if (!(done & 2) && c2 >= need) {
-        stage_tile_warp(Y, A2, ld2);
-        done |= 2;
-      }
-      st[0] = done;
+      win = __shfl_sync(0xffffffffu, win, 0);
+      if (win) __syncwarp();  // after lane 0's acquire loads
+      if (win & 1) stage_tile_warp(X, A1, ld1);
+      if (win & 2) stage_tile_warp(Y, A2, ld2);
     }
-    if (K < 4 && done != 3 && lane == 0) {  // loads for the next look (in flight until then)
+    if (K < 3 && lane == 0 && *(volatile int*)claim != 3) {  // loads for the next look
       st[1] = ld_acquire(f1);
       st[2] = ld_acquire(f2);
     }
-    if (K == 4 && lane == 0) *issued = done;
+  }
+  // the factor warps after their last strip (they wait for the W tail otherwise): a fresh look,
+  // and the staging of any ready, unclaimed tile spread over their 96 threads
+  __device__ __forceinline__ void after_strips() const {
+    __shared__ int s_win;
+    if (threadIdx.x == 0) {
+      int win = 0;
+      if (*(volatile int*)claim != 3) {
+        const int want = (ld_acquire(f1) >= need ? 1 : 0) | (ld_acquire(f2) >= need ? 2 : 0);
+        if (want) win = want & ~atomicOr(claim, want);
+      }
+      s_win = win;
+    }
+    named_sync(6, 32 * NFW);
+    const int win = s_win;
+    for (int t = 0; t < 2; ++t) {
+      if (!(win & (1 << t))) continue;
+      double* dst = t ? Y : X;
+      const double* src = t ? A2 : A1;
+      const int64_t ld = t ? ld2 : ld1;
+      for (int idx = threadIdx.x; idx < 2048; idx += 32 * NFW) {
+        const int r2 = idx & 31, c = idx >> 5;
+        cp_async16(dst + c * LDS + 2 * r2, src + (int64_t)c * ld + 2 * r2);
+      }
+    }
+    if (win) asm volatile("cp.async.commit_group;\n" ::: "memory");
   }
 };
 
@@ -425,7 +450,7 @@ struct ChainPrefetch {
 // this CTA only (POTRF(k+1) publishes the tile's next version).
 // Trace records (optional): ntasks + 3k + {0, 1, 2} for POTRF / TRSM / SYRK of step k.
 __device__ void chain_cta(const DagArgs& a, int* st, double* sm) {
-  __shared__ int s_ok, s_issued;
+  __shared__ int s_ok, s_claim;
   double* X = sm + kPotrfSmemDoubles;  // A_{k+1,k}, then L_{k+1,k}
   double* Y = X + PB * LDS;            // A_{k+1,k+1}
   const double* Ws = sm + PB * LDA2;   // K2 body's W = L_kk^{-1} (ld LDA2 = LDS)
@@ -468,9 +493,10 @@ __device__ void chain_cta(const DagArgs& a, int* st, double* sm) {
     const unsigned long long t0 = a.trace ? gtimer() : 0;
     // POTRF(k): the block is in shared memory (A_00 staged above, else the SYRK(k, k, k-1) result,
     // whose input version k was waited for)
-    int hst[3] = {last ? 3 : 0, 0, 0};
+    int hst[3] = {0, 0, 0};
+    if (threadIdx.x == 0) s_claim = last ? 3 : 0;  // the body starts with a barrier
     ChainPrefetch hook{last ? nullptr : stf(k + 1, k), last ? nullptr : stf(k + 1, k + 1), k + 1, X, Ab, ldb, Y, Ad, ldd,
-                       &s_issued, hst};
+                       &s_claim, hst};
     double* Wk = a.W + (size_t)k * PB * PB;
     const int gk = a.t0 + k;  // global 64-block column
     double* slot = a.slots + gk;  // one log-det slot per 64-block column (panel gk / nsub, block gk % nsub)
@@ -491,8 +517,8 @@ __device__ void chain_cta(const DagArgs& a, int* st, double* sm) {
     // TRSM(k+1, k): L_{k+1,k} = A_{k+1,k} W_k^T
     CTRACE(k, 0);
     const unsigned long long t2 = a.trace ? gtimer() : 0;
-    const int issued = s_issued;
-    if (warp == 7) asm volatile("cp.async.wait_all;\n" ::: "memory");
+    const int issued = s_claim;
+    asm volatile("cp.async.wait_all;\n" ::: "memory");  // staging issued inside the body (warp 7, factor warps)
     if (!(issued & 1)) {
       if (threadIdx.x == 0) s_ok = wait_ge(stf(k + 1, k), k + 1, a.info);
       __syncthreads();

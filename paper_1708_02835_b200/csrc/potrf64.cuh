@@ -238,6 +238,7 @@ __device__ __forceinline__ int factor_strip(const int K, double* As, double* dv,
 // only its real strips.
 struct NoHook {
   __device__ __forceinline__ void operator()(int) const {}
+  __device__ __forceinline__ void after_strips() const {}  // factor warps, after their last strip
 };
 
 template <bool kFromSmem = false, class Hook = NoHook>
@@ -281,6 +282,7 @@ __device__ __forceinline__ bool potrf64_body(double* __restrict__ a, int64_t lda
       named_arrive(1 + K, 256);
     }
     if (tid == 0 && first >= 0) badj = first;
+    hook.after_strips();
   } else {
     constexpr int NH = 256 - 32 * NFW;  // helper threads
 #pragma unroll 1
