@@ -391,11 +391,22 @@ struct ChainPrefetch {
   int64_t ld2;
   int* claim;  // shared: bits of the tiles whose staging is issued (1 X, 2 Y); claimed by atomicOr
   int* st;     // registers of warp 7: {unused, counter 1, counter 2} (lane 0 loads)
+  const DagArgs* pa;  // the next step's tile pointers, computed by warp 7 at K = 0 (idle then; the
+  int knext;          // integer work is ~1 us of latency on the chain otherwise): A_{k+2,k+1},
+  double** nptr;      // A_{k+2,k+2} and their ld into shared nptr[0..1] / nld[0..1]
+  int64_t* nld;
   // warp 7 at the start of helper phase K = 1..3: counters loaded at K - 1 are looked at; a
   // ready tile is claimed and staged by the warp. K = 4 (the W tail) stages nothing: the
   // factor warps, idle by then, look again (after_strips).
   __device__ __forceinline__ void operator()(int K) const {
     const int lane = threadIdx.x & 31;
+    if (K == 0 && lane == 0 && knext + 1 < pa->nt) {
+      int64_t l0, l1;
+      nptr[0] = tile_ptr(*pa, knext + 1, knext, l0);
+      nptr[1] = tile_ptr(*pa, knext + 1, knext + 1, l1);
+      nld[0] = l0;
+      nld[1] = l1;
+    }
     if (K > 0 && K < 4 && *(volatile int*)claim != 3) {
       int win = 0;
       if (lane == 0) {
@@ -484,19 +495,21 @@ __device__ void chain_cta(const DagArgs& a, int* st, double* sm) {
     __syncthreads();
   }
   rec(3 * (a.nt - 1) + 1, t_entry, t_entry);  // (the last step has no TRSM): kernel entry .. A_00 ready
+  __shared__ double* s_nptr[2];
+  __shared__ int64_t s_nld[2];
+  int64_t ld, ldb = 0, ldd = 0;  // this step's tiles: A_kk (= last step's A_{k,k}), A_{k+1,k}, A_{k+1,k+1}
+  double* Akk = tile_ptr(a, 0, 0, ld);
+  double* Ab = a.nt > 1 ? tile_ptr(a, 1, 0, ldb) : nullptr;
+  double* Ad = a.nt > 1 ? tile_ptr(a, 1, 1, ldd) : nullptr;
   for (int k = 0; k < a.nt; ++k) {
     const bool last = k + 1 == a.nt;
-    int64_t ld, ldb = 0, ldd = 0;
-    double* Akk = tile_ptr(a, k, k, ld);
-    double* Ab = last ? nullptr : tile_ptr(a, k + 1, k, ldb);
-    double* Ad = last ? nullptr : tile_ptr(a, k + 1, k + 1, ldd);
     const unsigned long long t0 = a.trace ? gtimer() : 0;
     // POTRF(k): the block is in shared memory (A_00 staged above, else the SYRK(k, k, k-1) result,
     // whose input version k was waited for)
     int hst[3] = {0, 0, 0};
     if (threadIdx.x == 0) s_claim = last ? 3 : 0;  // the body starts with a barrier
     ChainPrefetch hook{last ? nullptr : stf(k + 1, k), last ? nullptr : stf(k + 1, k + 1), k + 1, X, Ab, ldb, Y, Ad, ldd,
-                       &s_claim, hst};
+                       &s_claim, hst, &a, k + 1, s_nptr, s_nld};
     double* Wk = a.W + (size_t)k * PB * PB;
     const int gk = a.t0 + k;  // global 64-block column
     double* slot = a.slots + gk;  // one log-det slot per 64-block column (panel gk / nsub, block gk % nsub)
@@ -596,6 +609,14 @@ __device__ void chain_cta(const DagArgs& a, int* st, double* sm) {
     __syncthreads();
     CTRACE(k, 7);
     rec(3 * k + 2, t4, t5);
+    Akk = Ad;  // the next step's tiles (s_nptr written by warp 7 inside this step's body)
+    ld = ldd;
+    if (k + 2 < a.nt) {
+      Ab = s_nptr[0];
+      ldb = s_nld[0];
+      Ad = s_nptr[1];
+      ldd = s_nld[1];
+    }
   }
 }
 

@@ -27,4 +27,5 @@ with ex.Context(device=0, tile_tasks=1, graphs=-1) as c:
     print("K0 cycles per pivot:", " ".join(str(v) for v in t[32:48]))
     c = t[64:72]
     print("chain TRSM/SYRK of step 6 (cycles from the body's end): staged %d, mma (warp 0) %d, barrier %d, "
-          "stored+barrier %d | SYRK staged %d, mma+barrier %d, stored+barrier %d" % tuple(v - c[0] for v in c[1:8]))
+          "stored+barrier %d | SYRK staged %d, mma+barrier %d, stored+barrier %d"
+          % tuple(v - c[0] for v in c[1:8]))
