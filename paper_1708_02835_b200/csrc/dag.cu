@@ -375,10 +375,11 @@ __device__ __forceinline__ void stage_tile_warp(double* dst, const double* src, 
   asm volatile("cp.async.commit_group;\n" ::: "memory");
 }
 
-// Prefetch hook of the chain CTA (runs on warp 7 inside POTRF(k), potrf64_body): polls the
-// version counters of A_{k+1,k} and A_{k+1,k+1} without blocking -- the counter values
-// loaded at strip K are looked at in strip K + 1 -- and issues the cp.async of each tile
-// into X / Y once the pool has finished it. Bits of *issued: 1 X, 2 Y.
+// Prefetch hook of the chain CTA inside POTRF(k) (potrf64_body): warp 7 polls the version
+// counters of A_{k+1,k} and A_{k+1,k+1} without blocking -- the values loaded at strip K are
+// looked at in strip K + 1 -- and issues the cp.async of each tile into X / Y once the pool
+// has finished it; after their last strip the factor warps take one more, fresh look
+// (after_strips). Each tile is claimed in *claim (bits 1 X, 2 Y) by whichever side stages it.
 struct ChainPrefetch {
   const int* f1;
   const int* f2;
