@@ -231,7 +231,9 @@ __device__ __forceinline__ int factor_strip(const int K, double* As, double* dv,
 // kFromSmem: the block is already in As (smem_p, ld LDA2; lower triangle and the diagonal 16 x 16
 // blocks are read) -- the tile-task chain CTA hands the SYRK result over in shared memory.
 // hook(K), K = 0..4, runs on warp 7 (a helper warp without block work) at the start of strip
-// K's helper phase (K = 4: after the last one): the chain CTA polls and prefetches the next tiles there. Returns false
+// K's helper phase (K = 4: after the last one), hook.after_strips() on the factor warps after
+// their last strip (idle until the W tail ends): the chain CTA polls and prefetches the next
+// step's tiles there and computes its tile pointers. Returns false
 // (uniformly) when a pivot failed (info written). nstrips (1..4): 16-column strips holding
 // columns < n; the others are identity padding (R12): not factored, L stays the generated
 // identity, W gets identity rows, log L_ii = 0 -- the ragged last block of a matrix costs
