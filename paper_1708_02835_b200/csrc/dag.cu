@@ -692,35 +692,52 @@ __global__ void __launch_bounds__(256, 1) dag_factor_kernel(DagArgs a) {
   finish_tail(a, sm);
 }
 
-// Pool CTAs: tickets in list-schedule order (dag_plan). A GEMM task takes the CTA's next
-// ticket while its own operands are landing; if that is a GEMM too and its two operand tiles
-// are already final (a non-blocking look at their counters), their staging is issued at once
-// into the other buffer pair and lands during this task's products. The next task's C tile
-// version is waited for when it starts; nothing waits on the next ticket before the current
-// task is published, so the ticket order stays deadlock free.
+// Pool CTAs: tickets in list-schedule order (dag_plan). With many tiles (nt >= kAhead2Nt: the
+// pool is the bottleneck) tickets are taken two ahead: while a CTA runs ticket t it already
+// holds the next one (descriptor loaded) and grabs the one after, so the atomic and the
+// descriptor load are off the task's path; with fewer (the chain is the bottleneck, and a held
+// ticket may be a task it waits for) one ahead: a GEMM task grabs its next ticket while its
+// operands land, other tasks after they publish. A GEMM task looks at its next
+// ticket while its own operands land: if that is a GEMM whose two operand tiles are already
+// final (a non-blocking look at their counters), their staging is issued at once into the
+// other buffer pair and lands during this task's products; the next task's C tile version is
+// waited for when it starts. A CTA runs its tickets in increasing order and never waits on a
+// later one before publishing the current task, so the ticket order stays deadlock free.
+constexpr int kAhead2Nt = 32;  // n >= 2048 (tools/tile_tasks_timing.py: 2400 681 -> 659 us, 3200 1308 -> 1249;
+                               // 1600 405 -> 413, so one ahead below)
 __device__ void pool_cta(const DagArgs& a, int* st, int* zs, double* sm) {
-  __shared__ int s_task, s_ok, s_pre;
-  unsigned long long t_grab = 0;
+  __shared__ int s_ok, s_pre, s_t[2];
+  __shared__ int4 s_tk[2];  // descriptors of the current and the next ticket
+  unsigned long long t_grab = 0, t_grab_n = 0, t_grab_nn = 0;
   auto stf = [&](int r, int c) { return st + (r * a.nt + c) * kPad; };
-  int t = 0, b = 0;
-  bool have = false, pre = false;  // have: ticket t already taken; pre: its operands in flight into pair b
-  for (;;) {
-    if (!have) {
-      if (threadIdx.x == 0) {
-        s_task = atomicAdd(a.sync, 1);
-        if (a.trace) t_grab = gtimer();
-      }
-      __syncthreads();
-      t = s_task;
-      pre = false;
+  const int4 none = make_int4(-1, 0, 0, 0);
+  const bool ahead2 = a.nt >= kAhead2Nt;
+  if (threadIdx.x == 0) {
+    const int t0 = atomicAdd(a.sync, 1);
+    if (a.trace) t_grab = gtimer();
+    s_t[0] = t0;
+    s_tk[0] = t0 < a.ntasks ? a.tasks[t0] : none;
+    if (ahead2) {
+      const int t1 = atomicAdd(a.sync, 1);
+      if (a.trace) t_grab_n = gtimer();
+      s_t[1] = t1;
+      s_tk[1] = t1 < a.ntasks ? a.tasks[t1] : none;
     }
-    have = false;
+  }
+  __syncthreads();
+  int b = 0;
+  bool pre = false;  // the operands of the current ticket are in flight into buffer pair b
+  for (;;) {
+    const int t = s_t[0];
     if (t >= a.ntasks) return;
-    const int4 tk = a.tasks[t];
+    const int4 tk = s_tk[0];
     const int type = tk.x, i = tk.y, j = tk.z, k = tk.w;
     double* As = sm + 2 * b * PB * LDS;
     double* Bs = As + PB * LDS;
+    int tnn = 0;       // thread 0: the ticket after next, grabbed now (the atomic's latency overlaps
+    int4 tknn = none;  // the input polls) and its descriptor (loaded after them, used at the end)
     if (threadIdx.x == 0) {
+      if (ahead2) tnn = atomicAdd(a.sync, 1);
       bool ok = true;
       switch (type) {
         case kTrsm: ok = wait_ge3(stf(k, k), k + 2, stf(i, k), k + 1, nullptr, 0, a.info); break;
@@ -733,10 +750,12 @@ __device__ void pool_cta(const DagArgs& a, int* st, int* zs, double* sm) {
         default: ok = wait_ge3(zs + k * kPad, k + 2, stf(j, k), k + 2, zs + j * kPad, k + 1, a.info); break;
       }
       s_ok = ok;
+      if (ahead2 && tnn < a.ntasks) tknn = a.tasks[tnn];
       if (a.trace) {
         a.trace[4 * t] = blockIdx.x;
         a.trace[4 * t + 1] = t_grab;
         a.trace[4 * t + 2] = gtimer();
+        t_grab_nn = gtimer();
       }
     }
     __syncthreads();
@@ -746,6 +765,7 @@ __device__ void pool_cta(const DagArgs& a, int* st, int* zs, double* sm) {
     }
     int* flag;
     int64_t ld, ld2;
+    int next_pre = 0;
     switch (type) {
       case kTrsm: {
         double* Aik = tile_ptr(a, i, k, ld);
@@ -762,25 +782,26 @@ __device__ void pool_cta(const DagArgs& a, int* st, int* zs, double* sm) {
           if (i != j) stage_tile(Bs, tile_ptr(a, j, k, ldj), ldj);
         }
         // C -= A B^T; diagonal tile (A == B): the warp tiles above the diagonal are skipped.
-        // The C fragments load, and the next ticket is taken, while the operands land.
+        // The C fragments load, and the next ticket is looked at, while the operands land.
         const bool skip = i == j && frag_upper();
         Frag f;
         if (!skip) frag_load(f, Aij, ld);
         if (threadIdx.x == 0) {
-          const int tn = atomicAdd(a.sync, 1);
-          if (a.trace) t_grab = gtimer();
-          int p = 0;
-          if (tn < a.ntasks) {
-            const int4 n4 = a.tasks[tn];
-            p = n4.x == kGemm && ld_acquire(stf(n4.y, n4.w)) >= n4.w + 2 && ld_acquire(stf(n4.z, n4.w)) >= n4.w + 2;
+          if (!ahead2) {  // one ahead: the next ticket now, while the operands land
+            const int t1 = atomicAdd(a.sync, 1);
+            if (a.trace) t_grab_n = gtimer();
+            s_t[1] = t1;
+            s_tk[1] = t1 < a.ntasks ? a.tasks[t1] : none;
           }
-          s_task = tn;
-          s_pre = p;
+          const int4 n4 = s_tk[1];
+          s_pre = s_t[1] < a.ntasks && n4.x == kGemm && ld_acquire(stf(n4.y, n4.w)) >= n4.w + 2 &&
+                  ld_acquire(stf(n4.z, n4.w)) >= n4.w + 2;
         }
         __syncthreads();
         const int nb = b ^ 1;
-        if (s_pre) {  // the next GEMM's operands into the other pair, one cp.async group
-          const int4 n4 = a.tasks[s_task];
+        next_pre = s_pre;
+        if (next_pre) {  // the next GEMM's operands into the other pair, one cp.async group
+          const int4 n4 = s_tk[1];
           double* An = sm + 2 * nb * PB * LDS;
           int64_t ldi, ldj;
           const double* src_a = tile_ptr(a, n4.y, n4.w, ldi);
@@ -803,7 +824,6 @@ __device__ void pool_cta(const DagArgs& a, int* st, int* zs, double* sm) {
           frag_neg(f);
           frag_store(f, Aij, ld);
         }
-        have = true;
         flag = stf(i, j);
         break;
       }
@@ -838,18 +858,27 @@ __device__ void pool_cta(const DagArgs& a, int* st, int* zs, double* sm) {
         break;
       }
     }
-    __syncthreads();
+    __syncthreads();  // every thread's stores issued; every thread has read s_tk / s_t / s_pre
     if (threadIdx.x == 0) {
       st_release(flag, type == kGen ? 1 : k + 2);
       if (a.trace) a.trace[4 * t + 3] = gtimer();
+      if (ahead2 || type == kGemm) {  // the held next ticket becomes current
+        s_t[0] = s_t[1];
+        s_tk[0] = s_tk[1];
+        s_t[1] = tnn;
+        s_tk[1] = tknn;
+        t_grab = t_grab_n;
+        t_grab_n = t_grab_nn;
+      } else {  // one ahead, after a task that held none: grab now
+        const int t0 = atomicAdd(a.sync, 1);
+        if (a.trace) t_grab = gtimer();
+        s_t[0] = t0;
+        s_tk[0] = t0 < a.ntasks ? a.tasks[t0] : none;
+      }
     }
-    if (have) {
-      t = s_task;
-      pre = s_pre;
-      b = pre ? b ^ 1 : 0;
-    } else {
-      b = 0;
-    }
+    __syncthreads();
+    pre = next_pre != 0;
+    b = pre ? b ^ 1 : 0;
   }
 }
 
